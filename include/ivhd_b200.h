@@ -1,0 +1,143 @@
+/*
+ * ivhd_b200.h — C ABI of the B200-native IVHD embedding loop.
+ *
+ * One context = one embedding run on one GPU (or one rank's shard of it).
+ * Plain pointers and sizes only; every host pointer is read/written
+ * synchronously before the call returns.  All functions return an
+ * ivhd_status; on failure ivhd_last_error(ctx) (or ivhd_global_error() when
+ * no context exists yet) holds a one-line message.
+ *
+ * The reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/ivhd/):
+ *
+ *   ivhd_create / ivhd_destroy      _Run.__init__ device state       engine.py:162-221
+ *   ivhd_set_graph                  _Run._build_edges (binary)       engine.py:225-262
+ *   ivhd_set_connections            ConnectionSet(...)               forces.py:20-50
+ *   ivhd_set_positions              init_layout result / observer    engine.py:124-129,214
+ *   ivhd_get_positions              RunResult.embedding.points       engine.py:413
+ *   ivhd_set_optimizer              make_optimizer                   optim.py:249-256
+ *   ivhd_set_step_size              _apply_mutation("b")             engine.py:424-432
+ *   ivhd_run                        the loop body, n times           engine.py:346-384
+ *   ivhd_compute_forces             compute_forces(..., with_stress) forces.py:139-181
+ *   ivhd_stress                     stress                           forces.py:78-83
+ *   ivhd_get_deltas                 EmbeddingState.deltas            engine.py:379
+ *   ivhd_snapshot / ivhd_restore    (new) device-side checkpoint     SURVEY.md §5 checkpoint row
+ *   ivhd_shard_* / ivhd_step_*      (new) vertex-range sharding
+ */
+#ifndef IVHD_B200_H
+#define IVHD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IVHD_ABI_VERSION 1
+
+enum ivhd_status {
+  IVHD_OK = 0,
+  IVHD_ERR_INVALID_ARG = 1, /* -> InvalidArgumentError / DimensionMismatchError */
+  IVHD_ERR_CUDA = 2,        /* CUDA runtime failure (message has the CUDA error) */
+  IVHD_ERR_DIVERGED = 3,    /* -> NumericalDivergenceError(iteration, state)    */
+  IVHD_ERR_STATE = 4        /* call order violated (e.g. run before set_graph)  */
+};
+
+enum ivhd_norm { IVHD_NORM_L2 = 0, IVHD_NORM_L1 = 1 };
+
+enum ivhd_optimizer_kind {
+  IVHD_OPT_FORCE_DIRECTED = 0,
+  IVHD_OPT_SGD = 1,
+  IVHD_OPT_MOMENTUM = 2,
+  IVHD_OPT_NESTEROV = 3,
+  IVHD_OPT_ADAM = 4,
+  IVHD_OPT_ADADELTA = 5
+};
+
+/* Mirrors IntegratorParams (optim.py:15-56) + OptimizerParams (optim.py:59-68).
+ * step = b for force-directed, alpha for sgd/momentum/nesterov/adam,
+ * scale for adadelta (optim.py:71-77 defaults already resolved by the host). */
+typedef struct ivhd_optimizer_params {
+  int32_t kind;        /* ivhd_optimizer_kind */
+  int32_t auto_adapt;  /* force-directed: self-adapting b with rollback  */
+  double step;         /* b / alpha / scale                               */
+  double a;            /* friction retention                              */
+  double tau;          /* adaption threshold (already tau_for(M))        */
+  double gamma1, gamma2;
+  double beta, gamma_v, gamma_s, rho, eps;
+} ivhd_optimizer_params;
+
+typedef struct ivhd_ctx ivhd_ctx;
+
+int ivhd_abi_version(void);
+const char* ivhd_global_error(void);
+
+/* stream: a cudaStream_t (as integer) to launch on, or 0 for a private one. */
+int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream);
+int ivhd_destroy(ivhd_ctx* ctx);
+const char* ivhd_last_error(const ivhd_ctx* ctx);
+
+/* Binary-mode connections of slot (0 = main set, 1 = RNN-filtered set):
+ * nn block (i, nn_ids[i*nn_stride + c]) for c < ncols, then rn block
+ * (i, rn_ids[i*rn + r]); nn pairs target 0 weight 1, rn pairs target 1
+ * weight c.  Builds the symmetrised CSR on the device. */
+int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_stride,
+                   int ncols, const int32_t* rn_ids, int rn);
+
+/* Generic connection set (edges (L,2) row-major).  targets/scale may be NULL
+ * (NULL targets = binary: 0 for nn, 1 for random pairs). */
+int ivhd_set_connections(ivhd_ctx* ctx, int slot, const int32_t* edges,
+                         const uint8_t* is_random, const double* targets,
+                         const double* scale, int64_t n_conn);
+
+int ivhd_set_positions(ivhd_ctx* ctx, const double* y);      /* (m, dim) */
+int ivhd_get_positions(ivhd_ctx* ctx, double* y_out);        /* (m, dim) */
+int ivhd_get_deltas(ivhd_ctx* ctx, double* d_out);           /* (m, dim) */
+int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p); /* resets state */
+int ivhd_set_step_size(ivhd_ctx* ctx, double step);
+int ivhd_get_step_size(ivhd_ctx* ctx, double* step_out);
+
+/* Run n_iter loop iterations on slot with norm and random-pair weight c.
+ * stress_out/step_out (length n_iter, may be NULL) receive the trace
+ * (stress at the pre-step positions, step size after the step).
+ * *done_out = iterations completed.  On IVHD_ERR_DIVERGED the positions are
+ * the last finite ones and stress_out[*done_out] holds the diverging
+ * iteration's stress (engine.py:373-377). */
+int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter,
+             double* stress_out, double* step_out, int64_t* done_out);
+
+/* Operator level: forces (m, dim) and stress at y (host array) on slot. */
+int ivhd_compute_forces(ivhd_ctx* ctx, int slot, int norm, double c, const double* y,
+                        double* forces_out, double* stress_out);
+int ivhd_stress(ivhd_ctx* ctx, int slot, int norm, double c, const double* y,
+                double* stress_out);
+
+int ivhd_synchronize(ivhd_ctx* ctx);
+
+/* Device-side checkpoint of positions + optimizer state + control block
+ * (restore is asynchronous on the context stream; used to restart a run
+ * from identical initial conditions without host copies). */
+int ivhd_snapshot(ivhd_ctx* ctx);
+int ivhd_restore(ivhd_ctx* ctx);
+
+/* ---- vertex-range sharding (one context per rank, full graph replicated) ----
+ * A rank updates vertices [v_begin, v_end) (tile aligned, see
+ * ivhd_tile_vertices), then the caller all-gathers the positions slice and
+ * the tile partials (device pointers from ivhd_shard_buffers) and calls
+ * ivhd_step_finalize, which reduces all tiles in a fixed order so every
+ * rank takes the same commit/rollback decision. */
+int ivhd_tile_vertices(ivhd_ctx* ctx, int64_t* tile_v_out, int64_t* n_tiles_out);
+int ivhd_shard_set_range(ivhd_ctx* ctx, int64_t v_begin, int64_t v_end);
+/* ybuf[2] = the two position buffers; floats_per_vertex = their row stride;
+ * partials = double4 per tile; cur_out = index of the buffer holding the
+ * current positions (the next step writes the other one). */
+int ivhd_shard_buffers(ivhd_ctx* ctx, uint64_t* ybuf0, uint64_t* ybuf1,
+                       int64_t* floats_per_vertex, uint64_t* partials, int* cur_out);
+int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c);
+int ivhd_step_finalize(ivhd_ctx* ctx, double* stress_out, double* step_out,
+                       int* committed_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IVHD_B200_H */

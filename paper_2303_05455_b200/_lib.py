@@ -1,0 +1,130 @@
+"""ctypes binding of libivhd_b200.so (declared in include/ivhd_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, the first call raises DeviceError.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import DeviceError, IvhdError, InvalidArgumentError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("IVHD_B200_LIB", os.path.join(HERE, "libivhd_b200.so"))
+
+OK, ERR_INVALID_ARG, ERR_CUDA, ERR_DIVERGED, ERR_STATE = range(5)
+NORM = {"l2": 0, "l1": 1}
+OPT_KIND = {"force-directed": 0, "sgd": 1, "momentum": 2, "nesterov": 3, "adam": 4, "adadelta": 5}
+
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+c_f64p = ctypes.POINTER(ctypes.c_double)
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_u64p = ctypes.POINTER(ctypes.c_uint64)
+c_u8p = ctypes.POINTER(ctypes.c_uint8)
+
+
+class OptimizerParams(ctypes.Structure):
+    """ivhd_optimizer_params."""
+
+    _fields_ = [
+        ("kind", ctypes.c_int32), ("auto_adapt", ctypes.c_int32), ("step", ctypes.c_double),
+        ("a", ctypes.c_double), ("tau", ctypes.c_double), ("gamma1", ctypes.c_double),
+        ("gamma2", ctypes.c_double), ("beta", ctypes.c_double), ("gamma_v", ctypes.c_double),
+        ("gamma_s", ctypes.c_double), ("rho", ctypes.c_double), ("eps", ctypes.c_double),
+    ]
+
+
+# name -> (restype, argtypes); exactly the symbols include/ivhd_b200.h declares
+SIGNATURES = {
+    "ivhd_abi_version": (ctypes.c_int, []),
+    "ivhd_global_error": (ctypes.c_char_p, []),
+    "ivhd_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int64,
+                                   ctypes.c_int, ctypes.c_uint64]),
+    "ivhd_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "ivhd_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
+    "ivhd_set_graph": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, ctypes.c_int64,
+                                      ctypes.c_int, c_i32p, ctypes.c_int]),
+    "ivhd_set_connections": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, c_u8p, c_f64p,
+                                            c_f64p, ctypes.c_int64]),
+    "ivhd_set_positions": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),
+    "ivhd_get_positions": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),
+    "ivhd_get_deltas": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),
+    "ivhd_set_optimizer": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(OptimizerParams)]),
+    "ivhd_set_step_size": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double]),
+    "ivhd_get_step_size": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),
+    "ivhd_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                ctypes.c_int64, c_f64p, c_f64p, c_i64p]),
+    "ivhd_compute_forces": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_double, c_f64p, c_f64p, c_f64p]),
+    "ivhd_stress": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                   c_f64p, c_f64p]),
+    "ivhd_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "ivhd_snapshot": (ctypes.c_int, [ctypes.c_void_p]),
+    "ivhd_restore": (ctypes.c_int, [ctypes.c_void_p]),
+    "ivhd_tile_vertices": (ctypes.c_int, [ctypes.c_void_p, c_i64p, c_i64p]),
+    "ivhd_shard_set_range": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64]),
+    "ivhd_shard_buffers": (ctypes.c_int, [ctypes.c_void_p, c_u64p, c_u64p, c_i64p, c_u64p,
+                                          ctypes.POINTER(ctypes.c_int)]),
+    "ivhd_step_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_double]),
+    "ivhd_step_finalize": (ctypes.c_int, [ctypes.c_void_p, c_f64p, c_f64p,
+                                          ctypes.POINTER(ctypes.c_int)]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load (once) and return the CDLL; raises DeviceError if it is absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DeviceError(
+                    f"CUDA library not built: {LIB_PATH} is missing "
+                    "(run `python -m paper_2303_05455_b200.build`)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            if lib.ivhd_abi_version() != 1:
+                raise DeviceError("libivhd_b200.so ABI version mismatch")
+            _lib = lib
+        return _lib
+
+
+def ptr(a, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype)) if a is not None else None
+
+
+def f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+class StatusError(IvhdError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def check(code, ctx_handle=None):
+    """Map an ivhd_status to the reference's exception classes."""
+    if code == OK:
+        return
+    lib = load()
+    msg = (lib.ivhd_last_error(ctx_handle) if ctx_handle else lib.ivhd_global_error()) or b""
+    msg = msg.decode(errors="replace")
+    if code == ERR_INVALID_ARG:
+        raise InvalidArgumentError(msg)
+    if code == ERR_DIVERGED:
+        raise StatusError(code, msg)
+    raise DeviceError(f"ivhd status {code}: {msg}")

@@ -1,0 +1,981 @@
+// ivhd_capi.cu — context, symmetrised-CSR builder, launch plumbing and the
+// extern "C" entry points declared in include/ivhd_b200.h.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/ivhd_b200.h"
+#include "ivhd_step.cuh"
+
+using namespace ivhd;
+
+namespace {
+
+thread_local std::string g_error;
+
+struct CsrSlot {
+  uint32_t* row_ptr = nullptr;  // [M+1]
+  uint32_t* col = nullptr;      // [n]
+  float2* ew = nullptr;         // [n] or nullptr (binary)
+  int64_t n = 0;                // entries (2 * connections)
+  int64_t cap = 0;
+  int G = 4;
+  bool valid = false;
+};
+
+using KernelFn = void (*)(StepArgs);
+
+struct GraphKey {
+  int slot, norm, opt, G;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(slot, norm, opt, G) < std::tie(o.slot, o.norm, o.opt, o.G);
+  }
+};
+
+}  // namespace
+
+struct ivhd_ctx {
+  int device = 0;
+  int64_t m = 0;
+  int dim = 2;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 148;
+
+  int tile_v = 64;
+  int n_tiles = 0;
+  int n_tiles_cap = 0;  // padded to a multiple of 8 (rank counts 1/2/4/8)
+  int64_t v_cap = 0;    // vertex capacity of position/state buffers
+
+  CsrSlot slots[2];
+
+  float* ybuf[2] = {nullptr, nullptr};  // 8 floats/vertex capacity
+  float* state = nullptr;               // 8 floats/vertex capacity
+  double4* partial = nullptr;
+  double2* trace = nullptr;
+  int64_t trace_cap = 0;
+  Ctrl* ctrl = nullptr;      // device
+  Ctrl* ctrl_h = nullptr;    // pinned host mirror
+  Ctrl* opctrl = nullptr;    // device, operator calls
+  double4* red_out = nullptr;
+
+  // scratch
+  double* stage = nullptr;  // (v_cap * 4) doubles: host <-> device conversion
+  float* op_y = nullptr;    // operator positions (8 floats/vertex)
+  double* op_force = nullptr;
+  float* snap_y = nullptr;      // snapshot: positions (8 floats/vertex)
+  float* snap_state = nullptr;  // snapshot: optimizer state
+  Ctrl snap_ctrl{};
+  bool snap_valid = false;
+
+  ivhd_optimizer_params opt{};
+  bool opt_set = false;
+  bool pos_set = false;
+  Hyper hyper{};
+
+  int64_t shard_begin = 0, shard_end = 0;  // sharded mode range (0,0 = whole)
+  bool sharded = false;
+
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  int graph_chunk = 64;
+
+  std::map<KernelFn, int> occ;
+  std::string err;
+};
+
+namespace {
+
+int fail(ivhd_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  g_error = buf;
+  return code;
+}
+
+#define CU(ctx, call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(ctx, IVHD_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+#define TRY(expr)               \
+  do {                          \
+    int r_ = (expr);            \
+    if (r_ != IVHD_OK) return r_; \
+  } while (0)
+
+inline int ys_of(int dim, int opt) { return (opt == OPT_NEST) ? (dim == 2 ? 4 : 8) : (dim == 2 ? 2 : 4); }
+
+// ------------------------------------------------------------ kernel table
+
+template <int DIM, int G>
+KernelFn pick_opt(int opt) {
+  switch (opt) {
+    case OPT_FD: return step_kernel<DIM, OPT_FD, G>;
+    case OPT_SGD: return step_kernel<DIM, OPT_SGD, G>;
+    case OPT_MOM: return step_kernel<DIM, OPT_MOM, G>;
+    case OPT_NEST: return step_kernel<DIM, OPT_NEST, G>;
+    case OPT_ADAM: return step_kernel<DIM, OPT_ADAM, G>;
+    case OPT_ADADELTA: return step_kernel<DIM, OPT_ADADELTA, G>;
+    default: return step_kernel<DIM, OPT_NONE, G>;
+  }
+}
+
+KernelFn pick_kernel(int dim, int opt, int G) {
+  if (dim == 2) return G == 4 ? pick_opt<2, 4>(opt) : (G == 8 ? pick_opt<2, 8>(opt) : pick_opt<2, 16>(opt));
+  return G == 4 ? pick_opt<3, 4>(opt) : (G == 8 ? pick_opt<3, 8>(opt) : pick_opt<3, 16>(opt));
+}
+
+KernelFn pick_finalize(int opt) {
+  switch (opt) {
+    case OPT_FD: return finalize_kernel<OPT_FD>;
+    case OPT_ADAM: return finalize_kernel<OPT_ADAM>;
+    default: return finalize_kernel<OPT_SGD>;
+  }
+}
+
+int occupancy(ivhd_ctx* ctx, KernelFn fn) {
+  auto it = ctx->occ.find(fn);
+  if (it != ctx->occ.end()) return it->second;
+  int n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kBlock, 0) != cudaSuccess || n < 1) n = 1;
+  ctx->occ[fn] = n;
+  return n;
+}
+
+// ------------------------------------------------------------ small kernels
+
+__global__ void k_half_edges(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                             int64_t L, int64_t m, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals, int* __restrict__ bad) {
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < 2 * L;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = h < L ? src[h] : dst[h - L];
+    if (r < 0 || r >= m) *bad = 1;
+    keys[h] = (uint32_t)max(0, min((int32_t)(m - 1), r));
+    vals[h] = (uint32_t)h;
+  }
+}
+
+__global__ void k_row_ptr(const uint32_t* __restrict__ keys, int64_t n, int64_t m,
+                          uint32_t* __restrict__ row_ptr) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;  // first k with keys[k] >= r
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < (uint32_t)r) lo = mid + 1; else hi = mid;
+    }
+    row_ptr[r] = (uint32_t)lo;
+  }
+}
+
+__global__ void k_fill_cols(const uint32_t* __restrict__ vals, int64_t n, int64_t L,
+                            const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                            const uint8_t* __restrict__ rand, int64_t n_nn,
+                            const float* __restrict__ tgt, const float* __restrict__ scl,
+                            uint32_t* __restrict__ col, float2* __restrict__ ew) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = vals[k];
+    const int64_t e = h < L ? h : h - L;
+    const uint32_t other = (uint32_t)(h < L ? dst[e] : src[e]);
+    const bool rn = rand ? (rand[e] != 0) : (e >= n_nn);
+    col[k] = other | (rn ? kRandBit : 0u);
+    if (ew) ew[k] = make_float2(tgt ? tgt[e] : (rn ? 1.f : 0.f), scl ? scl[e] : 1.f);
+  }
+}
+
+__global__ void k_binary_edges(const int32_t* __restrict__ nn, int64_t stride, int ncols,
+                               const int32_t* __restrict__ rn, int nrn, int64_t m,
+                               int32_t* __restrict__ src, int32_t* __restrict__ dst) {
+  const int64_t n_nn = m * ncols, L = n_nn + m * nrn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < n_nn) {
+      const int64_t i = e / ncols;
+      src[e] = (int32_t)i;
+      dst[e] = nn[i * stride + (e - i * ncols)];
+    } else {
+      const int64_t q = e - n_nn, i = q / nrn;
+      src[e] = (int32_t)i;
+      dst[e] = rn[q];
+    }
+  }
+}
+
+__global__ void k_split_edges(const int32_t* __restrict__ edges, int64_t L,
+                              int32_t* __restrict__ src, int32_t* __restrict__ dst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    src[e] = edges[2 * e];
+    dst[e] = edges[2 * e + 1];
+  }
+}
+
+__global__ void k_d2f(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+
+// host double (m, dim) -> layout with stride ys; Nesterov look = y + beta*v
+__global__ void k_pack_positions(const double* __restrict__ y, int64_t m, int dim, int ys,
+                                 const float* __restrict__ vel, int vel_stride, float beta,
+                                 float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float* o = out + i * ys;
+    const int look_off = (ys == 4 && dim == 2) ? 2 : 4;
+    for (int d = 0; d < dim; ++d) {
+      const float v = (float)y[i * dim + d];
+      o[d] = v;
+      if (vel) o[look_off + d] = v + beta * vel[i * vel_stride + d];
+    }
+  }
+}
+
+__global__ void k_unpack_positions(const float* __restrict__ in, int64_t m, int dim, int ys,
+                                   double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < dim; ++d) y[i * dim + d] = (double)in[i * ys + d];
+}
+
+__global__ void k_deltas(const float* __restrict__ a, const float* __restrict__ b, int64_t m,
+                         int dim, int ys, int commit, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < dim; ++d)
+      out[i * dim + d] = commit ? (double)a[i * ys + d] - (double)b[i * ys + d] : 0.0;
+}
+
+// fixed-order reduction of partial tiles into one double4 (operator calls)
+__global__ void __launch_bounds__(kBlock) k_reduce_partials(const double4* __restrict__ p, int n,
+                                                            double4* __restrict__ out) {
+  __shared__ double4 sm[kBlock / 32];
+  double4 s = make_double4(0, 0, 0, 0);
+  for (int t = threadIdx.x; t < n; t += kBlock) {
+    const double4 q = p[t];
+    s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+  }
+  s = block_sum4(s, sm);
+  if (threadIdx.x == 0) *out = s;
+}
+
+inline int grid_for(int64_t n, int sms) {
+  const int64_t g = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sms * 16));
+}
+
+// ------------------------------------------------------------- CSR builder
+
+int ensure_slot(ivhd_ctx* ctx, CsrSlot& s, int64_t n, bool weighted) {
+  if (s.row_ptr == nullptr) CU(ctx, cudaMalloc(&s.row_ptr, sizeof(uint32_t) * (ctx->m + 1)));
+  if (n > s.cap) {
+    if (s.col) CU(ctx, cudaFree(s.col));
+    if (s.ew) CU(ctx, cudaFree(s.ew));
+    s.col = nullptr;
+    s.ew = nullptr;
+    CU(ctx, cudaMalloc(&s.col, sizeof(uint32_t) * std::max<int64_t>(n, 1)));
+    s.cap = n;
+  }
+  if (weighted && s.ew == nullptr) CU(ctx, cudaMalloc(&s.ew, sizeof(float2) * std::max<int64_t>(s.cap, 1)));
+  if (!weighted && s.ew != nullptr) {
+    CU(ctx, cudaFree(s.ew));
+    s.ew = nullptr;
+  }
+  return IVHD_OK;
+}
+
+void drop_graphs(ivhd_ctx* ctx) {
+  for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+  ctx->graphs.clear();
+}
+
+// src/dst: device int32 [L]; rand: device u8 [L] or null (then e >= n_nn is random);
+// tgt/scl: device float [L] or null.
+int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, const uint8_t* rand,
+              int64_t n_nn, const float* tgt, const float* scl, int64_t L) {
+  CsrSlot& S = ctx->slots[slot];
+  const int64_t n = 2 * L;
+  if (n >= (int64_t)0x7fffffffLL) return fail(ctx, IVHD_ERR_INVALID_ARG, "too many connections (%lld)", (long long)L);
+  const bool weighted = (tgt != nullptr) || (scl != nullptr);
+  TRY(ensure_slot(ctx, S, n, weighted));
+  drop_graphs(ctx);
+  S.valid = false;
+  S.n = n;
+  cudaStream_t st = ctx->stream;
+  if (n == 0) {
+    CU(ctx, cudaMemsetAsync(S.row_ptr, 0, sizeof(uint32_t) * (ctx->m + 1), st));
+    CU(ctx, cudaStreamSynchronize(st));
+    S.G = 4;
+    S.valid = true;
+    return IVHD_OK;
+  }
+  uint32_t *keys = nullptr, *keys2 = nullptr, *vals = nullptr, *vals2 = nullptr;
+  int* bad = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int end_bit = 1;
+  while (end_bit < 32 && ((int64_t)1 << end_bit) < ctx->m) ++end_bit;
+  cudaError_t e = cudaSuccess;
+  int hbad = 0;
+  auto cleanup = [&]() {
+    cudaFree(keys); cudaFree(keys2); cudaFree(vals); cudaFree(vals2); cudaFree(bad); cudaFree(tmp);
+  };
+  do {
+    if ((e = cudaMalloc(&keys, 4 * n)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&keys2, 4 * n)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&vals, 4 * n)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&vals2, 4 * n)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&bad, sizeof(int))) != cudaSuccess) break;
+    if ((e = cudaMemsetAsync(bad, 0, sizeof(int), st)) != cudaSuccess) break;
+    k_half_edges<<<grid_for(n, ctx->sm_count), 256, 0, st>>>(src, dst, L, ctx->m, keys, vals, bad);
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0,
+                                             end_bit, st)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16))) != cudaSuccess) break;
+    // LSD radix sort is stable: rows list out-halves (connection order) then in-halves.
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0,
+                                             end_bit, st)) != cudaSuccess) break;
+    k_row_ptr<<<grid_for(ctx->m + 1, ctx->sm_count), 256, 0, st>>>(keys2, n, ctx->m, S.row_ptr);
+    k_fill_cols<<<grid_for(n, ctx->sm_count), 256, 0, st>>>(vals2, n, L, src, dst, rand, n_nn, tgt, scl,
+                                                           S.col, S.ew);
+    if ((e = cudaGetLastError()) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    e = cudaStreamSynchronize(st);
+  } while (0);
+  cleanup();
+  if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "CSR build: %s", cudaGetErrorString(e));
+  if (hbad) return fail(ctx, IVHD_ERR_INVALID_ARG, "connection endpoint outside [0, %lld)", (long long)ctx->m);
+  // lanes per row: nearest power of two to the mean symmetrised degree
+  const double mean = (double)n / (double)ctx->m;
+  S.G = mean <= 8.0 ? 4 : (mean <= 20.0 ? 8 : 16);
+  S.valid = true;
+  return IVHD_OK;
+}
+
+// ---------------------------------------------------------- launch helpers
+
+StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
+  const CsrSlot& S = ctx->slots[slot];
+  StepArgs A{};
+  A.row_ptr = S.row_ptr;
+  A.col = S.col;
+  A.ew = S.ew;
+  A.ybuf0 = ctx->ybuf[0];
+  A.ybuf1 = ctx->ybuf[1];
+  A.state = ctx->state;
+  A.partial = ctx->partial;
+  A.trace = ctx->trace;
+  A.ctrl = ctx->ctrl;
+  A.force_out = nullptr;
+  A.tile_v = ctx->tile_v;
+  A.norm = norm;
+  A.fuse_finalize = fuse;
+  A.h = ctx->hyper;
+  if (ctx->sharded) {
+    A.v_begin = ctx->shard_begin;
+    A.v_end = std::min<int64_t>(ctx->shard_end, ctx->m);
+    A.tile0 = (int)(ctx->shard_begin / ctx->tile_v);
+    A.n_tiles = (int)((ctx->shard_end - ctx->shard_begin) / ctx->tile_v);
+    A.n_tiles_global = ctx->n_tiles_cap;
+  } else {
+    A.v_begin = 0;
+    A.v_end = ctx->m;
+    A.tile0 = 0;
+    A.n_tiles = ctx->n_tiles;
+    A.n_tiles_global = ctx->n_tiles;
+  }
+  return A;
+}
+
+int launch_step(ivhd_ctx* ctx, KernelFn fn, const StepArgs& A) {
+  const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
+  fn<<<grid, kBlock, 0, ctx->stream>>>(A);
+  CU(ctx, cudaGetLastError());
+  return IVHD_OK;
+}
+
+int check_ready(ivhd_ctx* ctx, int slot) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (slot < 0 || slot > 1) return fail(ctx, IVHD_ERR_INVALID_ARG, "slot must be 0 or 1");
+  if (!ctx->slots[slot].valid) return fail(ctx, IVHD_ERR_STATE, "connection slot %d not set", slot);
+  CU(ctx, cudaSetDevice(ctx->device));
+  return IVHD_OK;
+}
+
+int push_ctrl(ivhd_ctx* ctx) {
+  CU(ctx, cudaMemcpyAsync(ctx->ctrl, ctx->ctrl_h, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  return IVHD_OK;
+}
+
+int pull_ctrl(ivhd_ctx* ctx) {
+  CU(ctx, cudaMemcpyAsync(ctx->ctrl_h, ctx->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
+}
+
+int upload_stage(ivhd_ctx* ctx, const double* host, int64_t count) {
+  CU(ctx, cudaMemcpyAsync(ctx->stage, host, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+  return IVHD_OK;
+}
+
+int vel_stride(int dim) { return dim == 2 ? 2 : 4; }
+
+}  // namespace
+
+// ======================================================================= C ABI
+
+extern "C" {
+
+int ivhd_abi_version(void) { return IVHD_ABI_VERSION; }
+
+const char* ivhd_global_error(void) { return g_error.c_str(); }
+
+const char* ivhd_last_error(const ivhd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_error.c_str(); }
+
+int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream) {
+  if (!out) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null output pointer");
+  *out = nullptr;
+  if (m < 1) return fail(nullptr, IVHD_ERR_INVALID_ARG, "need at least one point");
+  if (m >= (int64_t)0x7fffffff) return fail(nullptr, IVHD_ERR_INVALID_ARG, "M too large for 31-bit ids");
+  if (dim != 2 && dim != 3) return fail(nullptr, IVHD_ERR_INVALID_ARG, "target_dim must be 2 or 3");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, IVHD_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, IVHD_ERR_INVALID_ARG, "bad device %d", device);
+  ivhd_ctx* ctx = new ivhd_ctx();
+  ctx->device = device;
+  ctx->m = m;
+  ctx->dim = dim;
+  auto bail = [&](int code) {
+    g_error = ctx->err;
+    ivhd_destroy(ctx);
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, IVHD_ERR_CUDA, "cudaSetDevice failed"));
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (stream) {
+    ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(ctx, IVHD_ERR_CUDA, "stream create failed"));
+    ctx->own_stream = true;
+  }
+  // Fixed tile size (a function of M only): the reduction order is the same
+  // for any grid size and any number of ranks.
+  int64_t tv = 64;
+  while (tv < 4096 && tv * 4096 <= m) tv <<= 1;
+  ctx->tile_v = (int)tv;
+  ctx->n_tiles = (int)((m + tv - 1) / tv);
+  ctx->n_tiles_cap = (ctx->n_tiles + 7) / 8 * 8;
+  ctx->v_cap = (int64_t)ctx->n_tiles_cap * tv;
+  const int64_t vc = ctx->v_cap;
+  int rc = IVHD_OK;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (rc != IVHD_OK) return;
+    cudaError_t ee = cudaMalloc(p, bytes);
+    if (ee != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(ee));
+    else cudaMemset(*p, 0, bytes);
+  };
+  alloc((void**)&ctx->ybuf[0], sizeof(float) * 8 * vc);
+  alloc((void**)&ctx->ybuf[1], sizeof(float) * 8 * vc);
+  alloc((void**)&ctx->state, sizeof(float) * 8 * vc);
+  alloc((void**)&ctx->partial, sizeof(double4) * ctx->n_tiles_cap);
+  alloc((void**)&ctx->ctrl, sizeof(Ctrl));
+  alloc((void**)&ctx->opctrl, sizeof(Ctrl));
+  alloc((void**)&ctx->red_out, sizeof(double4));
+  alloc((void**)&ctx->stage, sizeof(double) * 4 * vc);
+  if (rc != IVHD_OK) return bail(rc);
+  if (cudaMallocHost(&ctx->ctrl_h, sizeof(Ctrl)) != cudaSuccess)
+    return bail(fail(ctx, IVHD_ERR_CUDA, "pinned alloc failed"));
+  memset(ctx->ctrl_h, 0, sizeof(Ctrl));
+  ctx->ctrl_h->c = 0.1;
+  ctx->ctrl_h->step = 0.002;
+  cudaMemcpy(ctx->ctrl, ctx->ctrl_h, sizeof(Ctrl), cudaMemcpyHostToDevice);
+  // default optimizer: force-directed with the reference defaults (optim.py:24-29)
+  ivhd_optimizer_params p{};
+  p.kind = IVHD_OPT_FORCE_DIRECTED;
+  p.auto_adapt = 1;
+  p.step = 0.002;
+  p.a = 0.99;
+  p.tau = 1e-3 * (double)m;
+  p.gamma1 = 1.1;
+  p.gamma2 = 0.9;
+  p.beta = 0.9;
+  p.gamma_v = 0.9;
+  p.gamma_s = 0.999;
+  p.rho = 0.95;
+  p.eps = 1e-8;
+  if ((rc = ivhd_set_optimizer(ctx, &p)) != IVHD_OK) return bail(rc);
+  *out = ctx;
+  return IVHD_OK;
+}
+
+int ivhd_destroy(ivhd_ctx* ctx) {
+  if (!ctx) return IVHD_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  drop_graphs(ctx);
+  for (auto& s : ctx->slots) {
+    cudaFree(s.row_ptr); cudaFree(s.col); cudaFree(s.ew);
+  }
+  cudaFree(ctx->ybuf[0]); cudaFree(ctx->ybuf[1]); cudaFree(ctx->state); cudaFree(ctx->partial);
+  cudaFree(ctx->trace); cudaFree(ctx->ctrl); cudaFree(ctx->opctrl); cudaFree(ctx->red_out);
+  cudaFree(ctx->stage); cudaFree(ctx->op_y); cudaFree(ctx->op_force);
+  cudaFree(ctx->snap_y); cudaFree(ctx->snap_state);
+  if (ctx->ctrl_h) cudaFreeHost(ctx->ctrl_h);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return IVHD_OK;
+}
+
+int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_stride, int ncols,
+                   const int32_t* rn_ids, int rn) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (slot < 0 || slot > 1) return fail(ctx, IVHD_ERR_INVALID_ARG, "slot must be 0 or 1");
+  if (ncols < 0 || rn < 0 || nn_stride < ncols || (ncols > 0 && !nn_ids) || (rn > 0 && !rn_ids))
+    return fail(ctx, IVHD_ERR_INVALID_ARG, "bad graph arguments");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const int64_t m = ctx->m, n_nn = m * ncols, L = n_nn + m * rn;
+  int32_t *d_nn = nullptr, *d_rn = nullptr, *d_src = nullptr, *d_dst = nullptr;
+  cudaError_t e = cudaSuccess;
+  do {
+    if (ncols > 0) {
+      if ((e = cudaMalloc(&d_nn, sizeof(int32_t) * m * nn_stride)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(d_nn, nn_ids, sizeof(int32_t) * m * nn_stride, cudaMemcpyHostToDevice,
+                               ctx->stream)) != cudaSuccess) break;
+    }
+    if (rn > 0) {
+      if ((e = cudaMalloc(&d_rn, sizeof(int32_t) * m * rn)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(d_rn, rn_ids, sizeof(int32_t) * m * rn, cudaMemcpyHostToDevice,
+                               ctx->stream)) != cudaSuccess) break;
+    }
+    if ((e = cudaMalloc(&d_src, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
+    if ((e = cudaMalloc(&d_dst, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
+    if (L > 0)
+      k_binary_edges<<<grid_for(L, ctx->sm_count), 256, 0, ctx->stream>>>(d_nn, nn_stride, ncols, d_rn, rn,
+                                                                          m, d_src, d_dst);
+    e = cudaGetLastError();
+  } while (0);
+  int rc = IVHD_OK;
+  if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "set_graph: %s", cudaGetErrorString(e));
+  else rc = build_csr(ctx, slot, d_src, d_dst, nullptr, n_nn, nullptr, nullptr, L);
+  cudaFree(d_nn); cudaFree(d_rn); cudaFree(d_src); cudaFree(d_dst);
+  return rc;
+}
+
+int ivhd_set_connections(ivhd_ctx* ctx, int slot, const int32_t* edges, const uint8_t* is_random,
+                         const double* targets, const double* scale, int64_t n_conn) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (slot < 0 || slot > 1) return fail(ctx, IVHD_ERR_INVALID_ARG, "slot must be 0 or 1");
+  if (n_conn < 0 || (n_conn > 0 && (!edges || !is_random)))
+    return fail(ctx, IVHD_ERR_INVALID_ARG, "bad connection arguments");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const int64_t L = n_conn, Lc = std::max<int64_t>(L, 1);
+  int32_t *d_e = nullptr, *d_src = nullptr, *d_dst = nullptr;
+  uint8_t* d_r = nullptr;
+  double* d_tmp = nullptr;
+  float *d_t = nullptr, *d_s = nullptr;
+  cudaError_t e = cudaSuccess;
+  cudaStream_t st = ctx->stream;
+  do {
+    if ((e = cudaMalloc(&d_e, sizeof(int32_t) * 2 * Lc)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&d_src, sizeof(int32_t) * Lc)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&d_dst, sizeof(int32_t) * Lc)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&d_r, Lc)) != cudaSuccess) break;
+    if (L > 0) {
+      if ((e = cudaMemcpyAsync(d_e, edges, sizeof(int32_t) * 2 * L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(d_r, is_random, L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+      k_split_edges<<<grid_for(L, ctx->sm_count), 256, 0, st>>>(d_e, L, d_src, d_dst);
+    }
+    if (targets || scale) {
+      if ((e = cudaMalloc(&d_tmp, sizeof(double) * Lc)) != cudaSuccess) break;
+    }
+    if (targets) {
+      if ((e = cudaMalloc(&d_t, sizeof(float) * Lc)) != cudaSuccess) break;
+      if (L > 0) {
+        if ((e = cudaMemcpyAsync(d_tmp, targets, sizeof(double) * L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+        k_d2f<<<grid_for(L, ctx->sm_count), 256, 0, st>>>(d_tmp, d_t, L);
+      }
+    }
+    if (scale) {
+      if ((e = cudaMalloc(&d_s, sizeof(float) * Lc)) != cudaSuccess) break;
+      if (L > 0) {
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;  // d_tmp reuse
+        if ((e = cudaMemcpyAsync(d_tmp, scale, sizeof(double) * L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+        k_d2f<<<grid_for(L, ctx->sm_count), 256, 0, st>>>(d_tmp, d_s, L);
+      }
+    }
+    e = cudaGetLastError();
+  } while (0);
+  int rc = IVHD_OK;
+  if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "set_connections: %s", cudaGetErrorString(e));
+  else rc = build_csr(ctx, slot, d_src, d_dst, d_r, 0, d_t, d_s, L);
+  cudaFree(d_e); cudaFree(d_src); cudaFree(d_dst); cudaFree(d_r); cudaFree(d_tmp); cudaFree(d_t); cudaFree(d_s);
+  return rc;
+}
+
+int ivhd_set_positions(ivhd_ctx* ctx, const double* y) {
+  if (!ctx || !y) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  const int ys = ys_of(ctx->dim, ctx->opt.kind);
+  TRY(upload_stage(ctx, y, ctx->m * ctx->dim));
+  const bool nest = ctx->opt.kind == IVHD_OPT_NESTEROV;
+  float* dst = ctx->ybuf[ctx->ctrl_h->cur];
+  k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
+      ctx->stage, ctx->m, ctx->dim, ys, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
+      (float)ctx->hyper.beta, dst);
+  CU(ctx, cudaGetLastError());
+  ctx->ctrl_h->status = 0;
+  ctx->ctrl_h->last_commit = 0;
+  TRY(push_ctrl(ctx));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->pos_set = true;
+  return IVHD_OK;
+}
+
+int ivhd_get_positions(ivhd_ctx* ctx, double* y_out) {
+  if (!ctx || !y_out) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  const int ys = ys_of(ctx->dim, ctx->opt.kind);
+  k_unpack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
+      ctx->ybuf[ctx->ctrl_h->cur], ctx->m, ctx->dim, ys, ctx->stage);
+  CU(ctx, cudaGetLastError());
+  CU(ctx, cudaMemcpyAsync(y_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
+}
+
+int ivhd_get_deltas(ivhd_ctx* ctx, double* d_out) {
+  if (!ctx || !d_out) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  const int ys = ys_of(ctx->dim, ctx->opt.kind);
+  const int cur = ctx->ctrl_h->cur;
+  k_deltas<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
+      ctx->ybuf[cur], ctx->ybuf[cur ^ 1], ctx->m, ctx->dim, ys, ctx->ctrl_h->last_commit, ctx->stage);
+  CU(ctx, cudaGetLastError());
+  CU(ctx, cudaMemcpyAsync(d_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
+}
+
+int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p) {
+  if (!ctx || !p) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  if (p->kind < 0 || p->kind > 5) return fail(ctx, IVHD_ERR_INVALID_ARG, "unknown optimizer kind %d", p->kind);
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  const int old_ys = ys_of(ctx->dim, ctx->opt.kind);
+  const int new_ys = ys_of(ctx->dim, p->kind);
+  if (ctx->pos_set && old_ys != new_ys) {
+    // re-pack the current positions for the new layout (velocity starts at 0)
+    float* cur = ctx->ybuf[ctx->ctrl_h->cur];
+    k_unpack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(cur, ctx->m, ctx->dim,
+                                                                                old_ys, ctx->stage);
+    CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * 8 * ctx->v_cap, ctx->stream));
+    k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
+        ctx->stage, ctx->m, ctx->dim, new_ys, p->kind == IVHD_OPT_NESTEROV ? ctx->state : nullptr,
+        vel_stride(ctx->dim), (float)p->beta, cur);
+    CU(ctx, cudaGetLastError());
+  }
+  CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * 8 * ctx->v_cap, ctx->stream));
+  ctx->opt = *p;
+  ctx->opt_set = true;
+  Hyper h{};
+  h.a = (float)p->a;
+  h.g1 = (float)p->gamma1;
+  h.g2 = (float)p->gamma2;
+  h.tau = p->tau;
+  h.adapt = p->auto_adapt;
+  h.beta = (float)p->beta;
+  h.gv = (float)p->gamma_v;
+  h.gs = (float)p->gamma_s;
+  h.rho = (float)p->rho;
+  h.eps = (float)p->eps;
+  ctx->hyper = h;
+  ctx->ctrl_h->step = p->step;
+  ctx->ctrl_h->adam_t = 0;
+  ctx->ctrl_h->last_commit = 0;
+  TRY(push_ctrl(ctx));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  drop_graphs(ctx);
+  return IVHD_OK;
+}
+
+int ivhd_set_step_size(ivhd_ctx* ctx, double step) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (!(step > 0)) return fail(ctx, IVHD_ERR_INVALID_ARG, "step size must be positive, got %g", step);
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  ctx->ctrl_h->step = step;
+  TRY(push_ctrl(ctx));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
+}
+
+int ivhd_get_step_size(ivhd_ctx* ctx, double* step_out) {
+  if (!ctx || !step_out) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  *step_out = ctx->ctrl_h->step;
+  return IVHD_OK;
+}
+
+static int ensure_trace(ivhd_ctx* ctx, int64_t n) {
+  if (n <= ctx->trace_cap) return IVHD_OK;
+  const int64_t cap = std::max<int64_t>(n, 4096);
+  if (ctx->trace) CU(ctx, cudaFree(ctx->trace));
+  ctx->trace = nullptr;
+  CU(ctx, cudaMalloc(&ctx->trace, sizeof(double2) * cap));
+  ctx->trace_cap = cap;
+  drop_graphs(ctx);
+  return IVHD_OK;
+}
+
+int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double* stress_out,
+             double* step_out, int64_t* done_out) {
+  TRY(check_ready(ctx, slot));
+  if (done_out) *done_out = 0;
+  if (norm != IVHD_NORM_L2 && norm != IVHD_NORM_L1) return fail(ctx, IVHD_ERR_INVALID_ARG, "unknown norm %d", norm);
+  if (n_iter < 0) return fail(ctx, IVHD_ERR_INVALID_ARG, "n_iter must be >= 0");
+  if (!ctx->pos_set) return fail(ctx, IVHD_ERR_STATE, "positions not set");
+  if (ctx->sharded) return fail(ctx, IVHD_ERR_STATE, "context is sharded; use ivhd_step_local/finalize");
+  TRY(ensure_trace(ctx, n_iter));
+  TRY(pull_ctrl(ctx));
+  if (ctx->ctrl_h->status != 0) return fail(ctx, IVHD_ERR_DIVERGED, "context already diverged");
+  ctx->ctrl_h->c = c;
+  ctx->ctrl_h->iter = 0;
+  ctx->ctrl_h->arrive = 0;
+  ctx->ctrl_h->next_tile = 0;
+  TRY(push_ctrl(ctx));
+  const CsrSlot& S = ctx->slots[slot];
+  KernelFn fn = pick_kernel(ctx->dim, ctx->opt.kind, S.G);
+  const StepArgs A = make_args(ctx, slot, norm, 1);
+  int64_t left = n_iter;
+  const int chunk = ctx->graph_chunk;
+  if (left >= chunk) {
+    const GraphKey key{slot, norm, ctx->opt.kind, S.G};
+    auto it = ctx->graphs.find(key);
+    cudaGraphExec_t exec = nullptr;
+    if (it == ctx->graphs.end()) {
+      cudaGraph_t graph = nullptr;
+      (void)occupancy(ctx, fn);  // not inside the capture
+      CU(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      int rc = IVHD_OK;
+      for (int i = 0; i < chunk && rc == IVHD_OK; ++i) rc = launch_step(ctx, fn, A);
+      cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+      if (rc != IVHD_OK) return rc;
+      if (ce != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+      ctx->graphs[key] = exec;
+    } else {
+      exec = it->second;
+    }
+    while (left >= chunk) {
+      CU(ctx, cudaGraphLaunch(exec, ctx->stream));
+      left -= chunk;
+    }
+  }
+  for (; left > 0; --left) TRY(launch_step(ctx, fn, A));
+  TRY(pull_ctrl(ctx));
+  const Ctrl& C = *ctx->ctrl_h;
+  const bool diverged = C.status != 0;
+  const int64_t done = diverged ? C.diverged_at : C.iter;
+  const int64_t ntr = diverged ? done + 1 : done;
+  if (ntr > 0 && (stress_out || step_out)) {
+    std::vector<double2> tr(ntr);
+    CU(ctx, cudaMemcpy(tr.data(), ctx->trace, sizeof(double2) * ntr, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < ntr; ++i) {
+      if (stress_out) stress_out[i] = tr[i].x;
+      if (step_out) step_out[i] = tr[i].y;
+    }
+  }
+  if (done_out) *done_out = done;
+  if (diverged) return fail(ctx, IVHD_ERR_DIVERGED, "embedding diverged at local iteration %lld", (long long)done);
+  return IVHD_OK;
+}
+
+static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* y, bool want_forces,
+                     double* forces_out, double* stress_out) {
+  TRY(check_ready(ctx, slot));
+  if (norm != IVHD_NORM_L2 && norm != IVHD_NORM_L1) return fail(ctx, IVHD_ERR_INVALID_ARG, "unknown norm %d", norm);
+  if (!y) return fail(ctx, IVHD_ERR_INVALID_ARG, "null positions");
+  if (!ctx->op_y) CU(ctx, cudaMalloc(&ctx->op_y, sizeof(float) * 4 * ctx->v_cap));
+  if (!ctx->op_force) CU(ctx, cudaMalloc(&ctx->op_force, sizeof(double) * 3 * ctx->v_cap));
+  const int ys = ctx->dim == 2 ? 2 : 4;
+  TRY(upload_stage(ctx, y, ctx->m * ctx->dim));
+  k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->stage, ctx->m, ctx->dim, ys,
+                                                                           nullptr, 0, 0.f, ctx->op_y);
+  TRY(pull_ctrl(ctx));
+  Ctrl oc{};
+  oc.c = c;
+  oc.gstep = ctx->ctrl_h->gstep;
+  CU(ctx, cudaMemcpyAsync(ctx->opctrl, &oc, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  const CsrSlot& S = ctx->slots[slot];
+  StepArgs A{};
+  A.row_ptr = S.row_ptr;
+  A.col = S.col;
+  A.ew = S.ew;
+  A.ybuf0 = ctx->op_y;
+  A.ybuf1 = ctx->op_y;
+  A.partial = ctx->partial;
+  A.ctrl = ctx->opctrl;
+  A.force_out = ctx->op_force;
+  A.v_begin = 0;
+  A.v_end = ctx->m;
+  A.tile_v = ctx->tile_v;
+  A.n_tiles = ctx->n_tiles;
+  A.n_tiles_global = ctx->n_tiles;
+  A.norm = norm;
+  A.fuse_finalize = 0;
+  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, S.G), A));
+  k_reduce_partials<<<1, kBlock, 0, ctx->stream>>>(ctx->partial, ctx->n_tiles, ctx->red_out);
+  CU(ctx, cudaGetLastError());
+  double4 red;
+  CU(ctx, cudaMemcpyAsync(&red, ctx->red_out, sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
+  if (want_forces)
+    CU(ctx, cudaMemcpyAsync(forces_out, ctx->op_force, sizeof(double) * ctx->m * ctx->dim,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (stress_out) *stress_out = 0.5 * red.x;
+  return IVHD_OK;
+}
+
+int ivhd_compute_forces(ivhd_ctx* ctx, int slot, int norm, double c, const double* y, double* forces_out,
+                        double* stress_out) {
+  if (!forces_out) return fail(ctx, IVHD_ERR_INVALID_ARG, "null forces_out");
+  return op_launch(ctx, slot, norm, c, y, true, forces_out, stress_out);
+}
+
+int ivhd_stress(ivhd_ctx* ctx, int slot, int norm, double c, const double* y, double* stress_out) {
+  return op_launch(ctx, slot, norm, c, y, false, nullptr, stress_out);
+}
+
+int ivhd_snapshot(ivhd_ctx* ctx) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const size_t bytes = sizeof(float) * 8 * ctx->v_cap;
+  if (!ctx->snap_y) CU(ctx, cudaMalloc(&ctx->snap_y, bytes));
+  if (!ctx->snap_state) CU(ctx, cudaMalloc(&ctx->snap_state, bytes));
+  TRY(pull_ctrl(ctx));
+  const size_t used = sizeof(float) * 8 * ctx->m;
+  CU(ctx, cudaMemcpyAsync(ctx->snap_y, ctx->ybuf[ctx->ctrl_h->cur], used, cudaMemcpyDeviceToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->snap_state, ctx->state, used, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->snap_ctrl = *ctx->ctrl_h;
+  ctx->snap_valid = true;
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
+}
+
+int ivhd_restore(ivhd_ctx* ctx) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (!ctx->snap_valid) return fail(ctx, IVHD_ERR_STATE, "no snapshot taken");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const size_t used = sizeof(float) * 8 * ctx->m;
+  *ctx->ctrl_h = ctx->snap_ctrl;
+  CU(ctx, cudaMemcpyAsync(ctx->ybuf[ctx->snap_ctrl.cur], ctx->snap_y, used, cudaMemcpyDeviceToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->state, ctx->snap_state, used, cudaMemcpyDeviceToDevice, ctx->stream));
+  TRY(push_ctrl(ctx));
+  return IVHD_OK;  // asynchronous: ordered before the next launch on the stream
+}
+
+int ivhd_synchronize(ivhd_ctx* ctx) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
+}
+
+// ------------------------------------------------------------ sharded mode
+
+int ivhd_tile_vertices(ivhd_ctx* ctx, int64_t* tile_v_out, int64_t* n_tiles_out) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (tile_v_out) *tile_v_out = ctx->tile_v;
+  if (n_tiles_out) *n_tiles_out = ctx->n_tiles_cap;
+  return IVHD_OK;
+}
+
+int ivhd_shard_set_range(ivhd_ctx* ctx, int64_t v_begin, int64_t v_end) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (v_begin < 0 || v_end < v_begin || v_end > ctx->v_cap || v_begin % ctx->tile_v || v_end % ctx->tile_v)
+    return fail(ctx, IVHD_ERR_INVALID_ARG, "shard range [%lld, %lld) not tile aligned (tile %d, cap %lld)",
+                (long long)v_begin, (long long)v_end, ctx->tile_v, (long long)ctx->v_cap);
+  ctx->shard_begin = v_begin;
+  ctx->shard_end = v_end;
+  ctx->sharded = true;
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaMemsetAsync(ctx->partial, 0, sizeof(double4) * ctx->n_tiles_cap, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
+}
+
+int ivhd_shard_buffers(ivhd_ctx* ctx, uint64_t* ybuf0, uint64_t* ybuf1, int64_t* floats_per_vertex,
+                       uint64_t* partials, int* cur_out) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  TRY(pull_ctrl(ctx));
+  if (ybuf0) *ybuf0 = reinterpret_cast<uint64_t>(ctx->ybuf[0]);
+  if (ybuf1) *ybuf1 = reinterpret_cast<uint64_t>(ctx->ybuf[1]);
+  if (floats_per_vertex) *floats_per_vertex = ys_of(ctx->dim, ctx->opt.kind);
+  if (partials) *partials = reinterpret_cast<uint64_t>(ctx->partial);
+  if (cur_out) *cur_out = ctx->ctrl_h->cur;
+  return IVHD_OK;
+}
+
+int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c) {
+  TRY(check_ready(ctx, slot));
+  if (!ctx->sharded) return fail(ctx, IVHD_ERR_STATE, "call ivhd_shard_set_range first");
+  if (!ctx->pos_set) return fail(ctx, IVHD_ERR_STATE, "positions not set");
+  TRY(ensure_trace(ctx, 1));
+  TRY(pull_ctrl(ctx));
+  if (ctx->ctrl_h->status != 0) return fail(ctx, IVHD_ERR_DIVERGED, "context already diverged");
+  ctx->ctrl_h->c = c;
+  ctx->ctrl_h->iter = 0;
+  ctx->ctrl_h->arrive = 0;
+  ctx->ctrl_h->next_tile = 0;
+  TRY(push_ctrl(ctx));
+  const CsrSlot& S = ctx->slots[slot];
+  StepArgs A = make_args(ctx, slot, norm, 0);
+  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.G), A));
+  return IVHD_OK;
+}
+
+int ivhd_step_finalize(ivhd_ctx* ctx, double* stress_out, double* step_out, int* committed_out) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  StepArgs A = make_args(ctx, 0, 0, 0);
+  pick_finalize(ctx->opt.kind)<<<1, kBlock, 0, ctx->stream>>>(A);
+  CU(ctx, cudaGetLastError());
+  TRY(pull_ctrl(ctx));
+  double2 tr;
+  CU(ctx, cudaMemcpy(&tr, ctx->trace, sizeof(double2), cudaMemcpyDeviceToHost));
+  if (stress_out) *stress_out = tr.x;
+  if (step_out) *step_out = tr.y;
+  if (committed_out) *committed_out = ctx->ctrl_h->last_commit;
+  if (ctx->ctrl_h->status != 0) return fail(ctx, IVHD_ERR_DIVERGED, "embedding diverged");
+  return IVHD_OK;
+}
+
+}  // extern "C"

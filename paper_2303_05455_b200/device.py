@@ -1,0 +1,174 @@
+"""Thin owner of one `ivhd_ctx` (include/ivhd_b200.h).
+
+`DeviceEmbedding` keeps the whole particle system resident on one GPU: the
+symmetrised CSR of the main and the RNN-filtered connection sets, the two
+position buffers, the optimizer state and the trace.  Every method is a
+synchronous C-ABI call; nothing here computes on the CPU.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import c_f64p, c_i32p, c_i64p, c_u8p, check, f64, i32, ptr
+from .errors import InvalidArgumentError
+
+
+class DeviceEmbedding:
+    def __init__(self, m, dim, device=0, stream=0):
+        self.lib = _lib.load()
+        self.m = int(m)
+        self.dim = int(dim)
+        h = ctypes.c_void_p()
+        check(self.lib.ivhd_create(ctypes.byref(h), int(device), self.m, self.dim, int(stream)))
+        self.h = h
+
+    # ------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ivhd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, code):
+        check(code, self.h)
+
+    # ---------------------------------------------------------- connections
+    def set_graph(self, slot, nn_sets, rn_assign):
+        """Binary-mode connections: nn (M, ncols) view (row stride honoured)
+        and rn (M, rn).  engine.py:225-262."""
+        nn = np.asarray(nn_sets)
+        if nn.ndim != 2 or nn.shape[0] != self.m:
+            raise InvalidArgumentError("nn_sets must be (M, ncols)")
+        base = nn if (nn.dtype == np.int32 and nn.strides[1] == 4) else i32(nn)
+        stride = base.strides[0] // 4 if base.shape[1] > 0 else 0
+        if base.strides[0] % 4 or stride < base.shape[1]:
+            base = i32(nn)
+            stride = base.shape[1]
+        rn = i32(rn_assign)
+        self._check(self.lib.ivhd_set_graph(
+            self.h, int(slot), base.ctypes.data_as(c_i32p) if base.size else None, int(stride),
+            int(base.shape[1]), rn.ctypes.data_as(c_i32p) if rn.size else None,
+            int(rn.shape[1]) if rn.ndim == 2 else 0))
+
+    def set_connections(self, slot, edges, is_random, targets=None, scale=None):
+        e = i32(edges).reshape(-1, 2)
+        r = np.ascontiguousarray(is_random, dtype=np.uint8)
+        t = None if targets is None else f64(targets)
+        s = None if scale is None else f64(scale)
+        self._check(self.lib.ivhd_set_connections(
+            self.h, int(slot), ptr(e, ctypes.c_int32), ptr(r, ctypes.c_uint8),
+            ptr(t, ctypes.c_double), ptr(s, ctypes.c_double), int(e.shape[0])))
+
+    # ---------------------------------------------------------------- state
+    def set_positions(self, y):
+        y = f64(y)
+        if y.shape != (self.m, self.dim):
+            raise InvalidArgumentError(f"positions must be ({self.m}, {self.dim})")
+        self._check(self.lib.ivhd_set_positions(self.h, y.ctypes.data_as(c_f64p)))
+
+    def positions(self):
+        out = np.empty((self.m, self.dim))
+        self._check(self.lib.ivhd_get_positions(self.h, out.ctypes.data_as(c_f64p)))
+        return out
+
+    def deltas(self):
+        out = np.empty((self.m, self.dim))
+        self._check(self.lib.ivhd_get_deltas(self.h, out.ctypes.data_as(c_f64p)))
+        return out
+
+    def set_optimizer(self, params):
+        self._check(self.lib.ivhd_set_optimizer(self.h, ctypes.byref(params)))
+
+    def set_step_size(self, value):
+        self._check(self.lib.ivhd_set_step_size(self.h, float(value)))
+
+    def step_size(self):
+        v = ctypes.c_double()
+        self._check(self.lib.ivhd_get_step_size(self.h, ctypes.byref(v)))
+        return v.value
+
+    # ---------------------------------------------------------------- loops
+    def run(self, slot, norm, c, n_iter):
+        """Run n_iter iterations; returns (stress[], step[], done, diverged)."""
+        stress = np.empty(max(int(n_iter), 1))
+        step = np.empty(max(int(n_iter), 1))
+        done = ctypes.c_int64(0)
+        code = self.lib.ivhd_run(self.h, int(slot), _lib.NORM[norm], float(c), int(n_iter),
+                                 stress.ctypes.data_as(c_f64p), step.ctypes.data_as(c_f64p),
+                                 ctypes.byref(done))
+        if code == _lib.ERR_DIVERGED:
+            d = done.value
+            return stress[: d + 1], step[: d + 1], d, True
+        self._check(code)
+        return stress[: done.value], step[: done.value], done.value, False
+
+    def compute_forces(self, slot, norm, c, y):
+        y = f64(y)
+        f = np.empty((self.m, self.dim))
+        e = ctypes.c_double()
+        self._check(self.lib.ivhd_compute_forces(self.h, int(slot), _lib.NORM[norm], float(c),
+                                                 y.ctypes.data_as(c_f64p), f.ctypes.data_as(c_f64p),
+                                                 ctypes.byref(e)))
+        return f, e.value
+
+    def stress(self, slot, norm, c, y):
+        y = f64(y)
+        e = ctypes.c_double()
+        self._check(self.lib.ivhd_stress(self.h, int(slot), _lib.NORM[norm], float(c),
+                                         y.ctypes.data_as(c_f64p), ctypes.byref(e)))
+        return e.value
+
+    def synchronize(self):
+        self._check(self.lib.ivhd_synchronize(self.h))
+
+    def snapshot(self):
+        self._check(self.lib.ivhd_snapshot(self.h))
+
+    def restore(self):
+        self._check(self.lib.ivhd_restore(self.h))
+
+    # -------------------------------------------------------------- sharding
+    def tiles(self):
+        tv, nt = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.lib.ivhd_tile_vertices(self.h, ctypes.byref(tv), ctypes.byref(nt)))
+        return tv.value, nt.value
+
+    def shard_set_range(self, v_begin, v_end):
+        self._check(self.lib.ivhd_shard_set_range(self.h, int(v_begin), int(v_end)))
+
+    def shard_buffers(self):
+        y0, y1, p = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        fpv, cur = ctypes.c_int64(), ctypes.c_int()
+        self._check(self.lib.ivhd_shard_buffers(self.h, ctypes.byref(y0), ctypes.byref(y1),
+                                                ctypes.byref(fpv), ctypes.byref(p),
+                                                ctypes.byref(cur)))
+        return {"ybuf": (y0.value, y1.value), "floats_per_vertex": fpv.value,
+                "partials": p.value, "cur": cur.value}
+
+    def step_local(self, slot, norm, c):
+        self._check(self.lib.ivhd_step_local(self.h, int(slot), _lib.NORM[norm], float(c)))
+
+    def step_finalize(self):
+        e, s, com = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        code = self.lib.ivhd_step_finalize(self.h, ctypes.byref(e), ctypes.byref(s),
+                                           ctypes.byref(com))
+        if code == _lib.ERR_DIVERGED:
+            return e.value, s.value, bool(com.value), True
+        self._check(code)
+        return e.value, s.value, bool(com.value), False
+
+
+__all__ = ["DeviceEmbedding", "c_i64p", "c_u8p"]

@@ -1,0 +1,126 @@
+"""Operator-level drop-ins: ConnectionSet, compute_forces, stress, gradient
+(reference forces.py:20-186), evaluated by the same CUDA kernel as the loop.
+
+Differences from the reference, by design:
+* arithmetic is float32 per connection with float64 reductions (the kernel's
+  contract; normwise relative agreement ~1e-7);
+* the degenerate random-pair fallback (d == 0, t != 0; forces.py:167-174)
+  draws its unit direction from a device counter hash instead of `rng`, so
+  `rng` is accepted and ignored (the magnitude w*t is the same).
+"""
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from .device import DeviceEmbedding
+from .errors import DimensionMismatchError, InvalidArgumentError
+
+NORM_L2 = "l2"
+NORM_L1 = "l1"
+
+
+@dataclass
+class ConnectionSet:
+    """Directed connections (forces.py:20-67)."""
+
+    edges: np.ndarray
+    targets: np.ndarray
+    is_random: np.ndarray
+    scale: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.edges = np.asarray(self.edges, dtype=np.int32)
+        self.targets = np.asarray(self.targets, dtype=np.float64)
+        self.is_random = np.asarray(self.is_random, dtype=bool)
+        if self.edges.ndim != 2 or self.edges.shape[1] != 2:
+            raise DimensionMismatchError("edges must be (L, 2)")
+        n = len(self.edges)
+        if self.targets.shape != (n,) or self.is_random.shape != (n,):
+            raise DimensionMismatchError("targets/is_random must be length L")
+        if self.scale is not None:
+            self.scale = np.asarray(self.scale, dtype=np.float64)
+            if self.scale.shape != (n,):
+                raise DimensionMismatchError("scale must be length L")
+
+    def __len__(self):
+        return len(self.edges)
+
+    def weights(self, c):
+        w = np.where(self.is_random, c, 1.0)
+        return w if self.scale is None else w * self.scale
+
+
+def _is_binary(conn):
+    t = np.asarray(conn.targets)
+    r = np.asarray(conn.is_random, dtype=bool)
+    return bool(np.array_equal(t, r.astype(np.float64)))
+
+
+class _OpCache(threading.local):
+    """One device context per thread, re-used while (M, dim) and the
+    connection arrays are unchanged."""
+
+    dev = None
+    key = None
+    conn_key = None
+
+
+_cache = _OpCache()
+
+
+def _device_for(m, dim, conn, device):
+    key = (m, dim, device)
+    if _cache.dev is None or _cache.key != key:
+        if _cache.dev is not None:
+            _cache.dev.close()
+        _cache.dev = DeviceEmbedding(m, dim, device=device)
+        _cache.key = key
+        _cache.conn_key = None
+    edges = np.asarray(conn.edges)
+    scale = getattr(conn, "scale", None)
+    arrays = (edges, np.asarray(conn.targets), np.asarray(conn.is_random),
+              None if scale is None else np.asarray(scale))
+    held = _cache.conn_key
+    same = held is not None and all(
+        (a is None and b is None) or (a is not None and b is not None and a.shape == b.shape
+                                      and np.array_equal(a, b))
+        for a, b in zip(arrays, held))
+    if not same:
+        _cache.conn_key = None
+        binary = _is_binary(conn)
+        _cache.dev.set_connections(0, edges, np.asarray(conn.is_random, dtype=np.uint8),
+                                   None if binary else conn.targets, scale)
+        _cache.conn_key = tuple(None if a is None else a.copy() for a in arrays)
+    return _cache.dev
+
+
+def _check_norm(norm):
+    if norm not in (NORM_L1, NORM_L2):
+        raise InvalidArgumentError(f"unknown norm {norm!r}")
+
+
+def compute_forces(positions, conn, c, norm=NORM_L2, rng=None, threads=1, with_stress=False,
+                   device=0):
+    """Force = -1/2 grad E (forces.py:139-181) on the GPU."""
+    del rng, threads
+    _check_norm(norm)
+    y = np.asarray(positions, dtype=np.float64)
+    m, dim = y.shape
+    dev = _device_for(m, dim, conn, device)
+    f, e = dev.compute_forces(0, norm, c, y)
+    return (f, e) if with_stress else f
+
+
+def stress(positions, conn, c, norm=NORM_L2, device=0):
+    """E = sum_conn w (t - d)^2 (forces.py:78-83) on the GPU."""
+    _check_norm(norm)
+    y = np.asarray(positions, dtype=np.float64)
+    m, dim = y.shape
+    return _device_for(m, dim, conn, device).stress(0, norm, c, y)
+
+
+def gradient(positions, conn, c, norm=NORM_L2, rng=None, threads=1, device=0):
+    """grad E = -2 * compute_forces (forces.py:184-186)."""
+    return -2.0 * compute_forces(positions, conn, c, norm, device=device)
