@@ -27,7 +27,6 @@ struct CsrSlot {
   float2* ew = nullptr;         // [n] or nullptr (binary)
   int64_t n = 0;                // entries (2 * connections)
   int64_t cap = 0;
-  int G = 4;
   bool valid = false;
 };
 
@@ -50,7 +49,8 @@ struct ivhd_ctx {
   bool own_stream = false;
   int sm_count = 148;
 
-  int tile_v = 64;
+  int tile_v = 256;
+  int rpt = 1;  // rows per thread (tile = 256 * rpt vertices)
   int n_tiles = 0;
   int n_tiles_cap = 0;  // padded to a multiple of 8 (rank counts 1/2/4/8)
   int64_t v_cap = 0;    // vertex capacity of position/state buffers
@@ -122,22 +122,34 @@ inline int ys_of(int dim, int opt) { return (opt == OPT_NEST) ? (dim == 2 ? 4 : 
 
 // ------------------------------------------------------------ kernel table
 
-template <int DIM, int G>
+template <int DIM, int OPT, int RPT, bool W>
+KernelFn kfn() {
+  return step_kernel<DIM, OPT, RPT, ItemsPerThread<DIM, OPT>::value, W>;
+}
+
+template <int DIM, int RPT, bool W>
 KernelFn pick_opt(int opt) {
   switch (opt) {
-    case OPT_FD: return step_kernel<DIM, OPT_FD, G>;
-    case OPT_SGD: return step_kernel<DIM, OPT_SGD, G>;
-    case OPT_MOM: return step_kernel<DIM, OPT_MOM, G>;
-    case OPT_NEST: return step_kernel<DIM, OPT_NEST, G>;
-    case OPT_ADAM: return step_kernel<DIM, OPT_ADAM, G>;
-    case OPT_ADADELTA: return step_kernel<DIM, OPT_ADADELTA, G>;
-    default: return step_kernel<DIM, OPT_NONE, G>;
+    case OPT_FD: return kfn<DIM, OPT_FD, RPT, W>();
+    case OPT_SGD: return kfn<DIM, OPT_SGD, RPT, W>();
+    case OPT_MOM: return kfn<DIM, OPT_MOM, RPT, W>();
+    case OPT_NEST: return kfn<DIM, OPT_NEST, RPT, W>();
+    case OPT_ADAM: return kfn<DIM, OPT_ADAM, RPT, W>();
+    case OPT_ADADELTA: return kfn<DIM, OPT_ADADELTA, RPT, W>();
+    default: return kfn<DIM, OPT_NONE, RPT, W>();
   }
 }
 
-KernelFn pick_kernel(int dim, int opt, int G) {
-  if (dim == 2) return G == 4 ? pick_opt<2, 4>(opt) : (G == 8 ? pick_opt<2, 8>(opt) : pick_opt<2, 16>(opt));
-  return G == 4 ? pick_opt<3, 4>(opt) : (G == 8 ? pick_opt<3, 8>(opt) : pick_opt<3, 16>(opt));
+template <int DIM, bool W>
+KernelFn pick_rpt(int opt, int rpt) {
+  return rpt == 1 ? pick_opt<DIM, 1, W>(opt) : pick_opt<DIM, 2, W>(opt);
+}
+
+// rpt = rows per thread of a tile (tile = 256 * rpt vertices); weighted =
+// per-entry {target, scale} stream present (euclidean / RNN-filtered sets)
+KernelFn pick_kernel(int dim, int opt, int rpt, bool weighted) {
+  if (dim == 2) return weighted ? pick_rpt<2, true>(opt, rpt) : pick_rpt<2, false>(opt, rpt);
+  return weighted ? pick_rpt<3, true>(opt, rpt) : pick_rpt<3, false>(opt, rpt);
 }
 
 KernelFn pick_finalize(int opt) {
@@ -323,7 +335,6 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
   if (n == 0) {
     CU(ctx, cudaMemsetAsync(S.row_ptr, 0, sizeof(uint32_t) * (ctx->m + 1), st));
     CU(ctx, cudaStreamSynchronize(st));
-    S.G = 4;
     S.valid = true;
     return IVHD_OK;
   }
@@ -362,9 +373,6 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
   cleanup();
   if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "CSR build: %s", cudaGetErrorString(e));
   if (hbad) return fail(ctx, IVHD_ERR_INVALID_ARG, "connection endpoint outside [0, %lld)", (long long)ctx->m);
-  // lanes per row: nearest power of two to the mean symmetrised degree
-  const double mean = (double)n / (double)ctx->m;
-  S.G = mean <= 8.0 ? 4 : (mean <= 20.0 ? 8 : 16);
   S.valid = true;
   return IVHD_OK;
 }
@@ -480,8 +488,8 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   }
   // Fixed tile size (a function of M only): the reduction order is the same
   // for any grid size and any number of ranks.
-  int64_t tv = 64;
-  while (tv < 4096 && tv * 4096 <= m) tv <<= 1;
+  ctx->rpt = m >= (1 << 18) ? 2 : 1;
+  const int64_t tv = (int64_t)kBlock * ctx->rpt;
   ctx->tile_v = (int)tv;
   ctx->n_tiles = (int)((m + tv - 1) / tv);
   ctx->n_tiles_cap = (ctx->n_tiles + 7) / 8 * 8;
@@ -770,12 +778,12 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   ctx->ctrl_h->next_tile = 0;
   TRY(push_ctrl(ctx));
   const CsrSlot& S = ctx->slots[slot];
-  KernelFn fn = pick_kernel(ctx->dim, ctx->opt.kind, S.G);
+  KernelFn fn = pick_kernel(ctx->dim, ctx->opt.kind, ctx->rpt, S.ew != nullptr);
   const StepArgs A = make_args(ctx, slot, norm, 1);
   int64_t left = n_iter;
   const int chunk = ctx->graph_chunk;
   if (left >= chunk) {
-    const GraphKey key{slot, norm, ctx->opt.kind, S.G};
+    const GraphKey key{slot, norm, ctx->opt.kind, ctx->rpt * 2 + (S.ew != nullptr)};
     auto it = ctx->graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (it == ctx->graphs.end()) {
@@ -851,7 +859,7 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   A.n_tiles_global = ctx->n_tiles;
   A.norm = norm;
   A.fuse_finalize = 0;
-  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, S.G), A));
+  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, ctx->rpt, S.ew != nullptr), A));
   k_reduce_partials<<<1, kBlock, 0, ctx->stream>>>(ctx->partial, ctx->n_tiles, ctx->red_out);
   CU(ctx, cudaGetLastError());
   double4 red;
@@ -956,9 +964,9 @@ int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c) {
   ctx->ctrl_h->arrive = 0;
   ctx->ctrl_h->next_tile = 0;
   TRY(push_ctrl(ctx));
-  const CsrSlot& S = ctx->slots[slot];
   StepArgs A = make_args(ctx, slot, norm, 0);
-  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.G), A));
+  const CsrSlot& S = ctx->slots[slot];
+  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, ctx->rpt, S.ew != nullptr), A));
   return IVHD_OK;
 }
 

@@ -32,7 +32,16 @@
 
 namespace ivhd {
 
+
 constexpr int kBlock = 256;
+
+// Block barrier.  __syncthreads() lowers to the *aligned* bar.sync, which
+// assumes every warp arrives converged; after the data-dependent merge-path
+// walk, lanes of one warp can arrive separately (independent thread
+// scheduling) and the aligned barrier then let early lanes through (observed
+// on B200 / CUDA 12.9).  The non-aligned barrier.sync counts threads.
+__device__ __forceinline__ void block_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
 constexpr uint32_t kRandBit = 0x80000000u;
 constexpr uint32_t kIdMask = 0x7fffffffu;
 
@@ -171,16 +180,15 @@ __device__ __noinline__ void degenerate_dir(uint32_t i, uint32_t j, long long st
 template <int DIM, bool NEST>
 __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[DIM],
                                       const float (&yo)[DIM], const float (&lo)[DIM],
-                                      uint32_t cw, const float2* __restrict__ ew, uint32_t k,
+                                      uint32_t cw, bool weighted, float2 tw,
                                       float c, int norm, uint32_t i, long long step,
                                       float (&f)[DIM], float& e) {
   const bool rn = cw & kRandBit;
   float t, w;
-  if (ew == nullptr) {
+  if (!weighted) {
     t = rn ? 1.f : 0.f;
     w = rn ? c : 1.f;
   } else {
-    const float2 tw = __ldg(ew + k);
     t = tw.x;
     w = (rn ? c : 1.f) * tw.y;
   }
@@ -236,13 +244,6 @@ __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[
   e = fmaf(w * r, r, e);
 }
 
-template <int G>
-__device__ __forceinline__ float group_sum(float x) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
 __device__ __forceinline__ bool all_finite(const float* v, int n) {
   bool ok = true;
   for (int d = 0; d < n; ++d) ok &= isfinite(v[d]);
@@ -261,28 +262,42 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double4* sm /*[kBlock/3
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v.x = warp_dsum(v.x); v.y = warp_dsum(v.y); v.z = warp_dsum(v.z); v.w = warp_dsum(v.w);
   if (lane == 0) sm[warp] = v;
-  __syncthreads();
+  block_sync();
   double4 r = make_double4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     for (int w = 0; w < kBlock / 32; ++w) {
       r.x += sm[w].x; r.y += sm[w].y; r.z += sm[w].z; r.w += sm[w].w;
     }
   }
-  __syncthreads();
+  block_sync();
   return r;  // valid in thread 0
 }
 
 // ---------------------------------------------------------------- finalize
 // Reduce all tile partials in a fixed order and take the iteration decision
-// (optim.py:80-92 + engine.py:373-384).  Executed by ONE whole block.
+// (optim.py:80-92 + engine.py:373-384).  Executed by ONE whole block; each
+// thread keeps 8 tiles in flight so the tail is ~one memory round trip.
 template <int OPT>
 __device__ void finalize_block(const StepArgs& A, double4* sm) {
   Ctrl* ctrl = A.ctrl;
+  const double2* p2 = reinterpret_cast<const double2*>(A.partial);
   double4 s = make_double4(0, 0, 0, 0);
-  for (int t = threadIdx.x; t < A.n_tiles_global; t += kBlock) {
-    const double2 p0 = __ldcg(reinterpret_cast<const double2*>(A.partial + t));
-    const double2 p1 = __ldcg(reinterpret_cast<const double2*>(A.partial + t) + 1);
-    s.x += p0.x; s.y += p0.y; s.z += p1.x; s.w += p1.y;
+  for (int t0 = threadIdx.x; t0 < A.n_tiles_global; t0 += 8 * kBlock) {
+    double2 a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * kBlock;
+      if (t < A.n_tiles_global) {
+        a[u] = __ldcg(p2 + 2 * t);
+        b[u] = __ldcg(p2 + 2 * t + 1);
+      } else {
+        a[u] = b[u] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s.x += a[u].x; s.y += a[u].y; s.z += b[u].x; s.w += b[u].y;
+    }
   }
   s = block_sum4(s, sm);
   if (threadIdx.x == 0) {
@@ -318,12 +333,156 @@ __device__ void finalize_block(const StepArgs& A, double4* sm) {
   }
 }
 
-// ------------------------------------------------------------------ kernel
+// ---------------------------------------------------------- merge path
+// Tile-local merge path of row ends (s_re[r] = end of row r, local entry
+// index) and entries: row-end r sits at diagonal s_re[r] + r.  Returns the
+// number of rows whose end item lies before diagonal d.
+__device__ __forceinline__ int merge_search(const uint32_t* s_re, int nrows, int d) {
+  int lo = 0, hi = nrows;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)s_re[mid] + mid < d) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
 
-template <int DIM, int OPT, int G>
-__global__ void __launch_bounds__(kBlock) step_kernel(StepArgs A) {
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+template <int SS>
+__device__ __forceinline__ void ld_state(const float* p, float (&s)[SS > 0 ? SS : 1]) {
+  if constexpr (SS == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    s[0] = t.x; s[1] = t.y;
+  } else if constexpr (SS == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    s[0] = t.x; s[1] = t.y; s[2] = t.z; s[3] = t.w;
+  } else if constexpr (SS == 8) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    const float4 u = *reinterpret_cast<const float4*>(p + 4);
+    s[0] = t.x; s[1] = t.y; s[2] = t.z; s[3] = t.w; s[4] = u.x; s[5] = u.y; s[6] = u.z; s[7] = u.w;
+  }
+}
+
+template <int SS>
+__device__ __forceinline__ void st_state(float* p, const float (&s)[SS > 0 ? SS : 1]) {
+  if constexpr (SS == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(s[0], s[1]);
+  } else if constexpr (SS == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(s[0], s[1], s[2], s[3]);
+  } else if constexpr (SS == 8) {
+    *reinterpret_cast<float4*>(p) = make_float4(s[0], s[1], s[2], s[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(s[4], s[5], s[6], s[7]);
+  }
+}
+
+// Optimizer update of one vertex (optim.py:95-236 with step_optimizer's
+// grad = -2 force, optim.py:259-263).  State vectors live in sv: FD delta /
+// momentum velocity at [0, DIM); Adam (v, s) and Adadelta (E[g^2], E[d^2])
+// at [0, DIM) and [V, V+DIM) with V = 2 (dim 2) or 4 (dim 3).
+template <int DIM, int OPT>
+__device__ __forceinline__ void apply_update(const StepArgs& A, float* __restrict__ Yout, long long v,
+                                             const float (&yi)[DIM], float (&sv)[Layout<DIM, OPT>::SS > 0 ? Layout<DIM, OPT>::SS : 1],
+                                             const float (&f)[DIM], float step, float bc1, float bc2,
+                                             double& acc_n, double& acc_o, double& acc_bad) {
+  using L = Layout<DIM, OPT>;
+  constexpr int V = DIM == 2 ? 2 : 4;
+  float yn[DIM];
+  if constexpr (OPT == OPT_FD) {
+    double so = 0.0, sn = 0.0;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const float dn = fmaf(A.h.a, sv[d], step * f[d]);
+      so += (double)sv[d] * (double)sv[d];
+      sn += (double)dn * (double)dn;
+      sv[d] = dn;
+      yn[d] = yi[d] + dn;
+    }
+    acc_o += so;
+    acc_n += sn;
+  } else if constexpr (OPT == OPT_SGD) {
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) yn[d] = yi[d] - step * (-2.f * f[d]);
+  } else if constexpr (OPT == OPT_MOM || OPT == OPT_NEST) {
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      sv[d] = A.h.beta * sv[d] - step * (-2.f * f[d]);
+      yn[d] = yi[d] + sv[d];
+    }
+  } else if constexpr (OPT == OPT_ADAM) {
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const float g = -2.f * f[d];
+      sv[d] = A.h.gv * sv[d] + (1.f - A.h.gv) * g;
+      sv[V + d] = A.h.gs * sv[V + d] + (1.f - A.h.gs) * g * g;
+      yn[d] = yi[d] - step * (sv[d] * bc1) / (A.h.eps + sqrtf(sv[V + d] * bc2));
+    }
+  } else if constexpr (OPT == OPT_ADADELTA) {
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const float g = -2.f * f[d];
+      sv[d] = A.h.rho * sv[d] + (1.f - A.h.rho) * g * g;
+      const float dl = -step * sqrtf(sv[V + d] + A.h.eps) / sqrtf(sv[d] + A.h.eps) * g;
+      sv[V + d] = A.h.rho * sv[V + d] + (1.f - A.h.rho) * dl * dl;
+      yn[d] = yi[d] + dl;
+    }
+  }
+  if constexpr (L::SS > 0) st_state<L::SS>(A.state + (size_t)v * L::SS, sv);
+  if constexpr (OPT == OPT_NEST) {
+    float la[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) la[d] = yn[d] + A.h.beta * sv[d];  // optim.py:174-175
+    if constexpr (DIM == 2) {
+      *reinterpret_cast<float4*>(Yout + (size_t)v * 4) = make_float4(yn[0], yn[1], la[0], la[1]);
+    } else {
+      *reinterpret_cast<float4*>(Yout + (size_t)v * 8) = make_float4(yn[0], yn[1], yn[2], 0.f);
+      *reinterpret_cast<float4*>(Yout + (size_t)v * 8 + 4) = make_float4(la[0], la[1], la[2], 0.f);
+    }
+  } else {
+    st_vec<DIM>(Yout + (size_t)v * L::YS, yn);
+  }
+  acc_bad += all_finite(yn, DIM) ? 0.0 : 1.0;
+}
+
+// Store one row partial produced by a thread walking entries [js, je):
+// complete rows go to s_row[r]; a row that starts here and continues goes to
+// s_tail[tid]; a row continued from an earlier thread goes to s_head[tid].
+template <int DIM>
+__device__ __forceinline__ void emit_row(int r, const float (&f)[DIM], float e, int js, int je,
+                                         const uint32_t* s_re, float4* s_row, float4* s_head,
+                                         float4* s_tail) {
+  const int rs = r > 0 ? (int)s_re[r - 1] : 0;
+  const int re = (int)s_re[r];
+  const bool started = rs >= js;
+  float4* dst = started ? (re <= je ? &s_row[r] : &s_tail[threadIdx.x]) : &s_head[threadIdx.x];
+  if constexpr (DIM == 2) *dst = make_float4(f[0], f[1], e, 0.f);
+  else *dst = make_float4(f[0], f[1], f[2], e);
+}
+
+// ------------------------------------------------------------------ kernel
+// Tile = TV = 256*RPT consecutive vertices.  Its rows' entries are walked as
+// one merge path of (row ends + entries); each thread owns P consecutive
+// items, so its column loads and position gathers are issued as one batch
+// and hub rows are split evenly across threads.  A row touching several
+// threads is summed as tail(first thread) + head(next) + ... in thread
+// order (deterministic); rows spanning a round of 256*P items carry over in
+// s_carry.  The thread owning row r (r mod 256) applies the optimizer.
+template <int DIM, int OPT, int RPT, int P, bool WEIGHTED>
+__global__ void __launch_bounds__(kBlock, 2) step_kernel(StepArgs A) {
   using L = Layout<DIM, OPT>;
   constexpr bool NEST = (OPT == OPT_NEST);
+  constexpr int TV = kBlock * RPT;
+  constexpr int ITEMS = kBlock * P;
+  constexpr int YS = L::YS;
+  constexpr int SSX = L::SS > 0 ? L::SS : 1;
+
+  __shared__ __align__(16) float s_y[TV * YS];
+  __shared__ float4 s_row[TV];
+  __shared__ float4 s_head[kBlock];
+  __shared__ float4 s_tail[kBlock];
+  __shared__ uint32_t s_re[TV];
+  __shared__ float4 s_carry[2];  // double-buffered by round parity
   __shared__ double4 sm_red[kBlock / 32];
   __shared__ int sm_tile;
 
@@ -335,180 +494,180 @@ __global__ void __launch_bounds__(kBlock) step_kernel(StepArgs A) {
   const long long gstep = ctrl->gstep;
   const float* __restrict__ Yin = cur ? A.ybuf1 : A.ybuf0;
   float* __restrict__ Yout = cur ? A.ybuf0 : A.ybuf1;
+  const int tid = threadIdx.x;
 
-  // Adam bias corrections (optim.py:200-204), fp64 like the reference's scalars.
-  float bc1 = 1.f, bc2 = 1.f;
+  float bc1 = 1.f, bc2 = 1.f;  // Adam bias corrections (optim.py:203-204)
   if constexpr (OPT == OPT_ADAM) {
     const double tt = (double)(ctrl->adam_t + 1);
     bc1 = (float)(1.0 / (1.0 - pow((double)A.h.gv, tt)));
     bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
   }
 
-  const int lg = threadIdx.x % G;
-  const int grp = threadIdx.x / G;
-  constexpr int kGroups = kBlock / G;
-
   while (true) {
-    if (threadIdx.x == 0) sm_tile = (int)atomicAdd(&ctrl->next_tile, 1u);
-    __syncthreads();
+    if (tid == 0) sm_tile = (int)atomicAdd(&ctrl->next_tile, 1u);
+    block_sync();
     const int tile = sm_tile;
-    __syncthreads();
     if (tile >= A.n_tiles) break;
-    const long long v0 = A.v_begin + (long long)tile * A.tile_v;
-    const long long v1 = min(v0 + (long long)A.tile_v, A.v_end);
-
+    const long long v0 = A.v_begin + (long long)tile * TV;
+    const int nrows = (int)max(0LL, min((long long)TV, A.v_end - v0));
     double acc_e = 0.0, acc_n = 0.0, acc_o = 0.0, acc_bad = 0.0;
-    // vb advances uniformly over the block so every lane reaches the group
-    // shuffles; lanes past the tile end carry an empty row.
-    for (long long vb = v0; vb < v1; vb += kGroups) {
-      const long long v = vb + grp;
-      const bool active = v < v1;
-      uint32_t beg = 0, end = 0;
-      float yi[DIM], li[DIM];
-      if (active) {
-        beg = __ldg(A.row_ptr + v);
-        end = __ldg(A.row_ptr + v + 1);
-        gather<DIM, NEST>(Yin, (uint32_t)v, yi, li);
-      } else {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) yi[d] = li[d] = 0.f;
-      }
-      float f[DIM];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) f[d] = 0.f;
-      float e = 0.f;
-      uint32_t k = beg + lg;
-      // two entries in flight per lane
-      for (; k + G < end; k += 2 * G) {
-        const uint32_t c0 = __ldg(A.col + k), c1 = __ldg(A.col + k + G);
-        float y0[DIM], l0[DIM], y1[DIM], l1[DIM];
-        gather<DIM, NEST>(Yin, c0 & kIdMask, y0, l0);
-        gather<DIM, NEST>(Yin, c1 & kIdMask, y1, l1);
-        entry<DIM, NEST>(yi, li, y0, l0, c0, A.ew, k, c, A.norm, (uint32_t)v, gstep, f, e);
-        entry<DIM, NEST>(yi, li, y1, l1, c1, A.ew, k + G, c, A.norm, (uint32_t)v, gstep, f, e);
-      }
-      if (k < end) {
-        const uint32_t c0 = __ldg(A.col + k);
-        float y0[DIM], l0[DIM];
-        gather<DIM, NEST>(Yin, c0 & kIdMask, y0, l0);
-        entry<DIM, NEST>(yi, li, y0, l0, c0, A.ew, k, c, A.norm, (uint32_t)v, gstep, f, e);
-      }
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) f[d] = group_sum<G>(f[d]);
-      e = group_sum<G>(e);
-      if (!active || lg != 0) continue;
-      acc_e += (double)e;
 
-      // ------------------------------------------------ optimizer update
-      if constexpr (OPT == OPT_NONE) {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)f[d];
+    if (nrows > 0) {
+      // ---- round trip 1: row ends, the tile's positions, owners' state
+      const uint32_t e0 = __ldg(A.row_ptr + v0);
+      for (int r = tid; r < nrows; r += kBlock) s_re[r] = __ldg(A.row_ptr + v0 + r + 1) - e0;
+      if constexpr (YS % 4 == 0) {
+        const float4* src = reinterpret_cast<const float4*>(Yin + (size_t)v0 * YS);
+        for (int q = tid; q < nrows * YS / 4; q += kBlock) reinterpret_cast<float4*>(s_y)[q] = __ldg(src + q);
       } else {
-        float* st = A.state + (size_t)v * L::SS;
-        float yn[DIM];
-        if constexpr (OPT == OPT_FD) {
-          // optim.py:113-124: delta <- a*delta + b*f; y <- y + delta (maybe rolled back)
-          float dl[DIM], dn[DIM];
-          ld_vec<DIM>(st, dl);
-          double so = 0.0, sn = 0.0;
+        const float2* src = reinterpret_cast<const float2*>(Yin + (size_t)v0 * YS);
+        for (int q = tid; q < nrows * YS / 2; q += kBlock) reinterpret_cast<float2*>(s_y)[q] = __ldg(src + q);
+      }
+      float sv[RPT][SSX];
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            dn[d] = fmaf(A.h.a, dl[d], step * f[d]);
-            yn[d] = yi[d] + dn[d];
-            so += (double)dl[d] * (double)dl[d];
-            sn += (double)dn[d] * (double)dn[d];
-          }
-          st_vec<DIM>(st, dn);
-          acc_o += so;
-          acc_n += sn;
-        } else if constexpr (OPT == OPT_SGD) {
-          // optim.py:140-141 with grad = -2 f (optim.py:259-263)
+      for (int kk = 0; kk < RPT; ++kk) {
+        const int r = tid + kk * kBlock;
+        if constexpr (L::SS > 0) {
+          if (r < nrows) ld_state<L::SS>(A.state + (size_t)(v0 + r) * L::SS, sv[kk]);
+        }
+      }
+      block_sync();
+      const int E = (int)s_re[nrows - 1];
+      const int total = nrows + E;
+
+      for (int base = 0, round = 0; base < total; base += ITEMS, ++round) {
+        const float4* carry_in = &s_carry[round & 1];
+        const int d0 = min(base + tid * P, total), d1 = min(d0 + P, total);
+        const int i0 = merge_search(s_re, nrows, d0);
+        const int i1 = merge_search(s_re, nrows, d1);
+        const int js = d0 - i0, ne = (d1 - i1) - js;
+        const int je = js + ne;
+        // ---- round trip 2 + 3: this thread's entries, then their positions
+        uint32_t cw[P];
+        float2 tw[WEIGHTED ? P : 1];
+        float gy[P][DIM], gl[P][DIM];
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) yn[d] = yi[d] - step * (-2.f * f[d]);
-        } else if constexpr (OPT == OPT_MOM || OPT == OPT_NEST) {
-          // optim.py:161-163: v <- beta v - alpha g; y <- y + v
-          float vv[DIM];
-          ld_vec<DIM>(st, vv);
+        for (int q = 0; q < P; ++q)
+          if (q < ne) cw[q] = __ldg(A.col + e0 + js + q);
+        if constexpr (WEIGHTED) {
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            vv[d] = A.h.beta * vv[d] - step * (-2.f * f[d]);
-            yn[d] = yi[d] + vv[d];
-          }
-          st_vec<DIM>(st, vv);
-          if constexpr (NEST) {
-            float la[DIM];
+          for (int q = 0; q < P; ++q)
+            if (q < ne) tw[q] = __ldg(A.ew + e0 + js + q);
+        }
 #pragma unroll
-            for (int d = 0; d < DIM; ++d) la[d] = yn[d] + A.h.beta * vv[d];  // optim.py:174-175
-            if constexpr (DIM == 2) {
-              *reinterpret_cast<float4*>(Yout + (size_t)v * 4) = make_float4(yn[0], yn[1], la[0], la[1]);
-            } else {
-              *reinterpret_cast<float4*>(Yout + (size_t)v * 8) = make_float4(yn[0], yn[1], yn[2], 0.f);
-              *reinterpret_cast<float4*>(Yout + (size_t)v * 8 + 4) = make_float4(la[0], la[1], la[2], 0.f);
+        for (int q = 0; q < P; ++q)
+          if (q < ne) gather<DIM, NEST>(Yin, cw[q] & kIdMask, gy[q], gl[q]);
+        // ---- walk: accumulate per row, emit at row changes
+        int cr = i0;
+        bool open = false;
+        float f[DIM];
+        float e = 0.f;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) f[d] = 0.f;
+#ifdef IVHD_NOUNROLL_WALK
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
+        for (int q = 0; q < P; ++q) {
+          if (q < ne) {
+            const int j = js + q;
+            int r = cr;
+            while ((int)s_re[r] <= j) ++r;
+            if (open && r != cr) {
+              emit_row<DIM>(cr, f, e, js, je, s_re, s_row, s_head, s_tail);
+#pragma unroll
+              for (int d = 0; d < DIM; ++d) f[d] = 0.f;
+              e = 0.f;
             }
-          }
-        } else if constexpr (OPT == OPT_ADAM) {
-          // optim.py:199-205
-          float m1[DIM], m2[DIM];
-          if constexpr (DIM == 2) {
-            float4 s4 = *reinterpret_cast<const float4*>(st);
-            m1[0] = s4.x; m1[1] = s4.y; m2[0] = s4.z; m2[1] = s4.w;
-          } else {
-            ld_vec<3>(st, m1);
-            ld_vec<3>(st + 4, m2);
-          }
+            cr = r;
+            open = true;
+            float yi[DIM], li[DIM];
+            const float* ys = s_y + r * YS;
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            const float g = -2.f * f[d];
-            m1[d] = A.h.gv * m1[d] + (1.f - A.h.gv) * g;
-            m2[d] = A.h.gs * m2[d] + (1.f - A.h.gs) * g * g;
-            yn[d] = yi[d] - step * (m1[d] * bc1) / (A.h.eps + sqrtf(m2[d] * bc2));
-          }
-          if constexpr (DIM == 2) {
-            *reinterpret_cast<float4*>(st) = make_float4(m1[0], m1[1], m2[0], m2[1]);
-          } else {
-            st_vec<3>(st, m1);
-            st_vec<3>(st + 4, m2);
-          }
-        } else if constexpr (OPT == OPT_ADADELTA) {
-          // optim.py:227-236
-          float sg[DIM], sd[DIM];
-          if constexpr (DIM == 2) {
-            float4 s4 = *reinterpret_cast<const float4*>(st);
-            sg[0] = s4.x; sg[1] = s4.y; sd[0] = s4.z; sd[1] = s4.w;
-          } else {
-            ld_vec<3>(st, sg);
-            ld_vec<3>(st + 4, sd);
-          }
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            const float g = -2.f * f[d];
-            sg[d] = A.h.rho * sg[d] + (1.f - A.h.rho) * g * g;
-            const float dl = -step * sqrtf(sd[d] + A.h.eps) / sqrtf(sg[d] + A.h.eps) * g;
-            sd[d] = A.h.rho * sd[d] + (1.f - A.h.rho) * dl * dl;
-            yn[d] = yi[d] + dl;
-          }
-          if constexpr (DIM == 2) {
-            *reinterpret_cast<float4*>(st) = make_float4(sg[0], sg[1], sd[0], sd[1]);
-          } else {
-            st_vec<3>(st, sg);
-            st_vec<3>(st + 4, sd);
+            for (int d = 0; d < DIM; ++d) {
+              yi[d] = ys[d];
+              li[d] = NEST ? ys[(DIM == 2 ? 2 : 4) + d] : ys[d];
+            }
+            float2 twq = make_float2(0.f, 0.f);
+            if constexpr (WEIGHTED) twq = tw[q];
+            entry<DIM, NEST>(yi, li, gy[q], gl[q], cw[q], WEIGHTED, twq,
+                             c, A.norm, (uint32_t)(v0 + r), gstep, f, e);
           }
         }
-        if constexpr (!NEST) st_vec<DIM>(Yout + (size_t)v * L::YS, yn);
-        acc_bad += all_finite(yn, DIM) ? 0.0 : 1.0;
+        if (open) emit_row<DIM>(cr, f, e, js, je, s_re, s_row, s_head, s_tail);
+        block_sync();
+
+        // ---- resolve the rows whose end item lies in this round
+        auto chain = [&](int r, int tlast) {
+          const int rs = r > 0 ? (int)s_re[r - 1] : 0;
+          const int da = rs + r;
+          int t;
+          float4 sum;
+          if (da >= base) {
+            t = (da - base) / P;
+            sum = s_tail[t];
+          } else {
+            t = -1;
+            sum = *carry_in;
+          }
+          for (++t; t <= tlast; ++t) sum = f4add(sum, s_head[t]);
+          return sum;
+        };
+#pragma unroll
+        for (int kk = 0; kk < RPT; ++kk) {
+          const int r = tid + kk * kBlock;
+          if (r >= nrows) continue;
+          const int pe = (int)s_re[r] + r;
+          if (pe < base || pe >= base + ITEMS) continue;
+          const int rs = r > 0 ? (int)s_re[r - 1] : 0;
+          const int re = (int)s_re[r];
+          float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (re > rs) {
+            const int da = rs + r, db = re - 1 + r;
+            if (da / P == db / P) sum = s_row[r];
+            else sum = chain(r, db >= base ? (db - base) / P : -1);
+          }
+          float fr[DIM];
+          fr[0] = sum.x;
+          fr[1] = sum.y;
+          if constexpr (DIM == 3) fr[2] = sum.z;
+          acc_e += (double)(DIM == 2 ? sum.z : sum.w);
+          const long long v = v0 + r;
+          if constexpr (OPT == OPT_NONE) {
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)fr[d];
+          } else {
+            float yi[DIM];
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) yi[d] = s_y[r * YS + d];
+            apply_update<DIM, OPT>(A, Yout, v, yi, sv[kk], fr, step, bc1, bc2, acc_n, acc_o, acc_bad);
+          }
+        }
+        // ---- carry the row that is still open at the round boundary
+        if (tid == 0 && base + ITEMS < total) {
+          const int ib = merge_search(s_re, nrows, base + ITEMS);
+          const int jb = base + ITEMS - ib;
+          const int rs = ib > 0 ? (int)s_re[ib - 1] : 0;
+          if (ib < nrows && jb > rs) {
+            const int da = rs + ib, db = (int)s_re[ib] - 1 + ib;
+            if (da / P != db / P) s_carry[(round + 1) & 1] = chain(ib, (jb - 1 + ib - base) / P);
+          }
+        }
+        block_sync();
       }
     }
     const double4 tot = block_sum4(make_double4(acc_e, acc_n, acc_o, acc_bad), sm_red);
-    if (threadIdx.x == 0) A.partial[A.tile0 + tile] = tot;
+    if (tid == 0) A.partial[A.tile0 + tile] = tot;
   }
 
   if (!A.fuse_finalize) return;
   // last-block-done: the block that retires last reduces and decides
   __shared__ bool sm_last;
   __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) sm_last = (atomicAdd(&ctrl->arrive, 1u) == gridDim.x - 1);
-  __syncthreads();
+  block_sync();
+  if (tid == 0) sm_last = (atomicAdd(&ctrl->arrive, 1u) == gridDim.x - 1);
+  block_sync();
   if (!sm_last) return;
   __threadfence();
   finalize_block<OPT>(A, sm_red);
@@ -521,5 +680,10 @@ __global__ void __launch_bounds__(kBlock) finalize_kernel(StepArgs A) {
   if (A.ctrl->status != 0) return;
   finalize_block<OPT>(A, sm_red);
 }
+
+// Items per thread: sized so the batched gathers fit in registers.
+template <int DIM, int OPT> struct ItemsPerThread {
+  static constexpr int value = (OPT == OPT_NEST) ? (DIM == 2 ? 6 : 4) : (DIM == 2 ? 12 : 6);
+};
 
 }  // namespace ivhd
