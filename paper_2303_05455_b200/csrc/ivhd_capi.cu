@@ -25,6 +25,10 @@ struct CsrSlot {
   uint32_t* row_ptr = nullptr;  // [M+1]
   uint32_t* col = nullptr;      // [n]
   float2* ew = nullptr;         // [n] or nullptr (binary)
+  uint8_t* tile_g = nullptr;    // [n_tiles_cap] lanes per vertex of each tile
+  int* units = nullptr;         // work units (tile << 6 | pass), tile-major order
+  int n_units = 0;
+  std::vector<int> unit_base;   // host: first unit of each tile (n_tiles_cap + 1)
   int64_t n = 0;                // entries (2 * connections)
   int64_t cap = 0;
   bool valid = false;
@@ -49,13 +53,18 @@ struct ivhd_ctx {
   bool own_stream = false;
   int sm_count = 148;
 
-  int tile_v = 256;
-  int rpt = 1;  // rows per thread (tile = 256 * rpt vertices)
+  int tile_v = kBlock;  // vertices per tile (fixed: reduction order independent of grid/ranks)
   int n_tiles = 0;
   int n_tiles_cap = 0;  // padded to a multiple of 8 (rank counts 1/2/4/8)
   int64_t v_cap = 0;    // vertex capacity of position/state buffers
 
   CsrSlot slots[2];
+  // Vertex relabelling (new id -> old id and back), fixed by the first CSR
+  // build: vertices sorted by descending degree so a tile's rows have
+  // near-equal length.  All device vertex arrays are in the new order.
+  int32_t* perm = nullptr;
+  int32_t* inv = nullptr;
+  bool perm_fixed = false;
 
   float* ybuf[2] = {nullptr, nullptr};  // 8 floats/vertex capacity
   float* state = nullptr;               // 8 floats/vertex capacity
@@ -122,34 +131,23 @@ inline int ys_of(int dim, int opt) { return (opt == OPT_NEST) ? (dim == 2 ? 4 : 
 
 // ------------------------------------------------------------ kernel table
 
-template <int DIM, int OPT, int RPT, bool W>
-KernelFn kfn() {
-  return step_kernel<DIM, OPT, RPT, ItemsPerThread<DIM, OPT>::value, W>;
-}
-
-template <int DIM, int RPT, bool W>
+template <int DIM, bool W>
 KernelFn pick_opt(int opt) {
   switch (opt) {
-    case OPT_FD: return kfn<DIM, OPT_FD, RPT, W>();
-    case OPT_SGD: return kfn<DIM, OPT_SGD, RPT, W>();
-    case OPT_MOM: return kfn<DIM, OPT_MOM, RPT, W>();
-    case OPT_NEST: return kfn<DIM, OPT_NEST, RPT, W>();
-    case OPT_ADAM: return kfn<DIM, OPT_ADAM, RPT, W>();
-    case OPT_ADADELTA: return kfn<DIM, OPT_ADADELTA, RPT, W>();
-    default: return kfn<DIM, OPT_NONE, RPT, W>();
+    case OPT_FD: return step_kernel<DIM, OPT_FD, W>;
+    case OPT_SGD: return step_kernel<DIM, OPT_SGD, W>;
+    case OPT_MOM: return step_kernel<DIM, OPT_MOM, W>;
+    case OPT_NEST: return step_kernel<DIM, OPT_NEST, W>;
+    case OPT_ADAM: return step_kernel<DIM, OPT_ADAM, W>;
+    case OPT_ADADELTA: return step_kernel<DIM, OPT_ADADELTA, W>;
+    default: return step_kernel<DIM, OPT_NONE, W>;
   }
 }
 
-template <int DIM, bool W>
-KernelFn pick_rpt(int opt, int rpt) {
-  return rpt == 1 ? pick_opt<DIM, 1, W>(opt) : pick_opt<DIM, 2, W>(opt);
-}
-
-// rpt = rows per thread of a tile (tile = 256 * rpt vertices); weighted =
-// per-entry {target, scale} stream present (euclidean / RNN-filtered sets)
-KernelFn pick_kernel(int dim, int opt, int rpt, bool weighted) {
-  if (dim == 2) return weighted ? pick_rpt<2, true>(opt, rpt) : pick_rpt<2, false>(opt, rpt);
-  return weighted ? pick_rpt<3, true>(opt, rpt) : pick_rpt<3, false>(opt, rpt);
+// weighted = per-entry {target, scale} stream present (euclidean / RNN sets)
+KernelFn pick_kernel(int dim, int opt, bool weighted) {
+  if (dim == 2) return weighted ? pick_opt<2, true>(opt) : pick_opt<2, false>(opt);
+  return weighted ? pick_opt<3, true>(opt) : pick_opt<3, false>(opt);
 }
 
 KernelFn pick_finalize(int opt) {
@@ -245,35 +243,130 @@ __global__ void k_d2f(const double* __restrict__ in, float* __restrict__ out, in
     out[i] = (float)in[i];
 }
 
-// host double (m, dim) -> layout with stride ys; Nesterov look = y + beta*v
+// host double (m, dim) in caller order -> device layout (stride ys) in the
+// relabelled order: out[r] = y[perm[r]]; Nesterov look = y + beta*v
 __global__ void k_pack_positions(const double* __restrict__ y, int64_t m, int dim, int ys,
-                                 const float* __restrict__ vel, int vel_stride, float beta,
-                                 float* __restrict__ out) {
+                                 const int32_t* __restrict__ perm, const float* __restrict__ vel,
+                                 int vel_stride, float beta, float* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     float* o = out + i * ys;
+    const int64_t src = perm[i];
     const int look_off = (ys == 4 && dim == 2) ? 2 : 4;
     for (int d = 0; d < dim; ++d) {
-      const float v = (float)y[i * dim + d];
+      const float v = (float)y[src * dim + d];
       o[d] = v;
       if (vel) o[look_off + d] = v + beta * vel[i * vel_stride + d];
     }
   }
 }
 
+// device layout (relabelled) -> double (m, dim) in caller order
 __global__ void k_unpack_positions(const float* __restrict__ in, int64_t m, int dim, int ys,
-                                   double* __restrict__ y) {
+                                   const int32_t* __restrict__ perm, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dst = perm[i];
+    for (int d = 0; d < dim; ++d) y[dst * dim + d] = (double)in[i * ys + d];
+  }
+}
+
+__global__ void k_unpermute_f64(const double* __restrict__ in, int64_t m, int dim,
+                                const int32_t* __restrict__ perm, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
-    for (int d = 0; d < dim; ++d) y[i * dim + d] = (double)in[i * ys + d];
+    for (int d = 0; d < dim; ++d) out[(int64_t)perm[i] * dim + d] = in[i * dim + d];
 }
 
 __global__ void k_deltas(const float* __restrict__ a, const float* __restrict__ b, int64_t m,
-                         int dim, int ys, int commit, double* __restrict__ out) {
+                         int dim, int ys, int commit, const int32_t* __restrict__ perm,
+                         double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dst = perm[i];
+    for (int d = 0; d < dim; ++d)
+      out[dst * dim + d] = commit ? (double)a[i * ys + d] - (double)b[i * ys + d] : 0.0;
+  }
+}
+
+__global__ void k_iota(int32_t* __restrict__ a, int64_t m) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
-    for (int d = 0; d < dim; ++d)
-      out[i * dim + d] = commit ? (double)a[i * ys + d] - (double)b[i * ys + d] : 0.0;
+    a[i] = (int32_t)i;
+}
+
+__global__ void k_degrees(const uint32_t* __restrict__ row_ptr, int64_t m, uint32_t* __restrict__ deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = row_ptr[i + 1] - row_ptr[i];
+}
+
+__global__ void k_inverse(const int32_t* __restrict__ perm, int64_t m, int32_t* __restrict__ inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[i]] = (int32_t)i;
+}
+
+// out[r] = in[src(r)] for rows of `stride` floats; src(r) = inv_old[perm_new[r]]
+__global__ void k_permute_rows(const float* __restrict__ in, int64_t m, int stride,
+                               const int32_t* __restrict__ perm_new, const int32_t* __restrict__ inv_old,
+                               float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = inv_old[perm_new[i]];
+    for (int d = 0; d < stride; ++d) out[i * stride + d] = in[src * stride + d];
+  }
+}
+
+// new-order degrees: deg_n[r] = deg_o[perm[r]]
+__global__ void k_gather_u32(const uint32_t* __restrict__ in, const int32_t* __restrict__ perm, int64_t m,
+                             uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[perm[i]];
+}
+
+// One warp per relabelled row: copy the old row's entries in order, mapping
+// the neighbour id through inv and attaching the class bit / weights.
+__global__ void k_fill_perm_cols(const uint32_t* __restrict__ rp_old, const uint32_t* __restrict__ rp_new,
+                                 const uint32_t* __restrict__ vals, int64_t m, int64_t L,
+                                 const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                 const uint8_t* __restrict__ rand, int64_t n_nn,
+                                 const float* __restrict__ tgt, const float* __restrict__ scl,
+                                 const int32_t* __restrict__ perm, const int32_t* __restrict__ inv,
+                                 uint32_t* __restrict__ col, float2* __restrict__ ew) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < m; r += nwarps) {
+    const int64_t o = perm[r];
+    const uint32_t b0 = rp_old[o], b1 = rp_old[o + 1], nb = rp_new[r];
+    for (uint32_t k = b0 + lane; k < b1; k += 32) {
+      const int64_t h = vals[k];
+      const int64_t e = h < L ? h : h - L;
+      const uint32_t other = (uint32_t)inv[h < L ? dst[e] : src[e]];
+      const bool rn = rand ? (rand[e] != 0) : (e >= n_nn);
+      const uint32_t kn = nb + (k - b0);
+      col[kn] = other | (rn ? kRandBit : 0u);
+      if (ew) ew[kn] = make_float2(tgt ? tgt[e] : (rn ? 1.f : 0.f), scl ? scl[e] : 1.f);
+    }
+  }
+}
+
+// Lanes per vertex of each tile: smallest power of two G with
+// G * kUnroll >= the tile's max degree (capped at a warp); pad tiles get 1.
+__global__ void k_tile_g(const uint32_t* __restrict__ rp, int64_t m, int n_tiles_cap,
+                         uint8_t* __restrict__ tile_g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_tiles_cap; t += nwarps) {
+    uint32_t mx = 0;
+    for (int64_t r = t * kBlock + lane; r < min(m, (t + 1) * (int64_t)kBlock); r += 32)
+      mx = max(mx, rp[r + 1] - rp[r]);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int G = 1;
+    while (G < 32 && (uint32_t)(G * kUnroll) < mx) G <<= 1;
+    if (lane == 0) tile_g[t] = (uint8_t)G;
+  }
 }
 
 // fixed-order reduction of partial tiles into one double4 (operator calls)
@@ -298,6 +391,7 @@ inline int grid_for(int64_t n, int sms) {
 
 int ensure_slot(ivhd_ctx* ctx, CsrSlot& s, int64_t n, bool weighted) {
   if (s.row_ptr == nullptr) CU(ctx, cudaMalloc(&s.row_ptr, sizeof(uint32_t) * (ctx->m + 1)));
+  if (s.tile_g == nullptr) CU(ctx, cudaMalloc(&s.tile_g, (size_t)ctx->n_tiles_cap));
   if (n > s.cap) {
     if (s.col) CU(ctx, cudaFree(s.col));
     if (s.ew) CU(ctx, cudaFree(s.ew));
@@ -319,12 +413,69 @@ void drop_graphs(ivhd_ctx* ctx) {
   ctx->graphs.clear();
 }
 
+int ys_now(ivhd_ctx* ctx);
+int ss_now(ivhd_ctx* ctx);
+int pull_ctrl(ivhd_ctx* ctx);
+
+// Fix the vertex order from the degrees of the first CSR built: stable sort
+// by descending degree (hubs first, so the dynamic tile scheduler starts the
+// longest tiles early).  Positions/state already uploaded are re-ordered.
+int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
+  const int64_t m = ctx->m;
+  cudaStream_t st = ctx->stream;
+  uint32_t *deg = nullptr, *deg2 = nullptr;
+  int32_t *ids = nullptr, *perm = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  TRY(pull_ctrl(ctx));
+  cudaError_t e = cudaSuccess;
+  do {
+    if ((e = cudaMalloc(&deg, 4 * m)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&deg2, 4 * m)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&ids, 4 * m)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&perm, 4 * m)) != cudaSuccess) break;
+    k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, deg);
+    k_iota<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ids, m);
+    if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
+        cudaSuccess) break;
+    if ((e = cudaMalloc(&tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
+    if ((e = cub::DeviceRadixSort::SortPairsDescending(tmp, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
+        cudaSuccess) break;
+    if (ctx->pos_set) {
+      // data is currently in the old order (ctx->perm / ctx->inv): re-order
+      float* scratch = reinterpret_cast<float*>(ctx->stage);  // 32 bytes/vertex
+      const int ys = ys_now(ctx), ss = ss_now(ctx);
+      float* y = ctx->ybuf[ctx->ctrl_h->cur];
+      k_permute_rows<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(y, m, ys, perm, ctx->inv, scratch);
+      if ((e = cudaMemcpyAsync(y, scratch, sizeof(float) * ys * m, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        break;
+      if (ss > 0) {
+        k_permute_rows<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ctx->state, m, ss, perm, ctx->inv, scratch);
+        if ((e = cudaMemcpyAsync(ctx->state, scratch, sizeof(float) * ss * m, cudaMemcpyDeviceToDevice, st)) !=
+            cudaSuccess) break;
+      }
+    }
+    if ((e = cudaMemcpyAsync(ctx->perm, perm, 4 * m, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) break;
+    k_inverse<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ctx->perm, m, ctx->inv);
+    e = cudaStreamSynchronize(st);
+  } while (0);
+  cudaFree(deg); cudaFree(deg2); cudaFree(ids); cudaFree(perm); cudaFree(tmp);
+  if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "vertex relabelling: %s", cudaGetErrorString(e));
+  ctx->perm_fixed = true;
+  return IVHD_OK;
+}
+
 // src/dst: device int32 [L]; rand: device u8 [L] or null (then e >= n_nn is random);
-// tgt/scl: device float [L] or null.
+// tgt/scl: device float [L] or null.  Builds the symmetrised CSR in the
+// relabelled vertex order: row r lists every connection incident to vertex
+// perm[r] — first those where it is the source, then those where it is the
+// destination, each in connection order (the reference's edge order,
+// engine.py:245-262) — so per-row summation order is independent of the
+// relabelling.
 int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, const uint8_t* rand,
               int64_t n_nn, const float* tgt, const float* scl, int64_t L) {
   CsrSlot& S = ctx->slots[slot];
-  const int64_t n = 2 * L;
+  const int64_t n = 2 * L, m = ctx->m;
   if (n >= (int64_t)0x7fffffffLL) return fail(ctx, IVHD_ERR_INVALID_ARG, "too many connections (%lld)", (long long)L);
   const bool weighted = (tgt != nullptr) || (scl != nullptr);
   TRY(ensure_slot(ctx, S, n, weighted));
@@ -332,47 +483,82 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
   S.valid = false;
   S.n = n;
   cudaStream_t st = ctx->stream;
-  if (n == 0) {
-    CU(ctx, cudaMemsetAsync(S.row_ptr, 0, sizeof(uint32_t) * (ctx->m + 1), st));
-    CU(ctx, cudaStreamSynchronize(st));
-    S.valid = true;
-    return IVHD_OK;
-  }
-  uint32_t *keys = nullptr, *keys2 = nullptr, *vals = nullptr, *vals2 = nullptr;
+  uint32_t *keys = nullptr, *keys2 = nullptr, *vals = nullptr, *vals2 = nullptr, *rp_old = nullptr, *deg = nullptr;
   int* bad = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   int end_bit = 1;
-  while (end_bit < 32 && ((int64_t)1 << end_bit) < ctx->m) ++end_bit;
+  while (end_bit < 32 && ((int64_t)1 << end_bit) < m) ++end_bit;
   cudaError_t e = cudaSuccess;
-  int hbad = 0;
-  auto cleanup = [&]() {
-    cudaFree(keys); cudaFree(keys2); cudaFree(vals); cudaFree(vals2); cudaFree(bad); cudaFree(tmp);
-  };
+  int hbad = 0, rc = IVHD_OK;
+  const int64_t nc = std::max<int64_t>(n, 1);
   do {
-    if ((e = cudaMalloc(&keys, 4 * n)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&keys2, 4 * n)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&vals, 4 * n)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&vals2, 4 * n)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&keys, 4 * nc)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&keys2, 4 * nc)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&vals, 4 * nc)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&vals2, 4 * nc)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&rp_old, 4 * (m + 1))) != cudaSuccess) break;
+    if ((e = cudaMalloc(&deg, 4 * (m + 1))) != cudaSuccess) break;
     if ((e = cudaMalloc(&bad, sizeof(int))) != cudaSuccess) break;
     if ((e = cudaMemsetAsync(bad, 0, sizeof(int), st)) != cudaSuccess) break;
-    k_half_edges<<<grid_for(n, ctx->sm_count), 256, 0, st>>>(src, dst, L, ctx->m, keys, vals, bad);
-    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0,
-                                             end_bit, st)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16))) != cudaSuccess) break;
-    // LSD radix sort is stable: rows list out-halves (connection order) then in-halves.
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0,
-                                             end_bit, st)) != cudaSuccess) break;
-    k_row_ptr<<<grid_for(ctx->m + 1, ctx->sm_count), 256, 0, st>>>(keys2, n, ctx->m, S.row_ptr);
-    k_fill_cols<<<grid_for(n, ctx->sm_count), 256, 0, st>>>(vals2, n, L, src, dst, rand, n_nn, tgt, scl,
-                                                           S.col, S.ew);
+    if (n > 0) {
+      k_half_edges<<<grid_for(n, ctx->sm_count), 256, 0, st>>>(src, dst, L, m, keys, vals, bad);
+      if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, end_bit,
+                                               st)) != cudaSuccess) break;
+      if ((e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16))) != cudaSuccess) break;
+      // LSD radix sort is stable: rows list out-halves (connection order) then in-halves.
+      if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, end_bit,
+                                               st)) != cudaSuccess) break;
+      k_row_ptr<<<grid_for(m + 1, ctx->sm_count), 256, 0, st>>>(keys2, n, m, rp_old);
+    } else {
+      if ((e = cudaMemsetAsync(rp_old, 0, 4 * (m + 1), st)) != cudaSuccess) break;
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) break;
     if ((e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+    if (hbad) break;
+    if (!ctx->perm_fixed && (rc = fix_permutation(ctx, rp_old)) != IVHD_OK) break;
+    // relabelled row pointers: exclusive scan of the permuted degrees
+    k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, keys);
+    k_gather_u32<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(keys, ctx->perm, m, deg);
+    if ((e = cudaMemsetAsync(deg + m, 0, 4, st)) != cudaSuccess) break;
+    size_t sb = 0;
+    if ((e = cub::DeviceScan::ExclusiveSum(nullptr, sb, deg, S.row_ptr, (int)(m + 1), st)) != cudaSuccess) break;
+    void* stmp = nullptr;
+    if ((e = cudaMalloc(&stmp, std::max<size_t>(sb, 16))) != cudaSuccess) break;
+    e = cub::DeviceScan::ExclusiveSum(stmp, sb, deg, S.row_ptr, (int)(m + 1), st);
+    cudaStreamSynchronize(st);
+    cudaFree(stmp);
+    if (e != cudaSuccess) break;
+    if (n > 0)
+      k_fill_perm_cols<<<grid_for(m * 32, ctx->sm_count), 256, 0, st>>>(
+          rp_old, S.row_ptr, vals2, m, L, src, dst, rand, n_nn, tgt, scl, ctx->perm, ctx->inv, S.col, S.ew);
+    k_tile_g<<<grid_for((int64_t)ctx->n_tiles_cap * 32, ctx->sm_count), 256, 0, st>>>(S.row_ptr, m,
+                                                                                     ctx->n_tiles_cap, S.tile_g);
+    if ((e = cudaGetLastError()) != cudaSuccess) break;
+    // work units: one per (tile, pass), in tile order
+    std::vector<uint8_t> g(ctx->n_tiles_cap);
+    if ((e = cudaMemcpyAsync(g.data(), S.tile_g, g.size(), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+    S.unit_base.assign(ctx->n_tiles_cap + 1, 0);
+    std::vector<int> units;
+    for (int t = 0; t < ctx->n_tiles_cap; ++t) {
+      S.unit_base[t + 1] = S.unit_base[t] + g[t];
+      for (int p = 0; p < g[t]; ++p) units.push_back(t << 6 | p);
+    }
+    S.n_units = (int)units.size();
+    if (S.units) cudaFree(S.units);
+    S.units = nullptr;
+    if ((e = cudaMalloc(&S.units, sizeof(int) * units.size())) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(S.units, units.data(), sizeof(int) * units.size(), cudaMemcpyHostToDevice, st)) !=
+        cudaSuccess) break;
     e = cudaStreamSynchronize(st);
   } while (0);
-  cleanup();
+  cudaFree(keys); cudaFree(keys2); cudaFree(vals); cudaFree(vals2); cudaFree(rp_old); cudaFree(deg);
+  cudaFree(bad); cudaFree(tmp);
+  if (rc != IVHD_OK) return rc;
   if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "CSR build: %s", cudaGetErrorString(e));
-  if (hbad) return fail(ctx, IVHD_ERR_INVALID_ARG, "connection endpoint outside [0, %lld)", (long long)ctx->m);
+  if (hbad) return fail(ctx, IVHD_ERR_INVALID_ARG, "connection endpoint outside [0, %lld)", (long long)m);
   S.valid = true;
   return IVHD_OK;
 }
@@ -392,22 +578,25 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   A.trace = ctx->trace;
   A.ctrl = ctx->ctrl;
   A.force_out = nullptr;
+  A.tile_g = S.tile_g;
+  A.units = S.units;
   A.tile_v = ctx->tile_v;
   A.norm = norm;
   A.fuse_finalize = fuse;
   A.h = ctx->hyper;
+  A.v_begin = 0;
+  A.v_end = ctx->m;
   if (ctx->sharded) {
-    A.v_begin = ctx->shard_begin;
-    A.v_end = std::min<int64_t>(ctx->shard_end, ctx->m);
-    A.tile0 = (int)(ctx->shard_begin / ctx->tile_v);
-    A.n_tiles = (int)((ctx->shard_end - ctx->shard_begin) / ctx->tile_v);
-    A.n_tiles_global = ctx->n_tiles_cap;
+    // every unit up to the padded tile count is written by some rank (pad
+    // tiles hold zeros), so all ranks reduce the same array in the same order
+    const int t0 = (int)(ctx->shard_begin / ctx->tile_v), t1 = (int)(ctx->shard_end / ctx->tile_v);
+    A.tile0 = S.unit_base[t0];
+    A.n_tiles = S.unit_base[t1] - S.unit_base[t0];
+    A.n_tiles_global = S.n_units;
   } else {
-    A.v_begin = 0;
-    A.v_end = ctx->m;
     A.tile0 = 0;
-    A.n_tiles = ctx->n_tiles;
-    A.n_tiles_global = ctx->n_tiles;
+    A.n_tiles = S.unit_base[ctx->n_tiles];
+    A.n_tiles_global = A.n_tiles;
   }
   return A;
 }
@@ -444,6 +633,14 @@ int upload_stage(ivhd_ctx* ctx, const double* host, int64_t count) {
 }
 
 int vel_stride(int dim) { return dim == 2 ? 2 : 4; }
+
+int ys_now(ivhd_ctx* ctx) { return ys_of(ctx->dim, ctx->opt.kind); }
+
+int ss_now(ivhd_ctx* ctx) {
+  const int k = ctx->opt.kind;
+  const int nv = (k == OPT_FD || k == OPT_MOM || k == OPT_NEST) ? 1 : (k == OPT_ADAM || k == OPT_ADADELTA) ? 2 : 0;
+  return nv == 0 ? 0 : (ctx->dim == 2 ? 2 * nv : 4 * nv);
+}
 
 }  // namespace
 
@@ -486,10 +683,9 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
       return bail(fail(ctx, IVHD_ERR_CUDA, "stream create failed"));
     ctx->own_stream = true;
   }
-  // Fixed tile size (a function of M only): the reduction order is the same
-  // for any grid size and any number of ranks.
-  ctx->rpt = m >= (1 << 18) ? 2 : 1;
-  const int64_t tv = (int64_t)kBlock * ctx->rpt;
+  // Fixed tile size: the reduction order is the same for any grid size and
+  // any number of ranks.
+  const int64_t tv = kBlock;
   ctx->tile_v = (int)tv;
   ctx->n_tiles = (int)((m + tv - 1) / tv);
   ctx->n_tiles_cap = (ctx->n_tiles + 7) / 8 * 8;
@@ -505,12 +701,17 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   alloc((void**)&ctx->ybuf[0], sizeof(float) * 8 * vc);
   alloc((void**)&ctx->ybuf[1], sizeof(float) * 8 * vc);
   alloc((void**)&ctx->state, sizeof(float) * 8 * vc);
-  alloc((void**)&ctx->partial, sizeof(double4) * ctx->n_tiles_cap);
+  alloc((void**)&ctx->partial, sizeof(double4) * 32 * ctx->n_tiles_cap);  // <= 32 units per tile
   alloc((void**)&ctx->ctrl, sizeof(Ctrl));
   alloc((void**)&ctx->opctrl, sizeof(Ctrl));
   alloc((void**)&ctx->red_out, sizeof(double4));
   alloc((void**)&ctx->stage, sizeof(double) * 4 * vc);
+  alloc((void**)&ctx->perm, sizeof(int32_t) * vc);
+  alloc((void**)&ctx->inv, sizeof(int32_t) * vc);
   if (rc != IVHD_OK) return bail(rc);
+  k_iota<<<grid_for(vc, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->perm, vc);  // identity until the first CSR
+  k_iota<<<grid_for(vc, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->inv, vc);
+  cudaStreamSynchronize(ctx->stream);
   if (cudaMallocHost(&ctx->ctrl_h, sizeof(Ctrl)) != cudaSuccess)
     return bail(fail(ctx, IVHD_ERR_CUDA, "pinned alloc failed"));
   memset(ctx->ctrl_h, 0, sizeof(Ctrl));
@@ -542,8 +743,9 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   drop_graphs(ctx);
   for (auto& s : ctx->slots) {
-    cudaFree(s.row_ptr); cudaFree(s.col); cudaFree(s.ew);
+    cudaFree(s.row_ptr); cudaFree(s.col); cudaFree(s.ew); cudaFree(s.tile_g); cudaFree(s.units);
   }
+  cudaFree(ctx->perm); cudaFree(ctx->inv);
   cudaFree(ctx->ybuf[0]); cudaFree(ctx->ybuf[1]); cudaFree(ctx->state); cudaFree(ctx->partial);
   cudaFree(ctx->trace); cudaFree(ctx->ctrl); cudaFree(ctx->opctrl); cudaFree(ctx->red_out);
   cudaFree(ctx->stage); cudaFree(ctx->op_y); cudaFree(ctx->op_force);
@@ -649,7 +851,7 @@ int ivhd_set_positions(ivhd_ctx* ctx, const double* y) {
   const bool nest = ctx->opt.kind == IVHD_OPT_NESTEROV;
   float* dst = ctx->ybuf[ctx->ctrl_h->cur];
   k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-      ctx->stage, ctx->m, ctx->dim, ys, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
+      ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
       (float)ctx->hyper.beta, dst);
   CU(ctx, cudaGetLastError());
   ctx->ctrl_h->status = 0;
@@ -666,7 +868,7 @@ int ivhd_get_positions(ivhd_ctx* ctx, double* y_out) {
   TRY(pull_ctrl(ctx));
   const int ys = ys_of(ctx->dim, ctx->opt.kind);
   k_unpack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-      ctx->ybuf[ctx->ctrl_h->cur], ctx->m, ctx->dim, ys, ctx->stage);
+      ctx->ybuf[ctx->ctrl_h->cur], ctx->m, ctx->dim, ys, ctx->perm, ctx->stage);
   CU(ctx, cudaGetLastError());
   CU(ctx, cudaMemcpyAsync(y_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim, cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -681,7 +883,8 @@ int ivhd_get_deltas(ivhd_ctx* ctx, double* d_out) {
   const int ys = ys_of(ctx->dim, ctx->opt.kind);
   const int cur = ctx->ctrl_h->cur;
   k_deltas<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-      ctx->ybuf[cur], ctx->ybuf[cur ^ 1], ctx->m, ctx->dim, ys, ctx->ctrl_h->last_commit, ctx->stage);
+      ctx->ybuf[cur], ctx->ybuf[cur ^ 1], ctx->m, ctx->dim, ys, ctx->ctrl_h->last_commit, ctx->perm,
+      ctx->stage);
   CU(ctx, cudaGetLastError());
   CU(ctx, cudaMemcpyAsync(d_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim, cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -700,10 +903,10 @@ int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p) {
     // re-pack the current positions for the new layout (velocity starts at 0)
     float* cur = ctx->ybuf[ctx->ctrl_h->cur];
     k_unpack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(cur, ctx->m, ctx->dim,
-                                                                                old_ys, ctx->stage);
+                                                                                old_ys, ctx->perm, ctx->stage);
     CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * 8 * ctx->v_cap, ctx->stream));
     k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-        ctx->stage, ctx->m, ctx->dim, new_ys, p->kind == IVHD_OPT_NESTEROV ? ctx->state : nullptr,
+        ctx->stage, ctx->m, ctx->dim, new_ys, ctx->perm, p->kind == IVHD_OPT_NESTEROV ? ctx->state : nullptr,
         vel_stride(ctx->dim), (float)p->beta, cur);
     CU(ctx, cudaGetLastError());
   }
@@ -778,12 +981,12 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   ctx->ctrl_h->next_tile = 0;
   TRY(push_ctrl(ctx));
   const CsrSlot& S = ctx->slots[slot];
-  KernelFn fn = pick_kernel(ctx->dim, ctx->opt.kind, ctx->rpt, S.ew != nullptr);
+  KernelFn fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr);
   const StepArgs A = make_args(ctx, slot, norm, 1);
   int64_t left = n_iter;
   const int chunk = ctx->graph_chunk;
   if (left >= chunk) {
-    const GraphKey key{slot, norm, ctx->opt.kind, ctx->rpt * 2 + (S.ew != nullptr)};
+    const GraphKey key{slot, norm, ctx->opt.kind, S.ew != nullptr ? 1 : 0};
     auto it = ctx->graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (it == ctx->graphs.end()) {
@@ -836,7 +1039,7 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   const int ys = ctx->dim == 2 ? 2 : 4;
   TRY(upload_stage(ctx, y, ctx->m * ctx->dim));
   k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->stage, ctx->m, ctx->dim, ys,
-                                                                           nullptr, 0, 0.f, ctx->op_y);
+                                                                           ctx->perm, nullptr, 0, 0.f, ctx->op_y);
   TRY(pull_ctrl(ctx));
   Ctrl oc{};
   oc.c = c;
@@ -852,21 +1055,26 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   A.partial = ctx->partial;
   A.ctrl = ctx->opctrl;
   A.force_out = ctx->op_force;
+  A.tile_g = S.tile_g;
+  A.units = S.units;
   A.v_begin = 0;
   A.v_end = ctx->m;
   A.tile_v = ctx->tile_v;
-  A.n_tiles = ctx->n_tiles;
-  A.n_tiles_global = ctx->n_tiles;
+  A.n_tiles = S.unit_base[ctx->n_tiles];
+  A.n_tiles_global = A.n_tiles;
   A.norm = norm;
   A.fuse_finalize = 0;
-  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, ctx->rpt, S.ew != nullptr), A));
-  k_reduce_partials<<<1, kBlock, 0, ctx->stream>>>(ctx->partial, ctx->n_tiles, ctx->red_out);
+  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, S.ew != nullptr), A));
+  k_reduce_partials<<<1, kBlock, 0, ctx->stream>>>(ctx->partial, A.n_tiles, ctx->red_out);
   CU(ctx, cudaGetLastError());
   double4 red;
   CU(ctx, cudaMemcpyAsync(&red, ctx->red_out, sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
-  if (want_forces)
-    CU(ctx, cudaMemcpyAsync(forces_out, ctx->op_force, sizeof(double) * ctx->m * ctx->dim,
+  if (want_forces) {
+    k_unpermute_f64<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->op_force, ctx->m, ctx->dim,
+                                                                             ctx->perm, ctx->stage);
+    CU(ctx, cudaMemcpyAsync(forces_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim,
                             cudaMemcpyDeviceToHost, ctx->stream));
+  }
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (stress_out) *stress_out = 0.5 * red.x;
   return IVHD_OK;
@@ -935,7 +1143,7 @@ int ivhd_shard_set_range(ivhd_ctx* ctx, int64_t v_begin, int64_t v_end) {
   ctx->shard_end = v_end;
   ctx->sharded = true;
   CU(ctx, cudaSetDevice(ctx->device));
-  CU(ctx, cudaMemsetAsync(ctx->partial, 0, sizeof(double4) * ctx->n_tiles_cap, ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->partial, 0, sizeof(double4) * 32 * ctx->n_tiles_cap, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   return IVHD_OK;
 }
@@ -966,7 +1174,7 @@ int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c) {
   TRY(push_ctrl(ctx));
   StepArgs A = make_args(ctx, slot, norm, 0);
   const CsrSlot& S = ctx->slots[slot];
-  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, ctx->rpt, S.ew != nullptr), A));
+  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr), A));
   return IVHD_OK;
 }
 

@@ -82,11 +82,13 @@ struct StepArgs {
   double2* trace;
   Ctrl* ctrl;
   double* force_out;      // OPT_NONE only: (M, DIM) float64
+  const uint8_t* tile_g;  // lanes per vertex of every (global) tile
+  const int* units;       // work unit -> (tile << 6) | pass, global unit order
   long long v_begin, v_end;
   int tile_v;
-  int n_tiles;            // tiles this launch processes
-  int tile0;              // global index of its first tile
-  int n_tiles_global;     // tiles reduced by the finalizer
+  int n_tiles;            // work units this launch processes
+  int tile0;              // global index of its first work unit
+  int n_tiles_global;     // work-unit partials reduced by the finalizer
   int norm;               // 0 = L2, 1 = L1
   int fuse_finalize;      // last block reduces + decides (single GPU)
   Hyper h;
@@ -333,23 +335,6 @@ __device__ void finalize_block(const StepArgs& A, double4* sm) {
   }
 }
 
-// ---------------------------------------------------------- merge path
-// Tile-local merge path of row ends (s_re[r] = end of row r, local entry
-// index) and entries: row-end r sits at diagonal s_re[r] + r.  Returns the
-// number of rows whose end item lies before diagonal d.
-__device__ __forceinline__ int merge_search(const uint32_t* s_re, int nrows, int d) {
-  int lo = 0, hi = nrows;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((int)s_re[mid] + mid < d) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
-  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
-}
-
 template <int SS>
 __device__ __forceinline__ void ld_state(const float* p, float (&s)[SS > 0 ? SS : 1]) {
   if constexpr (SS == 2) {
@@ -445,44 +430,21 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
   acc_bad += all_finite(yn, DIM) ? 0.0 : 1.0;
 }
 
-// Store one row partial produced by a thread walking entries [js, je):
-// complete rows go to s_row[r]; a row that starts here and continues goes to
-// s_tail[tid]; a row continued from an earlier thread goes to s_head[tid].
-template <int DIM>
-__device__ __forceinline__ void emit_row(int r, const float (&f)[DIM], float e, int js, int je,
-                                         const uint32_t* s_re, float4* s_row, float4* s_head,
-                                         float4* s_tail) {
-  const int rs = r > 0 ? (int)s_re[r - 1] : 0;
-  const int re = (int)s_re[r];
-  const bool started = rs >= js;
-  float4* dst = started ? (re <= je ? &s_row[r] : &s_tail[threadIdx.x]) : &s_head[threadIdx.x];
-  if constexpr (DIM == 2) *dst = make_float4(f[0], f[1], e, 0.f);
-  else *dst = make_float4(f[0], f[1], f[2], e);
-}
-
 // ------------------------------------------------------------------ kernel
-// Tile = TV = 256*RPT consecutive vertices.  Its rows' entries are walked as
-// one merge path of (row ends + entries); each thread owns P consecutive
-// items, so its column loads and position gathers are issued as one batch
-// and hub rows are split evenly across threads.  A row touching several
-// threads is summed as tail(first thread) + head(next) + ... in thread
-// order (deterministic); rows spanning a round of 256*P items carry over in
-// s_carry.  The thread owning row r (r mod 256) applies the optimizer.
-template <int DIM, int OPT, int RPT, int P, bool WEIGHTED>
-__global__ void __launch_bounds__(kBlock, 2) step_kernel(StepArgs A) {
+// Vertices are relabelled by degree at setup (ivhd_capi.cu), so the 256
+// consecutive vertices of a tile have near-equal degree.  Each tile carries
+// G = lanes per vertex (1, 2, 4, ..., 32; G * kUnroll >= its max degree
+// except for hubs): G lanes walk one CSR row with kUnroll independent column
+// loads and position gathers in flight each, reduce with a fixed xor
+// butterfly, and lane 0 applies the optimizer.  The only block barrier is
+// the per-tile partial reduction.
+constexpr int kUnroll = 8;
+
+template <int DIM, int OPT, bool WEIGHTED>
+__global__ void __launch_bounds__(kBlock, 3) step_kernel(StepArgs A) {
   using L = Layout<DIM, OPT>;
   constexpr bool NEST = (OPT == OPT_NEST);
-  constexpr int TV = kBlock * RPT;
-  constexpr int ITEMS = kBlock * P;
-  constexpr int YS = L::YS;
   constexpr int SSX = L::SS > 0 ? L::SS : 1;
-
-  __shared__ __align__(16) float s_y[TV * YS];
-  __shared__ float4 s_row[TV];
-  __shared__ float4 s_head[kBlock];
-  __shared__ float4 s_tail[kBlock];
-  __shared__ uint32_t s_re[TV];
-  __shared__ float4 s_carry[2];  // double-buffered by round parity
   __shared__ double4 sm_red[kBlock / 32];
   __shared__ int sm_tile;
 
@@ -503,162 +465,94 @@ __global__ void __launch_bounds__(kBlock, 2) step_kernel(StepArgs A) {
     bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
   }
 
+  // Work unit = one pass of a tile: 256/G vertices with G lanes each.  Heavy
+  // tiles (large G) thus spread over many blocks instead of serialising G
+  // passes in one; each unit writes its own partial (fixed unit order).
   while (true) {
     if (tid == 0) sm_tile = (int)atomicAdd(&ctrl->next_tile, 1u);
     block_sync();
-    const int tile = sm_tile;
-    if (tile >= A.n_tiles) break;
-    const long long v0 = A.v_begin + (long long)tile * TV;
-    const int nrows = (int)max(0LL, min((long long)TV, A.v_end - v0));
+    const int unit = sm_tile;
+    if (unit >= A.n_tiles) break;
+    const int packed = __ldg(A.units + A.tile0 + unit);
+    const int tile = packed >> 6, pass = packed & 63;
+    const long long v0 = (long long)tile * kBlock;
+    const int G = A.tile_g[tile];
+    const int lgG = __ffs(G) - 1;
+    const int lg = tid & (G - 1);
+    const int grp = tid >> lgG;
+    const int groups = kBlock >> lgG;
     double acc_e = 0.0, acc_n = 0.0, acc_o = 0.0, acc_bad = 0.0;
 
-    if (nrows > 0) {
-      // ---- round trip 1: row ends, the tile's positions, owners' state
-      const uint32_t e0 = __ldg(A.row_ptr + v0);
-      for (int r = tid; r < nrows; r += kBlock) s_re[r] = __ldg(A.row_ptr + v0 + r + 1) - e0;
-      if constexpr (YS % 4 == 0) {
-        const float4* src = reinterpret_cast<const float4*>(Yin + (size_t)v0 * YS);
-        for (int q = tid; q < nrows * YS / 4; q += kBlock) reinterpret_cast<float4*>(s_y)[q] = __ldg(src + q);
-      } else {
-        const float2* src = reinterpret_cast<const float2*>(Yin + (size_t)v0 * YS);
-        for (int q = tid; q < nrows * YS / 2; q += kBlock) reinterpret_cast<float2*>(s_y)[q] = __ldg(src + q);
-      }
-      float sv[RPT][SSX];
-#pragma unroll
-      for (int kk = 0; kk < RPT; ++kk) {
-        const int r = tid + kk * kBlock;
+    {
+      const long long v = v0 + (long long)pass * groups + grp;
+      const bool active = v < A.v_end;
+      uint32_t beg = 0, end = 0;
+      float yi[DIM], li[DIM], sv[SSX];
+      if (active) {
+        beg = __ldg(A.row_ptr + v);
+        end = __ldg(A.row_ptr + v + 1);
+        gather<DIM, NEST>(Yin, (uint32_t)v, yi, li);
         if constexpr (L::SS > 0) {
-          if (r < nrows) ld_state<L::SS>(A.state + (size_t)(v0 + r) * L::SS, sv[kk]);
+          if (lg == 0) ld_state<L::SS>(A.state + (size_t)v * L::SS, sv);
         }
-      }
-      block_sync();
-      const int E = (int)s_re[nrows - 1];
-      const int total = nrows + E;
-
-      for (int base = 0, round = 0; base < total; base += ITEMS, ++round) {
-        const float4* carry_in = &s_carry[round & 1];
-        const int d0 = min(base + tid * P, total), d1 = min(d0 + P, total);
-        const int i0 = merge_search(s_re, nrows, d0);
-        const int i1 = merge_search(s_re, nrows, d1);
-        const int js = d0 - i0, ne = (d1 - i1) - js;
-        const int je = js + ne;
-        // ---- round trip 2 + 3: this thread's entries, then their positions
-        uint32_t cw[P];
-        float2 tw[WEIGHTED ? P : 1];
-        float gy[P][DIM], gl[P][DIM];
+      } else {
 #pragma unroll
-        for (int q = 0; q < P; ++q)
-          if (q < ne) cw[q] = __ldg(A.col + e0 + js + q);
+        for (int d = 0; d < DIM; ++d) yi[d] = li[d] = 0.f;
+      }
+      float f[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) f[d] = 0.f;
+      float e = 0.f;
+      for (uint32_t k0 = beg + lg; k0 < end; k0 += (uint32_t)G * kUnroll) {
+        uint32_t cw[kUnroll];
+        float2 tw[WEIGHTED ? kUnroll : 1];
+        float gy[kUnroll][DIM], gl[kUnroll][DIM];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint32_t k = k0 + (uint32_t)(u * G);
+          if (k < end) cw[u] = __ldg(A.col + k);
+        }
         if constexpr (WEIGHTED) {
 #pragma unroll
-          for (int q = 0; q < P; ++q)
-            if (q < ne) tw[q] = __ldg(A.ew + e0 + js + q);
-        }
-#pragma unroll
-        for (int q = 0; q < P; ++q)
-          if (q < ne) gather<DIM, NEST>(Yin, cw[q] & kIdMask, gy[q], gl[q]);
-        // ---- walk: accumulate per row, emit at row changes
-        int cr = i0;
-        bool open = false;
-        float f[DIM];
-        float e = 0.f;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) f[d] = 0.f;
-#ifdef IVHD_NOUNROLL_WALK
-#pragma unroll 1
-#else
-#pragma unroll
-#endif
-        for (int q = 0; q < P; ++q) {
-          if (q < ne) {
-            const int j = js + q;
-            int r = cr;
-            while ((int)s_re[r] <= j) ++r;
-            if (open && r != cr) {
-              emit_row<DIM>(cr, f, e, js, je, s_re, s_row, s_head, s_tail);
-#pragma unroll
-              for (int d = 0; d < DIM; ++d) f[d] = 0.f;
-              e = 0.f;
-            }
-            cr = r;
-            open = true;
-            float yi[DIM], li[DIM];
-            const float* ys = s_y + r * YS;
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) {
-              yi[d] = ys[d];
-              li[d] = NEST ? ys[(DIM == 2 ? 2 : 4) + d] : ys[d];
-            }
-            float2 twq = make_float2(0.f, 0.f);
-            if constexpr (WEIGHTED) twq = tw[q];
-            entry<DIM, NEST>(yi, li, gy[q], gl[q], cw[q], WEIGHTED, twq,
-                             c, A.norm, (uint32_t)(v0 + r), gstep, f, e);
+          for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t k = k0 + (uint32_t)(u * G);
+            if (k < end) tw[u] = __ldg(A.ew + k);
           }
         }
-        if (open) emit_row<DIM>(cr, f, e, js, je, s_re, s_row, s_head, s_tail);
-        block_sync();
-
-        // ---- resolve the rows whose end item lies in this round
-        auto chain = [&](int r, int tlast) {
-          const int rs = r > 0 ? (int)s_re[r - 1] : 0;
-          const int da = rs + r;
-          int t;
-          float4 sum;
-          if (da >= base) {
-            t = (da - base) / P;
-            sum = s_tail[t];
-          } else {
-            t = -1;
-            sum = *carry_in;
-          }
-          for (++t; t <= tlast; ++t) sum = f4add(sum, s_head[t]);
-          return sum;
-        };
 #pragma unroll
-        for (int kk = 0; kk < RPT; ++kk) {
-          const int r = tid + kk * kBlock;
-          if (r >= nrows) continue;
-          const int pe = (int)s_re[r] + r;
-          if (pe < base || pe >= base + ITEMS) continue;
-          const int rs = r > 0 ? (int)s_re[r - 1] : 0;
-          const int re = (int)s_re[r];
-          float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (re > rs) {
-            const int da = rs + r, db = re - 1 + r;
-            if (da / P == db / P) sum = s_row[r];
-            else sum = chain(r, db >= base ? (db - base) / P : -1);
-          }
-          float fr[DIM];
-          fr[0] = sum.x;
-          fr[1] = sum.y;
-          if constexpr (DIM == 3) fr[2] = sum.z;
-          acc_e += (double)(DIM == 2 ? sum.z : sum.w);
-          const long long v = v0 + r;
-          if constexpr (OPT == OPT_NONE) {
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint32_t k = k0 + (uint32_t)(u * G);
+          if (k < end) gather<DIM, NEST>(Yin, cw[u] & kIdMask, gy[u], gl[u]);
+        }
 #pragma unroll
-            for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)fr[d];
-          } else {
-            float yi[DIM];
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) yi[d] = s_y[r * YS + d];
-            apply_update<DIM, OPT>(A, Yout, v, yi, sv[kk], fr, step, bc1, bc2, acc_n, acc_o, acc_bad);
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint32_t k = k0 + (uint32_t)(u * G);
+          if (k < end) {
+            float2 twu = make_float2(0.f, 0.f);
+            if constexpr (WEIGHTED) twu = tw[u];
+            entry<DIM, NEST>(yi, li, gy[u], gl[u], cw[u], WEIGHTED, twu, c, A.norm, (uint32_t)v,
+                             gstep, f, e);
           }
         }
-        // ---- carry the row that is still open at the round boundary
-        if (tid == 0 && base + ITEMS < total) {
-          const int ib = merge_search(s_re, nrows, base + ITEMS);
-          const int jb = base + ITEMS - ib;
-          const int rs = ib > 0 ? (int)s_re[ib - 1] : 0;
-          if (ib < nrows && jb > rs) {
-            const int da = rs + ib, db = (int)s_re[ib] - 1 + ib;
-            if (da / P != db / P) s_carry[(round + 1) & 1] = chain(ib, (jb - 1 + ib - base) / P);
-          }
+      }
+      // fixed xor butterfly over the G lanes of the group (G uniform per tile)
+      for (int o = G >> 1; o > 0; o >>= 1) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) f[d] += __shfl_xor_sync(0xffffffffu, f[d], o);
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+      }
+      if (active && lg == 0) {
+        acc_e += (double)e;
+        if constexpr (OPT == OPT_NONE) {
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)f[d];
+        } else {
+          apply_update<DIM, OPT>(A, Yout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
         }
-        block_sync();
       }
     }
     const double4 tot = block_sum4(make_double4(acc_e, acc_n, acc_o, acc_bad), sm_red);
-    if (tid == 0) A.partial[A.tile0 + tile] = tot;
+    if (tid == 0) A.partial[A.tile0 + unit] = tot;
   }
 
   if (!A.fuse_finalize) return;
@@ -680,10 +574,5 @@ __global__ void __launch_bounds__(kBlock) finalize_kernel(StepArgs A) {
   if (A.ctrl->status != 0) return;
   finalize_block<OPT>(A, sm_red);
 }
-
-// Items per thread: sized so the batched gathers fit in registers.
-template <int DIM, int OPT> struct ItemsPerThread {
-  static constexpr int value = (OPT == OPT_NEST) ? (DIM == 2 ? 6 : 4) : (DIM == 2 ? 12 : 6);
-};
 
 }  // namespace ivhd
