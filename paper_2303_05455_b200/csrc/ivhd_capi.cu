@@ -26,7 +26,7 @@ struct CsrSlot {
   uint32_t* col = nullptr;      // [n]
   float2* ew = nullptr;         // [n] or nullptr (binary)
   uint8_t* tile_g = nullptr;    // [n_tiles_cap] lanes per vertex of each tile
-  int* units = nullptr;         // work units (tile << 6 | pass), tile-major order
+  int* units = nullptr;         // work units (tile << 8 | pass << 3 | log2 G), tile-major order
   int n_units = 0;
   std::vector<int> unit_base;   // host: first unit of each tile (n_tiles_cap + 1)
   int64_t n = 0;                // entries (2 * connections)
@@ -35,6 +35,11 @@ struct CsrSlot {
 };
 
 using KernelFn = void (*)(StepArgs);
+
+struct KernelInfo {
+  KernelFn fn;
+  int smem;
+};
 
 struct GraphKey {
   int slot, norm, opt, G;
@@ -96,7 +101,7 @@ struct ivhd_ctx {
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int graph_chunk = 64;
 
-  std::map<KernelFn, int> occ;
+  std::map<KernelFn, int> occ;  // blocks per SM
   std::string err;
 };
 
@@ -131,23 +136,33 @@ inline int ys_of(int dim, int opt) { return (opt == OPT_NEST) ? (dim == 2 ? 4 : 
 
 // ------------------------------------------------------------ kernel table
 
-template <int DIM, bool W>
-KernelFn pick_opt(int opt) {
+template <int DIM, int OPT, bool W, int N>
+KernelInfo kinfo() {
+  return KernelInfo{step_kernel<DIM, OPT, W, N>, step_smem_bytes<DIM, OPT>()};
+}
+
+template <int DIM, bool W, int N>
+KernelInfo pick_opt(int opt) {
   switch (opt) {
-    case OPT_FD: return step_kernel<DIM, OPT_FD, W>;
-    case OPT_SGD: return step_kernel<DIM, OPT_SGD, W>;
-    case OPT_MOM: return step_kernel<DIM, OPT_MOM, W>;
-    case OPT_NEST: return step_kernel<DIM, OPT_NEST, W>;
-    case OPT_ADAM: return step_kernel<DIM, OPT_ADAM, W>;
-    case OPT_ADADELTA: return step_kernel<DIM, OPT_ADADELTA, W>;
-    default: return step_kernel<DIM, OPT_NONE, W>;
+    case OPT_FD: return kinfo<DIM, OPT_FD, W, N>();
+    case OPT_SGD: return kinfo<DIM, OPT_SGD, W, N>();
+    case OPT_MOM: return kinfo<DIM, OPT_MOM, W, N>();
+    case OPT_NEST: return kinfo<DIM, OPT_NEST, W, N>();
+    case OPT_ADAM: return kinfo<DIM, OPT_ADAM, W, N>();
+    case OPT_ADADELTA: return kinfo<DIM, OPT_ADADELTA, W, N>();
+    default: return kinfo<DIM, OPT_NONE, W, N>();
   }
 }
 
+template <int DIM, bool W>
+KernelInfo pick_norm(int opt, int norm) {
+  return norm == 0 ? pick_opt<DIM, W, 0>(opt) : pick_opt<DIM, W, 1>(opt);
+}
+
 // weighted = per-entry {target, scale} stream present (euclidean / RNN sets)
-KernelFn pick_kernel(int dim, int opt, bool weighted) {
-  if (dim == 2) return weighted ? pick_opt<2, true>(opt) : pick_opt<2, false>(opt);
-  return weighted ? pick_opt<3, true>(opt) : pick_opt<3, false>(opt);
+KernelInfo pick_kernel(int dim, int opt, bool weighted, int norm) {
+  if (dim == 2) return weighted ? pick_norm<2, true>(opt, norm) : pick_norm<2, false>(opt, norm);
+  return weighted ? pick_norm<3, true>(opt, norm) : pick_norm<3, false>(opt, norm);
 }
 
 KernelFn pick_finalize(int opt) {
@@ -158,12 +173,13 @@ KernelFn pick_finalize(int opt) {
   }
 }
 
-int occupancy(ivhd_ctx* ctx, KernelFn fn) {
-  auto it = ctx->occ.find(fn);
+int occupancy(ivhd_ctx* ctx, KernelInfo k) {
+  auto it = ctx->occ.find(k.fn);
   if (it != ctx->occ.end()) return it->second;
+  cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   int n = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kBlock, 0) != cudaSuccess || n < 1) n = 1;
-  ctx->occ[fn] = n;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, kBlock, k.smem) != cudaSuccess || n < 1) n = 1;
+  ctx->occ[k.fn] = n;
   return n;
 }
 
@@ -390,14 +406,15 @@ inline int grid_for(int64_t n, int sms) {
 // ------------------------------------------------------------- CSR builder
 
 int ensure_slot(ivhd_ctx* ctx, CsrSlot& s, int64_t n, bool weighted) {
-  if (s.row_ptr == nullptr) CU(ctx, cudaMalloc(&s.row_ptr, sizeof(uint32_t) * (ctx->m + 1)));
+  // +16 entries: TMA copies round sizes up to 16 bytes
+  if (s.row_ptr == nullptr) CU(ctx, cudaMalloc(&s.row_ptr, sizeof(uint32_t) * (ctx->m + 1 + 16)));
   if (s.tile_g == nullptr) CU(ctx, cudaMalloc(&s.tile_g, (size_t)ctx->n_tiles_cap));
   if (n > s.cap) {
     if (s.col) CU(ctx, cudaFree(s.col));
     if (s.ew) CU(ctx, cudaFree(s.ew));
     s.col = nullptr;
     s.ew = nullptr;
-    CU(ctx, cudaMalloc(&s.col, sizeof(uint32_t) * std::max<int64_t>(n, 1)));
+    CU(ctx, cudaMalloc(&s.col, sizeof(uint32_t) * (std::max<int64_t>(n, 1) + 16)));
     s.cap = n;
   }
   if (weighted && s.ew == nullptr) CU(ctx, cudaMalloc(&s.ew, sizeof(float2) * std::max<int64_t>(s.cap, 1)));
@@ -544,7 +561,8 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
     std::vector<int> units;
     for (int t = 0; t < ctx->n_tiles_cap; ++t) {
       S.unit_base[t + 1] = S.unit_base[t] + g[t];
-      for (int p = 0; p < g[t]; ++p) units.push_back(t << 6 | p);
+      const int lg = __builtin_ctz((unsigned)g[t]);
+      for (int p = 0; p < g[t]; ++p) units.push_back(t << 8 | p << 3 | lg);
     }
     S.n_units = (int)units.size();
     if (S.units) cudaFree(S.units);
@@ -601,9 +619,9 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   return A;
 }
 
-int launch_step(ivhd_ctx* ctx, KernelFn fn, const StepArgs& A) {
-  const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
-  fn<<<grid, kBlock, 0, ctx->stream>>>(A);
+int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
+  const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, k) * ctx->sm_count));
+  k.fn<<<grid, kBlock, k.smem, ctx->stream>>>(A);
   CU(ctx, cudaGetLastError());
   return IVHD_OK;
 }
@@ -981,7 +999,7 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   ctx->ctrl_h->next_tile = 0;
   TRY(push_ctrl(ctx));
   const CsrSlot& S = ctx->slots[slot];
-  KernelFn fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr);
+  KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm);
   const StepArgs A = make_args(ctx, slot, norm, 1);
   int64_t left = n_iter;
   const int chunk = ctx->graph_chunk;
@@ -1064,7 +1082,7 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   A.n_tiles_global = A.n_tiles;
   A.norm = norm;
   A.fuse_finalize = 0;
-  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, S.ew != nullptr), A));
+  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, S.ew != nullptr, norm), A));
   k_reduce_partials<<<1, kBlock, 0, ctx->stream>>>(ctx->partial, A.n_tiles, ctx->red_out);
   CU(ctx, cudaGetLastError());
   double4 red;
@@ -1174,7 +1192,7 @@ int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c) {
   TRY(push_ctrl(ctx));
   StepArgs A = make_args(ctx, slot, norm, 0);
   const CsrSlot& S = ctx->slots[slot];
-  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr), A));
+  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
   return IVHD_OK;
 }
 

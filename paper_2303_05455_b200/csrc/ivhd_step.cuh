@@ -83,7 +83,7 @@ struct StepArgs {
   Ctrl* ctrl;
   double* force_out;      // OPT_NONE only: (M, DIM) float64
   const uint8_t* tile_g;  // lanes per vertex of every (global) tile
-  const int* units;       // work unit -> (tile << 6) | pass, global unit order
+  const int* units;       // work unit -> tile << 8 | pass << 3 | log2(G), global unit order
   long long v_begin, v_end;
   int tile_v;
   int n_tiles;            // work units this launch processes
@@ -179,11 +179,14 @@ __device__ __noinline__ void degenerate_dir(uint32_t i, uint32_t j, long long st
 // Contribution of one symmetrised-CSR entry to row i (forces.py:97-124):
 //   L2: phi = -w (t == 0) | w (t - d)/d ; f += phi (y_i - y_o);  e += w (t-d)^2
 //   L1: f += sign(y_i - y_o) w (t - d);                           e += w (t-d)^2
-template <int DIM, bool NEST>
+// The L2 form is branch-free: with rs = rsqrt(d^2), w (t - d)/d = w (t rs - 1)
+// and d = d^2 rs (guarded at 0 and inf).  Random pairs at exactly zero
+// distance (t != 0, d == 0) take the rare degenerate branch (forces.py:167-174).
+template <int DIM, bool NEST, int NORM>
 __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[DIM],
                                       const float (&yo)[DIM], const float (&lo)[DIM],
                                       uint32_t cw, bool weighted, float2 tw,
-                                      float c, int norm, uint32_t i, long long step,
+                                      float c, uint32_t i, long long step,
                                       float (&f)[DIM], float& e) {
   const bool rn = cw & kRandBit;
   float t, w;
@@ -202,24 +205,33 @@ __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[
     d2 = fmaf(df[d], df[d], d2);
     d1 += fabsf(df[d]);
   }
-  if (norm == 0) {
-    const float dist = sqrtf(d2);
-    if (t == 0.f) {
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) f[d] = fmaf(-w, df[d], f[d]);
-    } else if (dist > 0.f) {
-      const float phi = w * (t - dist) / dist;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) f[d] = fmaf(phi, df[d], f[d]);
-    } else if (dist == 0.f) {
+  if constexpr (NORM == 0) {
+    const float rs = rsqrtf(d2);
+    float phi = (t == 0.f) ? -w : w * fmaf(t, rs, -1.f);
+    if (t != 0.f && d2 == 0.f) {  // degenerate random pair
       float u[DIM];
       degenerate_dir<DIM>(i, cw & kIdMask, step, u);
 #pragma unroll
       for (int d = 0; d < DIM; ++d) f[d] = fmaf(w * t, u[d], f[d]);
-    } else {  // NaN distance: propagate like the reference's factor
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) f[d] += dist;
+      phi = 0.f;
     }
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) f[d] = fmaf(phi, df[d], f[d]);
+    float q2 = d2, qs = rs;
+    if constexpr (NEST) {  // stress at the current (not look-ahead) positions: engine.py:370
+      q2 = 0.f;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        const float q = yi[d] - yo[d];
+        q2 = fmaf(q, q, q2);
+      }
+      qs = rsqrtf(q2);
+    }
+    float de = q2 * qs;
+    de = (q2 == 0.f) ? 0.f : de;
+    de = (q2 == INFINITY) ? INFINITY : de;
+    const float r = t - de;
+    e = fmaf(w * r, r, e);
   } else {
     const float s = w * (t - d1);
 #pragma unroll
@@ -227,23 +239,15 @@ __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[
       const float sg = df[d] > 0.f ? 1.f : (df[d] < 0.f ? -1.f : (df[d] == 0.f ? 0.f : df[d]));
       f[d] = fmaf(sg, s, f[d]);
     }
-  }
-  // stress at the current (not look-ahead) positions: engine.py:370
-  float dist_e;
-  if constexpr (NEST) {
-    float q2 = 0.f, q1 = 0.f;
+    float de = d1;
+    if constexpr (NEST) {
+      de = 0.f;
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      const float q = yi[d] - yo[d];
-      q2 = fmaf(q, q, q2);
-      q1 += fabsf(q);
+      for (int d = 0; d < DIM; ++d) de += fabsf(yi[d] - yo[d]);
     }
-    dist_e = norm == 0 ? sqrtf(q2) : q1;
-  } else {
-    dist_e = norm == 0 ? sqrtf(d2) : d1;
+    const float r = t - de;
+    e = fmaf(w * r, r, e);
   }
-  const float r = t - dist_e;
-  e = fmaf(w * r, r, e);
 }
 
 __device__ __forceinline__ bool all_finite(const float* v, int n) {
@@ -438,24 +442,106 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
 // loads and position gathers in flight each, reduce with a fixed xor
 // butterfly, and lane 0 applies the optimizer.  The only block barrier is
 // the per-tile partial reduction.
-constexpr int kUnroll = 8;
+#ifndef IVHD_UNROLL
+#define IVHD_UNROLL 8
+#endif
+#ifndef IVHD_MINBLOCKS
+#define IVHD_MINBLOCKS 3
+#endif
+constexpr int kUnroll = IVHD_UNROLL;
+constexpr int kStages = 3;         // TMA ring depth (units in flight per block)
+constexpr int kColCap = 2048;      // staged column entries per unit (larger units read global)
+constexpr int kUnitCache = 1024;   // unit words cached per block
 
-template <int DIM, int OPT, bool WEIGHTED>
-__global__ void __launch_bounds__(kBlock, 3) step_kernel(StepArgs A) {
+// ------------------------------------------------------------- TMA helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (TMA, non-tensor); 16-byte aligned, size % 16 == 0
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// Shared-memory layout of one ring stage for (DIM, OPT).
+template <int DIM, int OPT>
+struct StageLayout {
+  static constexpr int YS = Layout<DIM, OPT>::YS, SS = Layout<DIM, OPT>::SS;
+  static constexpr int RP_BYTES = ((kBlock + 1) * 4 + 15) / 16 * 16 + 16;
+  static constexpr int COL_BYTES = kColCap * 4 + 32;
+  static constexpr int Y_BYTES = kBlock * YS * 4;
+  static constexpr int S_BYTES = kBlock * (SS > 0 ? SS : 1) * 4;
+  static constexpr int RP_OFF = 0, COL_OFF = RP_BYTES, Y_OFF = COL_OFF + COL_BYTES, S_OFF = Y_OFF + Y_BYTES;
+  static constexpr int BYTES = S_OFF + S_BYTES;
+};
+
+template <int DIM, int OPT>
+constexpr int step_smem_bytes() {
+  return kStages * StageLayout<DIM, OPT>::BYTES;
+}
+
+// Per-stage metadata written by the producer before it arrives on the
+// stage's barriers (release) and read by consumers after the wait (acquire).
+struct StageMeta {
+  int packed;       // unit word: tile << 8 | pass << 3 | log2 G
+  int col_off;      // entries skipped at the front of the staged columns (alignment)
+  int staged;       // 1 if the unit's columns are in shared memory
+  int pad;
+};
+
+// ------------------------------------------------------------------ kernel
+// Persistent blocks take work units statically (u = blockIdx.x + k*grid;
+// heavy tiles first in unit order).  Thread 0 is also the TMA producer: for
+// unit k+2 it bulk-copies the row pointers, positions and optimizer state
+// into ring stage (k+2)%3, and once unit k+1's row pointers have landed it
+// bulk-copies that unit's contiguous column segment.  The block computes
+// unit k from shared memory; only the neighbour-position gathers go to
+// global memory (L2).  Tiles hold 256 vertices relabelled by degree; a unit
+// is one pass of a tile: 256/G vertices with G lanes each.
+template <int DIM, int OPT, bool WEIGHTED, int NORM>
+__global__ void __launch_bounds__(kBlock, IVHD_MINBLOCKS) step_kernel(StepArgs A) {
   using L = Layout<DIM, OPT>;
+  using SL = StageLayout<DIM, OPT>;
   constexpr bool NEST = (OPT == OPT_NEST);
   constexpr int SSX = L::SS > 0 ? L::SS : 1;
+  constexpr int YS = L::YS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar_a[kStages], bar_b[kStages];
+  __shared__ StageMeta meta[kStages];
+  __shared__ double4 sm_unit[2][kBlock / 32];
   __shared__ double4 sm_red[kBlock / 32];
-  __shared__ int sm_tile;
+  __shared__ int sm_units[kUnitCache];  // this block's unit words (static schedule)
 
   Ctrl* ctrl = A.ctrl;
   if (ctrl->status != 0) return;  // diverged earlier: later iterations are no-ops
-  const int cur = ctrl->cur;
+  const int ycur = ctrl->cur;
   const float c = (float)ctrl->c;
   const float step = (float)ctrl->step;
   const long long gstep = ctrl->gstep;
-  const float* __restrict__ Yin = cur ? A.ybuf1 : A.ybuf0;
-  float* __restrict__ Yout = cur ? A.ybuf0 : A.ybuf1;
+  const float* __restrict__ Yin = ycur ? A.ybuf1 : A.ybuf0;
+  float* __restrict__ Yout = ycur ? A.ybuf0 : A.ybuf1;
   const int tid = threadIdx.x;
 
   float bc1 = 1.f, bc2 = 1.f;  // Adam bias corrections (optim.py:203-204)
@@ -465,39 +551,116 @@ __global__ void __launch_bounds__(kBlock, 3) step_kernel(StepArgs A) {
     bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
   }
 
-  // Work unit = one pass of a tile: 256/G vertices with G lanes each.  Heavy
-  // tiles (large G) thus spread over many blocks instead of serialising G
-  // passes in one; each unit writes its own partial (fixed unit order).
-  while (true) {
-    if (tid == 0) sm_tile = (int)atomicAdd(&ctrl->next_tile, 1u);
-    block_sync();
-    const int unit = sm_tile;
-    if (unit >= A.n_tiles) break;
-    const int packed = __ldg(A.units + A.tile0 + unit);
-    const int tile = packed >> 6, pass = packed & 63;
-    const long long v0 = (long long)tile * kBlock;
-    const int G = A.tile_g[tile];
-    const int lgG = __ffs(G) - 1;
-    const int lg = tid & (G - 1);
-    const int grp = tid >> lgG;
-    const int groups = kBlock >> lgG;
-    double acc_e = 0.0, acc_n = 0.0, acc_o = 0.0, acc_bad = 0.0;
+  const int n_units = A.n_tiles;
+  const int grid = gridDim.x;
+  const int my_units = blockIdx.x < n_units ? (n_units - 1 - blockIdx.x) / grid + 1 : 0;
 
+  for (int k = tid; k < min(my_units, kUnitCache); k += kBlock)
+    sm_units[k] = __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bar_a[s], 1);
+      mbar_init(&bar_b[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  block_sync();
+
+  // producer helpers (thread 0 only)
+  auto unit_range = [&](int packed, long long& va, int& nv) {
+    const int tile = packed >> 8, pass = (packed >> 3) & 31, lgG = packed & 7;
+    const int groups = kBlock >> lgG;
+    va = (long long)tile * kBlock + (long long)pass * groups;
+    nv = (int)max(0LL, min((long long)groups, A.v_end - va));
+  };
+  auto issue_front = [&](int k) {  // row pointers + positions + state of local unit k
+    const int s = k % kStages;
+    unsigned char* st = smem_raw + s * SL::BYTES;
+    const int packed = k < kUnitCache ? sm_units[k] : __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
+    long long va;
+    int nv;
+    unit_range(packed, va, nv);
+    meta[s].packed = packed;
+    const uint32_t rp_bytes = (uint32_t)((nv + 1) * 4 + 15) / 16 * 16;
+    const uint32_t y_bytes = (uint32_t)nv * YS * 4;  // nv is a multiple of 8 except at the end
+    const uint32_t y_copy = (y_bytes + 15) / 16 * 16;
+    uint32_t s_copy = 0;
+    if constexpr (L::SS > 0) s_copy = ((uint32_t)nv * L::SS * 4 + 15) / 16 * 16;
+    mbar_expect_tx(&bar_a[s], rp_bytes + y_copy + s_copy);
+    bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_a[s]);
+    bulk_g2s(st + SL::Y_OFF, Yin + va * YS, y_copy, &bar_a[s]);
+    if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, A.state + va * L::SS, s_copy, &bar_a[s]);
+  };
+  auto issue_cols = [&](int k) {  // column segment of local unit k (its row pointers have landed)
+    const int s = k % kStages;
+    unsigned char* st = smem_raw + s * SL::BYTES;
+    mbar_wait(&bar_a[s], (uint32_t)(k / kStages) & 1);
+    long long va;
+    int nv;
+    unit_range(meta[s].packed, va, nv);
+    const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
+    const uint32_t e0 = rp[0], e1 = rp[nv];
+    const uint32_t a0 = e0 & ~3u, a1 = (e1 + 3u) & ~3u;  // 16-byte aligned cover
+    if (nv > 0 && e1 > e0 && a1 - a0 <= (uint32_t)kColCap + 4) {
+      meta[s].col_off = (int)(e0 - a0);
+      meta[s].staged = 1;
+      mbar_expect_tx(&bar_b[s], (a1 - a0) * 4);
+      bulk_g2s(st + SL::COL_OFF, A.col + a0, (a1 - a0) * 4, &bar_b[s]);
+    } else {
+      meta[s].col_off = 0;
+      meta[s].staged = 0;
+      mbar_arrive(&bar_b[s]);
+    }
+  };
+
+  if (tid == 0) {
+    if (my_units > 0) issue_front(0);
+    if (my_units > 1) issue_front(1);
+    if (my_units > 0) issue_cols(0);
+  }
+
+  int buf = 0;
+  for (int k = 0; k < my_units; ++k) {
+    const int u = blockIdx.x + k * grid;
+    const int s = k % kStages;
+    unsigned char* st = smem_raw + s * SL::BYTES;
+    if (tid == 0) {
+      if (k + 2 < my_units) issue_front(k + 2);
+      if (k + 1 < my_units) issue_cols(k + 1);
+    }
+    const uint32_t par = (uint32_t)(k / kStages) & 1;
+    mbar_wait(&bar_a[s], par);
+    mbar_wait(&bar_b[s], par);
+
+    const int packed = meta[s].packed;
+    const int lgG = packed & 7, G = 1 << lgG;
+    const int lg = tid & (G - 1), grp = tid >> lgG;
+    long long va;
+    int nv;
     {
-      const long long v = v0 + (long long)pass * groups + grp;
-      const bool active = v < A.v_end;
-      uint32_t beg = 0, end = 0;
-      float yi[DIM], li[DIM], sv[SSX];
-      if (active) {
-        beg = __ldg(A.row_ptr + v);
-        end = __ldg(A.row_ptr + v + 1);
-        gather<DIM, NEST>(Yin, (uint32_t)v, yi, li);
-        if constexpr (L::SS > 0) {
-          if (lg == 0) ld_state<L::SS>(A.state + (size_t)v * L::SS, sv);
-        }
-      } else {
+      const int tile = packed >> 8, pass = (packed >> 3) & 31;
+      const int groups = kBlock >> lgG;
+      va = (long long)tile * kBlock + (long long)pass * groups;
+      nv = (int)max(0LL, min((long long)groups, A.v_end - va));
+    }
+    const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
+    const uint32_t* colst = reinterpret_cast<const uint32_t*>(st + SL::COL_OFF);
+    const float* ys = reinterpret_cast<const float*>(st + SL::Y_OFF);
+    const float* ss = reinterpret_cast<const float*>(st + SL::S_OFF);
+    const bool staged = meta[s].staged != 0;
+    const uint32_t e0 = rp[0];
+    const int coff = meta[s].col_off;
+
+    double acc_e = 0.0, acc_n = 0.0, acc_o = 0.0, acc_bad = 0.0;
+    const bool active = grp < nv;
+    if (active) {
+      const long long v = va + grp;
+      const uint32_t beg = rp[grp], end = rp[grp + 1];
+      float yi[DIM], li[DIM];
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) yi[d] = li[d] = 0.f;
+      for (int d = 0; d < DIM; ++d) {
+        yi[d] = ys[grp * YS + d];
+        li[d] = NEST ? ys[grp * YS + (DIM == 2 ? 2 : 4) + d] : yi[d];
       }
       float f[DIM];
 #pragma unroll
@@ -508,51 +671,70 @@ __global__ void __launch_bounds__(kBlock, 3) step_kernel(StepArgs A) {
         float2 tw[WEIGHTED ? kUnroll : 1];
         float gy[kUnroll][DIM], gl[kUnroll][DIM];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const uint32_t k = k0 + (uint32_t)(u * G);
-          if (k < end) cw[u] = __ldg(A.col + k);
+        for (int q = 0; q < kUnroll; ++q) {
+          const uint32_t kk = k0 + (uint32_t)(q * G);
+          if (kk < end) cw[q] = staged ? colst[kk - e0 + coff] : __ldg(A.col + kk);
         }
         if constexpr (WEIGHTED) {
 #pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            const uint32_t k = k0 + (uint32_t)(u * G);
-            if (k < end) tw[u] = __ldg(A.ew + k);
+          for (int q = 0; q < kUnroll; ++q) {
+            const uint32_t kk = k0 + (uint32_t)(q * G);
+            if (kk < end) tw[q] = __ldg(A.ew + kk);
           }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const uint32_t k = k0 + (uint32_t)(u * G);
-          if (k < end) gather<DIM, NEST>(Yin, cw[u] & kIdMask, gy[u], gl[u]);
+        for (int q = 0; q < kUnroll; ++q) {
+          const uint32_t kk = k0 + (uint32_t)(q * G);
+          if (kk < end) gather<DIM, NEST>(Yin, cw[q] & kIdMask, gy[q], gl[q]);
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const uint32_t k = k0 + (uint32_t)(u * G);
-          if (k < end) {
-            float2 twu = make_float2(0.f, 0.f);
-            if constexpr (WEIGHTED) twu = tw[u];
-            entry<DIM, NEST>(yi, li, gy[u], gl[u], cw[u], WEIGHTED, twu, c, A.norm, (uint32_t)v,
-                             gstep, f, e);
+        for (int q = 0; q < kUnroll; ++q) {
+          const uint32_t kk = k0 + (uint32_t)(q * G);
+          if (kk < end) {
+            float2 twq = make_float2(0.f, 0.f);
+            if constexpr (WEIGHTED) twq = tw[q];
+            entry<DIM, NEST, NORM>(yi, li, gy[q], gl[q], cw[q], WEIGHTED, twq, c, (uint32_t)v, gstep, f, e);
           }
         }
       }
-      // fixed xor butterfly over the G lanes of the group (G uniform per tile)
-      for (int o = G >> 1; o > 0; o >>= 1) {
+      // fixed xor butterfly over the G lanes of the group (G uniform per unit);
+      // the mask names exactly this group's lanes (the walk leaves the warp diverged)
+      if (G > 1) {
+        const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((tid & 31) & ~(G - 1));
+        for (int o = G >> 1; o > 0; o >>= 1) {
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) f[d] += __shfl_xor_sync(0xffffffffu, f[d], o);
-        e += __shfl_xor_sync(0xffffffffu, e, o);
+          for (int d = 0; d < DIM; ++d) f[d] += __shfl_xor_sync(gmask, f[d], o);
+          e += __shfl_xor_sync(gmask, e, o);
+        }
       }
-      if (active && lg == 0) {
-        acc_e += (double)e;
+      if (lg == 0) {
+        acc_e = (double)e;
         if constexpr (OPT == OPT_NONE) {
 #pragma unroll
           for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)f[d];
         } else {
+          float sv[SSX];
+#pragma unroll
+          for (int q = 0; q < SSX; ++q) sv[q] = L::SS > 0 ? ss[grp * SSX + q] : 0.f;
           apply_update<DIM, OPT>(A, Yout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
         }
       }
     }
-    const double4 tot = block_sum4(make_double4(acc_e, acc_n, acc_o, acc_bad), sm_red);
-    if (tid == 0) A.partial[A.tile0 + unit] = tot;
+    // unit partial: fixed warp butterfly, then warps 0..7 in order
+    acc_e = warp_dsum(acc_e); acc_n = warp_dsum(acc_n); acc_o = warp_dsum(acc_o); acc_bad = warp_dsum(acc_bad);
+    if ((tid & 31) == 0) sm_unit[buf][tid >> 5] = make_double4(acc_e, acc_n, acc_o, acc_bad);
+    block_sync();  // also: every thread is done reading stage s before it is refilled
+    if (tid == 0) {
+      double4 t = make_double4(0, 0, 0, 0);
+#pragma unroll
+      for (int w = 0; w < kBlock / 32; ++w) {
+        const double4 q = sm_unit[buf][w];
+        t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
+      }
+      A.partial[A.tile0 + u] = t;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async refills
+    }
+    buf ^= 1;
   }
 
   if (!A.fuse_finalize) return;
