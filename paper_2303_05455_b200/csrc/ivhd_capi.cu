@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -439,6 +440,11 @@ int pull_ctrl(ivhd_ctx* ctx);
 // longest tiles early).  Positions/state already uploaded are re-ordered.
 int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
   const int64_t m = ctx->m;
+  const char* order = getenv("IVHD_ORDER");  // experiments: "identity" keeps the caller's order
+  if (order && strcmp(order, "identity") == 0) {
+    ctx->perm_fixed = true;
+    return IVHD_OK;
+  }
   cudaStream_t st = ctx->stream;
   uint32_t *deg = nullptr, *deg2 = nullptr;
   int32_t *ids = nullptr, *perm = nullptr;

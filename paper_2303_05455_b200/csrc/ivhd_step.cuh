@@ -33,7 +33,10 @@
 namespace ivhd {
 
 
-constexpr int kBlock = 256;
+#ifndef IVHD_BLOCK
+#define IVHD_BLOCK 256
+#endif
+constexpr int kBlock = IVHD_BLOCK;  // threads per block = vertices per tile
 
 // Block barrier.  __syncthreads() lowers to the *aligned* bar.sync, which
 // assumes every warp arrives converged; after the data-dependent merge-path
@@ -182,11 +185,19 @@ __device__ __noinline__ void degenerate_dir(uint32_t i, uint32_t j, long long st
 // The L2 form is branch-free: with rs = rsqrt(d^2), w (t - d)/d = w (t rs - 1)
 // and d = d^2 rs (guarded at 0 and inf).  Random pairs at exactly zero
 // distance (t != 0, d == 0) take the rare degenerate branch (forces.py:167-174).
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Adds the entry's force and stress contribution when `valid`; returns true
+// for a degenerate random pair (t != 0 at zero distance), whose force the
+// caller adds separately (rare path).  Branch-free.
 template <int DIM, bool NEST, int NORM>
-__device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[DIM],
+__device__ __forceinline__ bool entry(const float (&yi)[DIM], const float (&li)[DIM],
                                       const float (&yo)[DIM], const float (&lo)[DIM],
-                                      uint32_t cw, bool weighted, float2 tw,
-                                      float c, uint32_t i, long long step,
+                                      uint32_t cw, bool weighted, float2 tw, float c, bool valid,
                                       float (&f)[DIM], float& e) {
   const bool rn = cw & kRandBit;
   float t, w;
@@ -205,18 +216,16 @@ __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[
     d2 = fmaf(df[d], df[d], d2);
     d1 += fabsf(df[d]);
   }
+  bool degen = false;
   if constexpr (NORM == 0) {
-    const float rs = rsqrtf(d2);
+    const float rs = rsqrt_ftz(d2);
     float phi = (t == 0.f) ? -w : w * fmaf(t, rs, -1.f);
-    if (t != 0.f && d2 == 0.f) {  // degenerate random pair
-      float u[DIM];
-      degenerate_dir<DIM>(i, cw & kIdMask, step, u);
+    degen = (t != 0.f) && (d2 == 0.f);
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) f[d] = fmaf(w * t, u[d], f[d]);
-      phi = 0.f;
+    for (int d = 0; d < DIM; ++d) {
+      const float inc = phi * df[d];
+      f[d] += (valid && !degen) ? inc : 0.f;
     }
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) f[d] = fmaf(phi, df[d], f[d]);
     float q2 = d2, qs = rs;
     if constexpr (NEST) {  // stress at the current (not look-ahead) positions: engine.py:370
       q2 = 0.f;
@@ -225,19 +234,21 @@ __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[
         const float q = yi[d] - yo[d];
         q2 = fmaf(q, q, q2);
       }
-      qs = rsqrtf(q2);
+      qs = rsqrt_ftz(q2);
     }
     float de = q2 * qs;
     de = (q2 == 0.f) ? 0.f : de;
     de = (q2 == INFINITY) ? INFINITY : de;
     const float r = t - de;
-    e = fmaf(w * r, r, e);
+    const float inc = w * r * r;
+    e += valid ? inc : 0.f;
   } else {
     const float s = w * (t - d1);
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       const float sg = df[d] > 0.f ? 1.f : (df[d] < 0.f ? -1.f : (df[d] == 0.f ? 0.f : df[d]));
-      f[d] = fmaf(sg, s, f[d]);
+      const float inc = sg * s;
+      f[d] += valid ? inc : 0.f;
     }
     float de = d1;
     if constexpr (NEST) {
@@ -246,8 +257,10 @@ __device__ __forceinline__ void entry(const float (&yi)[DIM], const float (&li)[
       for (int d = 0; d < DIM; ++d) de += fabsf(yi[d] - yo[d]);
     }
     const float r = t - de;
-    e = fmaf(w * r, r, e);
+    const float inc = w * r * r;
+    e += valid ? inc : 0.f;
   }
+  return valid && degen;
 }
 
 __device__ __forceinline__ bool all_finite(const float* v, int n) {
@@ -450,8 +463,6 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
 #endif
 constexpr int kUnroll = IVHD_UNROLL;
 constexpr int kStages = 3;         // TMA ring depth (units in flight per block)
-constexpr int kColCap = 2048;      // staged column entries per unit (larger units read global)
-constexpr int kUnitCache = 1024;   // unit words cached per block
 
 // ------------------------------------------------------------- TMA helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -484,6 +495,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
+
+constexpr int kColCap = 2048;      // staged column entries per unit (larger units read global)
+constexpr int kUnitCache = 1024;   // unit words cached per block
 
 // Shared-memory layout of one ring stage for (DIM, OPT).
 template <int DIM, int OPT>
@@ -670,30 +684,53 @@ __global__ void __launch_bounds__(kBlock, IVHD_MINBLOCKS) step_kernel(StepArgs A
         uint32_t cw[kUnroll];
         float2 tw[WEIGHTED ? kUnroll : 1];
         float gy[kUnroll][DIM], gl[kUnroll][DIM];
+        // A slot past the row end becomes a zero-target pair with the vertex
+        // itself: zero distance, zero force, zero stress — no masking needed.
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
           const uint32_t kk = k0 + (uint32_t)(q * G);
+          cw[q] = (uint32_t)v;
           if (kk < end) cw[q] = staged ? colst[kk - e0 + coff] : __ldg(A.col + kk);
         }
         if constexpr (WEIGHTED) {
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
             const uint32_t kk = k0 + (uint32_t)(q * G);
+            tw[q] = make_float2(0.f, 1.f);
             if (kk < end) tw[q] = __ldg(A.ew + kk);
           }
         }
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
-          const uint32_t kk = k0 + (uint32_t)(q * G);
-          if (kk < end) gather<DIM, NEST>(Yin, cw[q] & kIdMask, gy[q], gl[q]);
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            gy[q][d] = yi[d];
+            gl[q][d] = li[d];
+          }
+          if (k0 + (uint32_t)(q * G) < end) gather<DIM, NEST>(Yin, cw[q] & kIdMask, gy[q], gl[q]);
         }
+        unsigned dmask = 0;
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
-          const uint32_t kk = k0 + (uint32_t)(q * G);
-          if (kk < end) {
-            float2 twq = make_float2(0.f, 0.f);
-            if constexpr (WEIGHTED) twq = tw[q];
-            entry<DIM, NEST, NORM>(yi, li, gy[q], gl[q], cw[q], WEIGHTED, twq, c, (uint32_t)v, gstep, f, e);
+          float2 twq = make_float2(0.f, 0.f);
+          if constexpr (WEIGHTED) twq = tw[q];
+          if (entry<DIM, NEST, NORM>(yi, li, gy[q], gl[q], cw[q], WEIGHTED, twq, c, true, f, e)) dmask |= 1u << q;
+        }
+        if (dmask) {  // degenerate random pairs (forces.py:167-174): measure-zero path
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            if ((dmask >> q) & 1u) {
+              const bool rn = cw[q] & kRandBit;
+              float t = rn ? 1.f : 0.f, w = rn ? c : 1.f;
+              if constexpr (WEIGHTED) {
+                t = tw[q].x;
+                w *= tw[q].y;
+              }
+              float uvec[DIM];
+              degenerate_dir<DIM>((uint32_t)v, cw[q] & kIdMask, gstep, uvec);
+#pragma unroll
+              for (int d = 0; d < DIM; ++d) f[d] = fmaf(w * t, uvec[d], f[d]);
+            }
           }
         }
       }
@@ -720,9 +757,16 @@ __global__ void __launch_bounds__(kBlock, IVHD_MINBLOCKS) step_kernel(StepArgs A
         }
       }
     }
-    // unit partial: fixed warp butterfly, then warps 0..7 in order
-    acc_e = warp_dsum(acc_e); acc_n = warp_dsum(acc_n); acc_o = warp_dsum(acc_o); acc_bad = warp_dsum(acc_bad);
-    if ((tid & 31) == 0) sm_unit[buf][tid >> 5] = make_double4(acc_e, acc_n, acc_o, acc_bad);
+    // unit partial: fixed float warp butterfly, then warps 0..7 in order in double
+    float pe = (float)acc_e, pn = (float)acc_n, po = (float)acc_o, pb = (float)acc_bad;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      pe += __shfl_xor_sync(0xffffffffu, pe, o);
+      pn += __shfl_xor_sync(0xffffffffu, pn, o);
+      po += __shfl_xor_sync(0xffffffffu, po, o);
+      pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    }
+    if ((tid & 31) == 0) sm_unit[buf][tid >> 5] = make_double4(pe, pn, po, pb);
     block_sync();  // also: every thread is done reading stage s before it is refilled
     if (tid == 0) {
       double4 t = make_double4(0, 0, 0, 0);

@@ -48,7 +48,9 @@ if __name__ == "__main__":
         np.save(CACHE, nb)
     for lib in sys.argv[1:]:
         for kind, m in graphs:
-            env = dict(os.environ, IVHD_B200_LIB=os.path.abspath(lib))
+            env = dict(os.environ, IVHD_B200_LIB=os.path.abspath(lib.split("@")[0]))
+            if "@" in lib:
+                env["IVHD_ORDER"] = lib.split("@")[1]
             r = subprocess.run([sys.executable, __file__, "--child", "300", kind, str(m)], env=env,
                                capture_output=True, text=True)
             print(r.stdout.strip() or r.stderr[-800:], flush=True)
