@@ -14,7 +14,11 @@ except Exception:  # pragma: no cover - reference not installed
 
 def _bases(name, *own):
     extra = getattr(_ref, name, None) if _ref is not None else None
-    return own + ((extra,) if extra is not None else ())
+    if extra is None:
+        return own
+    if own == (Exception,):
+        return (extra,)
+    return own + (extra,)
 
 
 class IvhdError(*_bases("IvhdError", Exception)):

@@ -1,0 +1,135 @@
+"""Vertex-range sharding of the IVHD loop across GPUs.
+
+The update is synchronous (Jacobi): every force of iteration n is computed
+from the same positions Y_n (engine.py:360-372), so vertex ranges are
+independent given Y_n and one exchange per iteration suffices.
+
+Each rank holds the full (relabelled) symmetrised CSR and a full replica of
+the positions, updates the vertices of its tile-aligned range [v0, v1) with
+the fused step kernel (ivhd_step_local), then all-gathers
+
+  * its slice of the new positions (8 B/vertex in 2-D), and
+  * its per-tile partials {stress, sum|dnew|^2, sum|dold|^2, #non-finite},
+
+and every rank runs the same fixed-order finalizer (ivhd_step_finalize) over
+the full tile array — so the auto-adapt commit/rollback decision, the trace
+and the positions are identical on all ranks, and identical to a single-GPU
+run (tiles and their reduction order do not depend on the rank count).
+
+The exchange goes through torch.distributed (NCCL over NVLink on GPUs, gloo
+for the CPU tests); the library launches on the caller's CUDA stream so the
+collectives are ordered with the kernels.
+"""
+
+import numpy as np
+
+from .errors import InvalidArgumentError
+
+
+def shard_ranges(n_tiles_cap, tile_v, world):
+    """Equal tile counts per rank (the padded tile count is a multiple of 8)."""
+    if world < 1 or n_tiles_cap % world:
+        raise InvalidArgumentError(f"world size {world} must divide the padded tile count {n_tiles_cap}")
+    per = n_tiles_cap // world
+    return [(r * per * tile_v, (r + 1) * per * tile_v) for r in range(world)]
+
+
+class _CudaArray:
+    """Zero-copy __cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class DeviceShardBackend:
+    """The real backend: one DeviceEmbedding (C ABI) per rank."""
+
+    def __init__(self, dev):
+        self.dev = dev
+
+    def __getattr__(self, name):
+        return getattr(self.dev, name)
+
+    def exchange_views(self):
+        import torch
+
+        b = self.dev.shard_buffers()
+        tile_v, n_tiles = self.dev.tiles()
+        n_floats = n_tiles * tile_v * b["floats_per_vertex"]
+        ynext = torch.as_tensor(_CudaArray(b["ybuf"][1 - b["cur"]], n_floats, "<f4"), device="cuda")
+        parts = torch.as_tensor(_CudaArray(b["partials"], n_tiles * 4, "<f8"), device="cuda")
+        return ynext, parts
+
+
+def _allgather_inplace(buf, rank, world, group=None):
+    """All ranks contribute chunk `rank` of `buf`; afterwards every rank holds all chunks."""
+    import torch
+    import torch.distributed as dist
+
+    chunk = buf.numel() // world
+    mine = buf[rank * chunk:(rank + 1) * chunk]
+    if buf.is_cuda:
+        dist.all_gather_into_tensor(buf, mine.clone(), group=group)
+    else:
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine.clone(), group=group)
+        buf.copy_(torch.cat(parts))
+
+
+class ShardedEmbedding:
+    """One rank's share of a distributed IVHD run (same surface as
+    DeviceEmbedding for set-up; `run` drives the per-iteration exchange)."""
+
+    def __init__(self, m, dim, rank, world, device=0, stream=0, group=None, backend=None):
+        if backend is None:
+            from .device import DeviceEmbedding
+
+            backend = DeviceShardBackend(DeviceEmbedding(m, dim, device=device, stream=stream))
+        self.backend = backend
+        self.m, self.dim, self.rank, self.world, self.group = int(m), int(dim), int(rank), int(world), group
+        tile_v, n_tiles_cap = backend.tiles()
+        self.ranges = shard_ranges(n_tiles_cap, tile_v, self.world)
+        self.v0, self.v1 = self.ranges[self.rank]
+        backend.shard_set_range(self.v0, self.v1)
+
+    # set-up: identical on every rank (same graph, same seeded draws)
+    def set_graph(self, slot, nn_sets, rn_assign):
+        self.backend.set_graph(slot, nn_sets, rn_assign)
+
+    def set_connections(self, *a, **k):
+        self.backend.set_connections(*a, **k)
+
+    def set_positions(self, y):
+        self.backend.set_positions(y)
+
+    def set_optimizer(self, params):
+        self.backend.set_optimizer(params)
+
+    def positions(self):
+        return self.backend.positions()
+
+    def snapshot(self):
+        self.backend.snapshot()
+
+    def restore(self):
+        self.backend.restore()
+
+    def step(self, slot, norm, c):
+        """One iteration: local update, exchange, fixed-order decision."""
+        self.backend.step_local(slot, norm, c)
+        ynext, parts = self.backend.exchange_views()
+        _allgather_inplace(ynext, self.rank, self.world, self.group)
+        _allgather_inplace(parts, self.rank, self.world, self.group)
+        return self.backend.step_finalize()
+
+    def run(self, slot, norm, c, n_iter):
+        """Same contract as DeviceEmbedding.run: (stress[], step[], done, diverged)."""
+        stress, step = [], []
+        for it in range(int(n_iter)):
+            e, b, _committed, div = self.step(slot, norm, c)
+            stress.append(e)
+            step.append(b)
+            if div:
+                return np.array(stress), np.array(step), it, True
+        return np.array(stress), np.array(step), int(n_iter), False

@@ -1,0 +1,143 @@
+"""System-level GPU tests: the NCCL sharded path, full-run quality parity
+against the CPU oracle, determinism, observer/mutation flow.  Marked gpu."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle.ivhd_oracle import OracleRun
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2303_05455_b200")
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem(m=6000, seed=0):
+    from paper_2303_05455_b200 import synth
+
+    return synth.planted_graph(m, 3, seed=seed)
+
+
+def test_sharded_nccl_world1_is_bit_identical_to_single_gpu():
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_05455_b200.config import resolve_optimizer
+    from paper_2303_05455_b200.device import DeviceEmbedding
+    from paper_2303_05455_b200.embed import init_layout, sample_random_neighbors
+    from paper_2303_05455_b200.sharded import ShardedEmbedding
+
+    nb = _problem()
+    m = nb.shape[0]
+    rng = np.random.default_rng(1)
+    y0 = init_layout(m, 2, rng)
+    rn = sample_random_neighbors(m, nb, 1, rng)
+    ref = DeviceEmbedding(m, 2)
+    ref.set_optimizer(resolve_optimizer("force-directed", m))
+    ref.set_positions(y0)
+    ref.set_graph(0, nb, rn)
+    s_ref, b_ref, _, _ = ref.run(0, "l2", 0.1, 40)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        stream = torch.cuda.current_stream()
+        sh = ShardedEmbedding(m, 2, 0, 1, stream=stream.cuda_stream)
+        sh.set_optimizer(resolve_optimizer("force-directed", m))
+        sh.set_positions(y0)
+        sh.set_graph(0, nb, rn)
+        s_sh, b_sh, done, div = sh.run(0, "l2", 0.1, 40)
+        assert done == 40 and not div
+        np.testing.assert_array_equal(sh.positions(), ref.positions())
+        np.testing.assert_array_equal(np.asarray(s_sh), s_ref)
+        np.testing.assert_array_equal(np.asarray(b_sh), b_ref)
+    finally:
+        dist.destroy_process_group()
+
+
+def _knn_preservation(Y, nb, k=2):
+    """Fraction of graph neighbours among each point's k nearest in 2-D."""
+    from scipy.spatial import cKDTree
+
+    _, idx = cKDTree(Y).query(Y, k=k + 1)
+    hits = [len(set(idx[i, 1:]) & set(nb[i, :k])) for i in range(len(Y))]
+    return float(np.mean(hits)) / k
+
+
+def _neighbor_hit(Y, labels, k=10):
+    from scipy.spatial import cKDTree
+
+    _, idx = cKDTree(Y).query(Y, k=k + 1)
+    return float((labels[idx[:, 1:]] == labels[:, None]).mean())
+
+
+def test_full_run_quality_matches_oracle_within_1pct():
+    """North star: after a full run the stress and the kNN-preservation /
+    neighbour-hit quality agree with the CPU reference within 1%."""
+    import torch
+
+    from paper_2303_05455_b200 import synth
+
+    m = 4000
+    nb, _, labels = synth.mixture_knn_graph(m, 20, k=2, clusters=6, seed=3)
+    cfg = dict(nn=2, rn=1, c=0.1, iterations=600, seed=0)
+    res = P.run_embedding(graph=P.KnnGraph(nb), config=P.EmbeddingConfig(**cfg))
+    ref = OracleRun(nb, **cfg)
+    ref.run()
+    assert res.state.stress == pytest.approx(ref.trace_stress[-1], rel=1e-2)
+    q_gpu, q_ref = _knn_preservation(res.embedding.points, nb), _knn_preservation(ref.Y, nb)
+    h_gpu, h_ref = _neighbor_hit(res.embedding.points, labels), _neighbor_hit(ref.Y, labels)
+    assert abs(q_gpu - q_ref) <= 0.01 * max(q_ref, 1e-9) + 1e-3
+    assert abs(h_gpu - h_ref) <= 0.01 * h_ref
+    torch.cuda.synchronize()
+
+
+def test_observer_stop_and_mutations_on_device():
+    nb = _problem(2000)
+    seen = []
+
+    def obs(it, pos, stress, params):
+        seen.append((it, params["b"], params["c"]))
+        if it == 3:
+            return {"c": 0.05, "b": 0.004}
+        if it == 9:
+            return {"stop": True}
+
+    res = P.run_embedding(graph=P.KnnGraph(nb), config=P.EmbeddingConfig(nn=3, rn=1, iterations=100),
+                          observer=obs)
+    assert len(res.trace.iterations) == 10
+    assert (3, "c", 0.05) in res.mutations and (3, "b", 0.004) in res.mutations
+    assert seen[4][2] == 0.05
+    # iteration 4 stepped with b = 0.004 (then possibly adapted by gamma1/gamma2)
+    assert any(seen[4][1] == pytest.approx(0.004 * g) for g in (1.0, 1.1, 0.9))
+
+
+def test_optimizer_swap_mid_run_keeps_positions():
+    nb = _problem(2000)
+
+    def obs(it, pos, stress, params):
+        if it == 4:
+            return {"optimizer": "nesterov"}
+
+    res = P.run_embedding(graph=P.KnnGraph(nb), config=P.EmbeddingConfig(nn=3, rn=1, iterations=20),
+                          observer=obs)
+    assert (4, "optimizer", "nesterov") in res.mutations
+    assert np.isfinite(res.embedding.points).all()
+
+
+def test_large_graph_runs_and_is_deterministic():
+    nb = _problem(300_000)
+    cfg = P.EmbeddingConfig(nn=3, rn=1, c=0.1, iterations=150, seed=2)
+    a = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    b = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    np.testing.assert_array_equal(a.embedding.points, b.embedding.points)
+    assert a.trace.stress == b.trace.stress
+    assert a.trace.stress[-1] < a.trace.stress[0]

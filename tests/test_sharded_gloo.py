@@ -1,0 +1,147 @@
+"""The multi-GPU driver (paper_2303_05455_b200/sharded.py) on CPU: two gloo
+ranks exchange position slices and tile partials exactly as the NCCL path
+does.  The per-rank compute is a numpy stand-in backend built from the CPU
+oracle (test infrastructure) with the library's tile/partial/decision
+contract, so the test checks the sharding, exchange and fixed-order decision
+logic: every rank ends bit-identical, a 2-rank run is bit-identical to a
+1-rank run, and both follow the oracle's force-directed trajectory."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from oracle.ivhd_oracle import OracleRun
+from paper_2303_05455_b200.sharded import ShardedEmbedding
+
+TILE = 256
+
+
+class NumpyShardBackend:
+    """CPU stand-in for DeviceShardBackend (float64, force-directed)."""
+
+    def __init__(self, m, conn, a=0.99, b=0.002, tau=None, c=0.1):
+        self.m, self.conn, self.c = m, conn, c
+        self.a, self.b, self.tau = a, b, 1e-3 * m if tau is None else tau
+        self.n_tiles_cap = ((m + TILE - 1) // TILE + 7) // 8 * 8
+        cap = self.n_tiles_cap * TILE
+        self.Y = [torch.zeros(cap * 2, dtype=torch.float64), torch.zeros(cap * 2, dtype=torch.float64)]
+        self.delta = np.zeros((cap, 2))
+        self.parts = torch.zeros(self.n_tiles_cap * 4, dtype=torch.float64)
+        self.cur = 0
+        self.csr = O.symmetrise(conn, m)
+
+    def tiles(self):
+        return TILE, self.n_tiles_cap
+
+    def shard_set_range(self, v0, v1):
+        self.v0, self.v1 = v0, v1
+
+    def set_positions(self, y):
+        self.Y[self.cur][: self.m * 2] = torch.from_numpy(np.asarray(y, dtype=np.float64).ravel())
+
+    def positions(self):
+        return self.Y[self.cur][: self.m * 2].numpy().reshape(self.m, 2).copy()
+
+    def step_local(self, slot, norm, c):
+        y = self.positions()
+        f, _ = O.csr_forces(y, self.csr, self.conn, self.c, norm)
+        row_ptr, other, cidx = self.csr
+        rows = np.repeat(np.arange(self.m), np.diff(row_ptr))
+        d = np.sqrt(((y[rows] - y[other]) ** 2).sum(axis=1))
+        w = self.conn.weights(self.c)[cidx]
+        e_row = np.bincount(rows, weights=w * (self.conn.target[cidx] - d) ** 2, minlength=self.m)
+        ynext = self.Y[1 - self.cur].numpy().reshape(-1, 2)
+        parts = self.parts.numpy().reshape(-1, 4)
+        for t in range(self.v0 // TILE, self.v1 // TILE):
+            lo, hi = t * TILE, min((t + 1) * TILE, self.m)
+            acc = np.zeros(4)
+            for v in range(lo, hi):
+                old = self.delta[v].copy()
+                new = self.a * old + self.b * f[v]
+                self.delta[v] = new
+                ynext[v] = y[v] + new
+                acc += [e_row[v], new @ new, old @ old, 0.0 if np.isfinite(ynext[v]).all() else 1.0]
+            parts[t] = acc
+
+    def exchange_views(self):
+        return self.Y[1 - self.cur], self.parts
+
+    def step_finalize(self):
+        s = self.parts.numpy().reshape(-1, 4).sum(axis=0)
+        E, dT = 0.5 * s[0], s[1] - s[2]
+        commit = True
+        if dT > self.tau:
+            self.b *= 0.9
+            commit = False
+        elif dT < -self.tau:
+            self.b *= 1.1
+            commit = False
+        if commit:
+            self.cur ^= 1
+        return E, self.b, commit, False
+
+
+def _problem(m=700, seed=0):
+    rng = np.random.default_rng(seed)
+    nb = ((np.arange(m)[:, None] + rng.integers(1, 30, size=(m, 2))) % m).astype(np.int32)
+    orc = OracleRun(nb, nn=2, rn=1, c=0.1, iterations=30, seed=seed)
+    return nb, orc
+
+
+def _worker(rank, world, port, iters, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nb, orc = _problem()
+        be = NumpyShardBackend(orc.m, orc.full)
+        sh = ShardedEmbedding(orc.m, 2, rank, world, backend=be)
+        sh.set_positions(orc.Y)
+        stress, steps, done, div = sh.run(0, "l2", 0.1, iters)
+        np.savez(os.path.join(out, f"rank{rank}_of{world}.npz"), y=sh.positions(), stress=stress, b=steps)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.timeout(300)
+def test_two_gloo_ranks_match_one_rank_and_oracle(tmp_path):
+    iters = 12
+    for world in (1, 2):
+        mp.start_processes(_worker, args=(world, _free_port(), iters, str(tmp_path)), nprocs=world,
+                           start_method="spawn", join=True)
+    r1 = np.load(tmp_path / "rank0_of1.npz")
+    a = np.load(tmp_path / "rank0_of2.npz")
+    b = np.load(tmp_path / "rank1_of2.npz")
+    # every rank holds the same positions and the same trace ...
+    np.testing.assert_array_equal(a["y"], b["y"])
+    np.testing.assert_array_equal(a["stress"], b["stress"])
+    np.testing.assert_array_equal(a["b"], b["b"])
+    # ... bit-identical to the unsharded run (tile order is rank-independent)
+    np.testing.assert_array_equal(a["y"], r1["y"])
+    np.testing.assert_array_equal(a["stress"], r1["stress"])
+    # ... and equal to the oracle's force-directed trajectory (float64)
+    _, orc = _problem()
+    for _ in range(iters):
+        orc.step()
+    np.testing.assert_allclose(a["y"], orc.Y, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(a["stress"], orc.trace_stress, rtol=1e-12)
+    np.testing.assert_allclose(a["b"], orc.trace_b, rtol=1e-14)
+
+
+def test_shard_plan_covers_all_vertices():
+    be = NumpyShardBackend(700, _problem()[1].full)
+    spans = [ShardedEmbedding(700, 2, r, 4, backend=NumpyShardBackend(700, be.conn)) for r in range(4)]
+    covered = sorted((s.v0, s.v1) for s in spans)
+    assert covered[0][0] == 0 and covered[-1][1] >= 700
+    assert all(covered[i][1] == covered[i + 1][0] for i in range(3))
