@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <map>
 #include <string>
 #include <tuple>
@@ -108,6 +109,15 @@ struct ivhd_ctx {
 
 namespace {
 
+template <class T>
+inline cudaError_t dalloc(ivhd_ctx* ctx, T** p, size_t bytes) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, ctx->stream);
+}
+template <class T>
+inline void dfree(ivhd_ctx* ctx, T* p) {
+  if (p) cudaFreeAsync(reinterpret_cast<void*>(const_cast<typename std::remove_const<T>::type*>(p)), ctx->stream);
+}
+
 int fail(ivhd_ctx* ctx, int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -132,6 +142,13 @@ int fail(ivhd_ctx* ctx, int code, const char* fmt, ...) {
     int r_ = (expr);            \
     if (r_ != IVHD_OK) return r_; \
   } while (0)
+
+// Stream-ordered allocation on the context stream: no device-wide syncs,
+// and the default pool keeps freed memory for the next context (see create).
+template <class T>
+inline cudaError_t dalloc(ivhd_ctx* ctx, T** p, size_t bytes);
+template <class T>
+inline void dfree(ivhd_ctx* ctx, T* p);
 
 inline int ys_of(int dim, int opt) { return (opt == OPT_NEST) ? (dim == 2 ? 4 : 8) : (dim == 2 ? 2 : 4); }
 
@@ -408,19 +425,19 @@ inline int grid_for(int64_t n, int sms) {
 
 int ensure_slot(ivhd_ctx* ctx, CsrSlot& s, int64_t n, bool weighted) {
   // +16 entries: TMA copies round sizes up to 16 bytes
-  if (s.row_ptr == nullptr) CU(ctx, cudaMalloc(&s.row_ptr, sizeof(uint32_t) * (ctx->m + 1 + 16)));
-  if (s.tile_g == nullptr) CU(ctx, cudaMalloc(&s.tile_g, (size_t)ctx->n_tiles_cap));
+  if (s.row_ptr == nullptr) CU(ctx, dalloc(ctx, &s.row_ptr, sizeof(uint32_t) * (ctx->m + 1 + 16)));
+  if (s.tile_g == nullptr) CU(ctx, dalloc(ctx, &s.tile_g, (size_t)ctx->n_tiles_cap));
   if (n > s.cap) {
-    if (s.col) CU(ctx, cudaFree(s.col));
-    if (s.ew) CU(ctx, cudaFree(s.ew));
+    if (s.col) dfree(ctx, s.col);
+    if (s.ew) dfree(ctx, s.ew);
     s.col = nullptr;
     s.ew = nullptr;
-    CU(ctx, cudaMalloc(&s.col, sizeof(uint32_t) * (std::max<int64_t>(n, 1) + 16)));
+    CU(ctx, dalloc(ctx, &s.col, sizeof(uint32_t) * (std::max<int64_t>(n, 1) + 16)));
     s.cap = n;
   }
-  if (weighted && s.ew == nullptr) CU(ctx, cudaMalloc(&s.ew, sizeof(float2) * std::max<int64_t>(s.cap, 1)));
+  if (weighted && s.ew == nullptr) CU(ctx, dalloc(ctx, &s.ew, sizeof(float2) * std::max<int64_t>(s.cap, 1)));
   if (!weighted && s.ew != nullptr) {
-    CU(ctx, cudaFree(s.ew));
+    dfree(ctx, s.ew);
     s.ew = nullptr;
   }
   return IVHD_OK;
@@ -453,15 +470,15 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
   TRY(pull_ctrl(ctx));
   cudaError_t e = cudaSuccess;
   do {
-    if ((e = cudaMalloc(&deg, 4 * m)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&deg2, 4 * m)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&ids, 4 * m)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&perm, 4 * m)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &deg, 4 * m)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &deg2, 4 * m)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &ids, 4 * m)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &perm, 4 * m)) != cudaSuccess) break;
     k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, deg);
     k_iota<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ids, m);
     if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
         cudaSuccess) break;
-    if ((e = cudaMalloc(&tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
     if ((e = cub::DeviceRadixSort::SortPairsDescending(tmp, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
         cudaSuccess) break;
     if (ctx->pos_set) {
@@ -482,7 +499,7 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
     k_inverse<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ctx->perm, m, ctx->inv);
     e = cudaStreamSynchronize(st);
   } while (0);
-  cudaFree(deg); cudaFree(deg2); cudaFree(ids); cudaFree(perm); cudaFree(tmp);
+  dfree(ctx, deg); dfree(ctx, deg2); dfree(ctx, ids); dfree(ctx, perm); dfree(ctx, tmp);
   if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "vertex relabelling: %s", cudaGetErrorString(e));
   ctx->perm_fixed = true;
   return IVHD_OK;
@@ -516,19 +533,19 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
   int hbad = 0, rc = IVHD_OK;
   const int64_t nc = std::max<int64_t>(n, 1);
   do {
-    if ((e = cudaMalloc(&keys, 4 * nc)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&keys2, 4 * nc)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&vals, 4 * nc)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&vals2, 4 * nc)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&rp_old, 4 * (m + 1))) != cudaSuccess) break;
-    if ((e = cudaMalloc(&deg, 4 * (m + 1))) != cudaSuccess) break;
-    if ((e = cudaMalloc(&bad, sizeof(int))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &keys, 4 * nc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &keys2, 4 * nc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &vals, 4 * nc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &vals2, 4 * nc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &rp_old, 4 * (m + 1))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &deg, 4 * (m + 1))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &bad, sizeof(int))) != cudaSuccess) break;
     if ((e = cudaMemsetAsync(bad, 0, sizeof(int), st)) != cudaSuccess) break;
     if (n > 0) {
       k_half_edges<<<grid_for(n, ctx->sm_count), 256, 0, st>>>(src, dst, L, m, keys, vals, bad);
       if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, end_bit,
                                                st)) != cudaSuccess) break;
-      if ((e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16))) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &tmp, std::max<size_t>(tmp_bytes, 16))) != cudaSuccess) break;
       // LSD radix sort is stable: rows list out-halves (connection order) then in-halves.
       if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, end_bit,
                                                st)) != cudaSuccess) break;
@@ -548,10 +565,10 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
     size_t sb = 0;
     if ((e = cub::DeviceScan::ExclusiveSum(nullptr, sb, deg, S.row_ptr, (int)(m + 1), st)) != cudaSuccess) break;
     void* stmp = nullptr;
-    if ((e = cudaMalloc(&stmp, std::max<size_t>(sb, 16))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &stmp, std::max<size_t>(sb, 16))) != cudaSuccess) break;
     e = cub::DeviceScan::ExclusiveSum(stmp, sb, deg, S.row_ptr, (int)(m + 1), st);
     cudaStreamSynchronize(st);
-    cudaFree(stmp);
+    dfree(ctx, stmp);
     if (e != cudaSuccess) break;
     if (n > 0)
       k_fill_perm_cols<<<grid_for(m * 32, ctx->sm_count), 256, 0, st>>>(
@@ -571,15 +588,15 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
       for (int p = 0; p < g[t]; ++p) units.push_back(t << 8 | p << 3 | lg);
     }
     S.n_units = (int)units.size();
-    if (S.units) cudaFree(S.units);
+    if (S.units) dfree(ctx, S.units);
     S.units = nullptr;
-    if ((e = cudaMalloc(&S.units, sizeof(int) * units.size())) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &S.units, sizeof(int) * units.size())) != cudaSuccess) break;
     if ((e = cudaMemcpyAsync(S.units, units.data(), sizeof(int) * units.size(), cudaMemcpyHostToDevice, st)) !=
         cudaSuccess) break;
     e = cudaStreamSynchronize(st);
   } while (0);
-  cudaFree(keys); cudaFree(keys2); cudaFree(vals); cudaFree(vals2); cudaFree(rp_old); cudaFree(deg);
-  cudaFree(bad); cudaFree(tmp);
+  dfree(ctx, keys); dfree(ctx, keys2); dfree(ctx, vals); dfree(ctx, vals2); dfree(ctx, rp_old); dfree(ctx, deg);
+  dfree(ctx, bad); dfree(ctx, tmp);
   if (rc != IVHD_OK) return rc;
   if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "CSR build: %s", cudaGetErrorString(e));
   if (hbad) return fail(ctx, IVHD_ERR_INVALID_ARG, "connection endpoint outside [0, %lld)", (long long)m);
@@ -700,6 +717,13 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   };
   if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, IVHD_ERR_CUDA, "cudaSetDevice failed"));
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  {  // keep freed stream-ordered memory pooled across contexts (repeated embeds)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   if (stream) {
     ctx->stream = reinterpret_cast<cudaStream_t>(stream);
   } else {
@@ -718,9 +742,9 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   int rc = IVHD_OK;
   auto alloc = [&](void** p, size_t bytes) {
     if (rc != IVHD_OK) return;
-    cudaError_t ee = cudaMalloc(p, bytes);
-    if (ee != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(ee));
-    else cudaMemset(*p, 0, bytes);
+    cudaError_t ee = cudaMallocAsync(p, bytes, ctx->stream);
+    if (ee != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(ee));
+    else cudaMemsetAsync(*p, 0, bytes, ctx->stream);
   };
   alloc((void**)&ctx->ybuf[0], sizeof(float) * 8 * vc);
   alloc((void**)&ctx->ybuf[1], sizeof(float) * 8 * vc);
@@ -767,13 +791,13 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   drop_graphs(ctx);
   for (auto& s : ctx->slots) {
-    cudaFree(s.row_ptr); cudaFree(s.col); cudaFree(s.ew); cudaFree(s.tile_g); cudaFree(s.units);
+    dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.units);
   }
-  cudaFree(ctx->perm); cudaFree(ctx->inv);
-  cudaFree(ctx->ybuf[0]); cudaFree(ctx->ybuf[1]); cudaFree(ctx->state); cudaFree(ctx->partial);
-  cudaFree(ctx->trace); cudaFree(ctx->ctrl); cudaFree(ctx->opctrl); cudaFree(ctx->red_out);
-  cudaFree(ctx->stage); cudaFree(ctx->op_y); cudaFree(ctx->op_force);
-  cudaFree(ctx->snap_y); cudaFree(ctx->snap_state);
+  dfree(ctx, ctx->perm); dfree(ctx, ctx->inv);
+  dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial);
+  dfree(ctx, ctx->trace); dfree(ctx, ctx->ctrl); dfree(ctx, ctx->opctrl); dfree(ctx, ctx->red_out);
+  dfree(ctx, ctx->stage); dfree(ctx, ctx->op_y); dfree(ctx, ctx->op_force);
+  dfree(ctx, ctx->snap_y); dfree(ctx, ctx->snap_state);
   if (ctx->ctrl_h) cudaFreeHost(ctx->ctrl_h);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -792,17 +816,17 @@ int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_st
   cudaError_t e = cudaSuccess;
   do {
     if (ncols > 0) {
-      if ((e = cudaMalloc(&d_nn, sizeof(int32_t) * m * nn_stride)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &d_nn, sizeof(int32_t) * m * nn_stride)) != cudaSuccess) break;
       if ((e = cudaMemcpyAsync(d_nn, nn_ids, sizeof(int32_t) * m * nn_stride, cudaMemcpyHostToDevice,
                                ctx->stream)) != cudaSuccess) break;
     }
     if (rn > 0) {
-      if ((e = cudaMalloc(&d_rn, sizeof(int32_t) * m * rn)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &d_rn, sizeof(int32_t) * m * rn)) != cudaSuccess) break;
       if ((e = cudaMemcpyAsync(d_rn, rn_ids, sizeof(int32_t) * m * rn, cudaMemcpyHostToDevice,
                                ctx->stream)) != cudaSuccess) break;
     }
-    if ((e = cudaMalloc(&d_src, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
-    if ((e = cudaMalloc(&d_dst, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_src, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_dst, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
     if (L > 0)
       k_binary_edges<<<grid_for(L, ctx->sm_count), 256, 0, ctx->stream>>>(d_nn, nn_stride, ncols, d_rn, rn,
                                                                           m, d_src, d_dst);
@@ -811,7 +835,7 @@ int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_st
   int rc = IVHD_OK;
   if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "set_graph: %s", cudaGetErrorString(e));
   else rc = build_csr(ctx, slot, d_src, d_dst, nullptr, n_nn, nullptr, nullptr, L);
-  cudaFree(d_nn); cudaFree(d_rn); cudaFree(d_src); cudaFree(d_dst);
+  dfree(ctx, d_nn); dfree(ctx, d_rn); dfree(ctx, d_src); dfree(ctx, d_dst);
   return rc;
 }
 
@@ -830,27 +854,27 @@ int ivhd_set_connections(ivhd_ctx* ctx, int slot, const int32_t* edges, const ui
   cudaError_t e = cudaSuccess;
   cudaStream_t st = ctx->stream;
   do {
-    if ((e = cudaMalloc(&d_e, sizeof(int32_t) * 2 * Lc)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&d_src, sizeof(int32_t) * Lc)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&d_dst, sizeof(int32_t) * Lc)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&d_r, Lc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_e, sizeof(int32_t) * 2 * Lc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_src, sizeof(int32_t) * Lc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_dst, sizeof(int32_t) * Lc)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_r, Lc)) != cudaSuccess) break;
     if (L > 0) {
       if ((e = cudaMemcpyAsync(d_e, edges, sizeof(int32_t) * 2 * L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
       if ((e = cudaMemcpyAsync(d_r, is_random, L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
       k_split_edges<<<grid_for(L, ctx->sm_count), 256, 0, st>>>(d_e, L, d_src, d_dst);
     }
     if (targets || scale) {
-      if ((e = cudaMalloc(&d_tmp, sizeof(double) * Lc)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &d_tmp, sizeof(double) * Lc)) != cudaSuccess) break;
     }
     if (targets) {
-      if ((e = cudaMalloc(&d_t, sizeof(float) * Lc)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &d_t, sizeof(float) * Lc)) != cudaSuccess) break;
       if (L > 0) {
         if ((e = cudaMemcpyAsync(d_tmp, targets, sizeof(double) * L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
         k_d2f<<<grid_for(L, ctx->sm_count), 256, 0, st>>>(d_tmp, d_t, L);
       }
     }
     if (scale) {
-      if ((e = cudaMalloc(&d_s, sizeof(float) * Lc)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &d_s, sizeof(float) * Lc)) != cudaSuccess) break;
       if (L > 0) {
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;  // d_tmp reuse
         if ((e = cudaMemcpyAsync(d_tmp, scale, sizeof(double) * L, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
@@ -862,7 +886,7 @@ int ivhd_set_connections(ivhd_ctx* ctx, int slot, const int32_t* edges, const ui
   int rc = IVHD_OK;
   if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "set_connections: %s", cudaGetErrorString(e));
   else rc = build_csr(ctx, slot, d_src, d_dst, d_r, 0, d_t, d_s, L);
-  cudaFree(d_e); cudaFree(d_src); cudaFree(d_dst); cudaFree(d_r); cudaFree(d_tmp); cudaFree(d_t); cudaFree(d_s);
+  dfree(ctx, d_e); dfree(ctx, d_src); dfree(ctx, d_dst); dfree(ctx, d_r); dfree(ctx, d_tmp); dfree(ctx, d_t); dfree(ctx, d_s);
   return rc;
 }
 
@@ -980,9 +1004,9 @@ int ivhd_get_step_size(ivhd_ctx* ctx, double* step_out) {
 static int ensure_trace(ivhd_ctx* ctx, int64_t n) {
   if (n <= ctx->trace_cap) return IVHD_OK;
   const int64_t cap = std::max<int64_t>(n, 4096);
-  if (ctx->trace) CU(ctx, cudaFree(ctx->trace));
+  if (ctx->trace) dfree(ctx, ctx->trace);
   ctx->trace = nullptr;
-  CU(ctx, cudaMalloc(&ctx->trace, sizeof(double2) * cap));
+  CU(ctx, dalloc(ctx, &ctx->trace, sizeof(double2) * cap));
   ctx->trace_cap = cap;
   drop_graphs(ctx);
   return IVHD_OK;
@@ -1058,8 +1082,8 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   TRY(check_ready(ctx, slot));
   if (norm != IVHD_NORM_L2 && norm != IVHD_NORM_L1) return fail(ctx, IVHD_ERR_INVALID_ARG, "unknown norm %d", norm);
   if (!y) return fail(ctx, IVHD_ERR_INVALID_ARG, "null positions");
-  if (!ctx->op_y) CU(ctx, cudaMalloc(&ctx->op_y, sizeof(float) * 4 * ctx->v_cap));
-  if (!ctx->op_force) CU(ctx, cudaMalloc(&ctx->op_force, sizeof(double) * 3 * ctx->v_cap));
+  if (!ctx->op_y) CU(ctx, dalloc(ctx, &ctx->op_y, sizeof(float) * 4 * ctx->v_cap));
+  if (!ctx->op_force) CU(ctx, dalloc(ctx, &ctx->op_force, sizeof(double) * 3 * ctx->v_cap));
   const int ys = ctx->dim == 2 ? 2 : 4;
   TRY(upload_stage(ctx, y, ctx->m * ctx->dim));
   k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->stage, ctx->m, ctx->dim, ys,
@@ -1118,8 +1142,8 @@ int ivhd_snapshot(ivhd_ctx* ctx) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
   CU(ctx, cudaSetDevice(ctx->device));
   const size_t bytes = sizeof(float) * 8 * ctx->v_cap;
-  if (!ctx->snap_y) CU(ctx, cudaMalloc(&ctx->snap_y, bytes));
-  if (!ctx->snap_state) CU(ctx, cudaMalloc(&ctx->snap_state, bytes));
+  if (!ctx->snap_y) CU(ctx, dalloc(ctx, &ctx->snap_y, bytes));
+  if (!ctx->snap_state) CU(ctx, dalloc(ctx, &ctx->snap_state, bytes));
   TRY(pull_ctrl(ctx));
   const size_t used = sizeof(float) * 8 * ctx->m;
   CU(ctx, cudaMemcpyAsync(ctx->snap_y, ctx->ybuf[ctx->ctrl_h->cur], used, cudaMemcpyDeviceToDevice, ctx->stream));
