@@ -28,7 +28,8 @@ struct CsrSlot {
   uint32_t* col = nullptr;      // [n]
   float2* ew = nullptr;         // [n] or nullptr (binary)
   uint8_t* tile_g = nullptr;    // [n_tiles_cap] lanes per vertex of each tile
-  int* units = nullptr;         // work units (tile << 8 | pass << 3 | log2 G), tile-major order
+  uint8_t* tile_dm = nullptr;   // [n_tiles_cap] max row length of each tile (clamped to 255)
+  int* units = nullptr;         // work units (tile << 12 | pass << 7 | min(maxdeg,15) << 3 | log2 G)
   int n_units = 0;
   std::vector<int> unit_base;   // host: first unit of each tile (n_tiles_cap + 1)
   int64_t n = 0;                // entries (2 * connections)
@@ -196,7 +197,7 @@ int occupancy(ivhd_ctx* ctx, KernelInfo k) {
   if (it != ctx->occ.end()) return it->second;
   cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   int n = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, kBlock, k.smem) != cudaSuccess || n < 1) n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, kThreads, k.smem) != cudaSuccess || n < 1) n = 1;
   ctx->occ[k.fn] = n;
   return n;
 }
@@ -335,6 +336,11 @@ __global__ void k_degrees(const uint32_t* __restrict__ row_ptr, int64_t m, uint3
     deg[i] = row_ptr[i + 1] - row_ptr[i];
 }
 
+__global__ void k_hybrid_key(uint32_t* __restrict__ deg, int64_t m) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = deg[i] > (uint32_t)kUnroll ? deg[i] : 0u;
+}
+
 __global__ void k_inverse(const int32_t* __restrict__ perm, int64_t m, int32_t* __restrict__ inv) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -389,7 +395,7 @@ __global__ void k_fill_perm_cols(const uint32_t* __restrict__ rp_old, const uint
 // Lanes per vertex of each tile: smallest power of two G with
 // G * kUnroll >= the tile's max degree (capped at a warp); pad tiles get 1.
 __global__ void k_tile_g(const uint32_t* __restrict__ rp, int64_t m, int n_tiles_cap,
-                         uint8_t* __restrict__ tile_g) {
+                         uint8_t* __restrict__ tile_g, uint8_t* __restrict__ tile_dm) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_tiles_cap; t += nwarps) {
@@ -399,7 +405,10 @@ __global__ void k_tile_g(const uint32_t* __restrict__ rp, int64_t m, int n_tiles
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     int G = 1;
     while (G < 32 && (uint32_t)(G * kUnroll) < mx) G <<= 1;
-    if (lane == 0) tile_g[t] = (uint8_t)G;
+    if (lane == 0) {
+      tile_g[t] = (uint8_t)G;
+      tile_dm[t] = (uint8_t)min(mx, 255u);
+    }
   }
 }
 
@@ -427,6 +436,7 @@ int ensure_slot(ivhd_ctx* ctx, CsrSlot& s, int64_t n, bool weighted) {
   // +16 entries: TMA copies round sizes up to 16 bytes
   if (s.row_ptr == nullptr) CU(ctx, dalloc(ctx, &s.row_ptr, sizeof(uint32_t) * (ctx->m + 1 + 16)));
   if (s.tile_g == nullptr) CU(ctx, dalloc(ctx, &s.tile_g, (size_t)ctx->n_tiles_cap));
+  if (s.tile_dm == nullptr) CU(ctx, dalloc(ctx, &s.tile_dm, (size_t)ctx->n_tiles_cap));
   if (n > s.cap) {
     if (s.col) dfree(ctx, s.col);
     if (s.ew) dfree(ctx, s.ew);
@@ -476,6 +486,8 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
     if ((e = dalloc(ctx, &perm, 4 * m)) != cudaSuccess) break;
     k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, deg);
     k_iota<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ids, m);
+    if (order && strcmp(order, "hybrid") == 0)  // experiment: light rows keep the caller's order
+      k_hybrid_key<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(deg, m);
     if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
         cudaSuccess) break;
     if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
@@ -574,18 +586,20 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
       k_fill_perm_cols<<<grid_for(m * 32, ctx->sm_count), 256, 0, st>>>(
           rp_old, S.row_ptr, vals2, m, L, src, dst, rand, n_nn, tgt, scl, ctx->perm, ctx->inv, S.col, S.ew);
     k_tile_g<<<grid_for((int64_t)ctx->n_tiles_cap * 32, ctx->sm_count), 256, 0, st>>>(S.row_ptr, m,
-                                                                                     ctx->n_tiles_cap, S.tile_g);
+                                                                                     ctx->n_tiles_cap, S.tile_g, S.tile_dm);
     if ((e = cudaGetLastError()) != cudaSuccess) break;
     // work units: one per (tile, pass), in tile order
-    std::vector<uint8_t> g(ctx->n_tiles_cap);
+    std::vector<uint8_t> g(ctx->n_tiles_cap), dm(ctx->n_tiles_cap);
     if ((e = cudaMemcpyAsync(g.data(), S.tile_g, g.size(), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(dm.data(), S.tile_dm, dm.size(), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
     S.unit_base.assign(ctx->n_tiles_cap + 1, 0);
     std::vector<int> units;
     for (int t = 0; t < ctx->n_tiles_cap; ++t) {
       S.unit_base[t + 1] = S.unit_base[t] + g[t];
       const int lg = __builtin_ctz((unsigned)g[t]);
-      for (int p = 0; p < g[t]; ++p) units.push_back(t << 8 | p << 3 | lg);
+      const int d15 = std::min<int>(dm[t], 15);
+      for (int p = 0; p < g[t]; ++p) units.push_back(t << 12 | p << 7 | d15 << 3 | lg);
     }
     S.n_units = (int)units.size();
     if (S.units) dfree(ctx, S.units);
@@ -644,7 +658,7 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
 
 int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
   const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, k) * ctx->sm_count));
-  k.fn<<<grid, kBlock, k.smem, ctx->stream>>>(A);
+  k.fn<<<grid, kThreads, k.smem, ctx->stream>>>(A);
   CU(ctx, cudaGetLastError());
   return IVHD_OK;
 }
@@ -683,6 +697,58 @@ int ss_now(ivhd_ctx* ctx) {
   return nv == 0 ? 0 : (ctx->dim == 2 ? 2 * nv : 4 * nv);
 }
 
+
+// ---------------------------------------------------------------- probes
+// Diagnostic kernels over the live CSR (one thread per row, thread-per-vertex):
+// mode 0 streams the column ids, 1 also gathers neighbour positions, 2 loads
+// the row's own position instead (coalesced).  Output one float per row.
+__global__ void k_probe(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                        const float2* __restrict__ Y, int64_t m, int mode, float* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < m; v += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = rp[v], e = rp[v + 1];
+    float acc = 0.f;
+    for (uint32_t k = b; k < e; k += 4) {
+      uint32_t c4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c4[q] = k + q < e ? __ldg(col + k + q) : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (k + q >= e) continue;
+        if (mode == 0) acc += (float)(c4[q] & 0xff);
+        else if (mode == 1) { const float2 p = __ldg(Y + (c4[q] & kIdMask)); acc += p.x + p.y; }
+        else { const float2 p = __ldg(Y + v + (c4[q] & 1)); acc += p.x + p.y; }
+      }
+    }
+    out[v] = acc;
+  }
+}
+
+}  // namespace
+
+extern "C" int ivhd_probe(ivhd_ctx* ctx, int slot, int mode, int iters, int blocks_per_sm, double* us_out) {
+  TRY(check_ready(ctx, slot));
+  const CsrSlot& S = ctx->slots[slot];
+  float* out = reinterpret_cast<float*>(ctx->stage);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = ctx->sm_count * blocks_per_sm;
+  k_probe<<<grid, 256, 0, ctx->stream>>>(S.row_ptr, S.col, reinterpret_cast<const float2*>(ctx->ybuf[0]), ctx->m, mode, out);
+  cudaEventRecord(a, ctx->stream);
+  for (int i = 0; i < iters; ++i)
+    k_probe<<<grid, 256, 0, ctx->stream>>>(S.row_ptr, S.col, reinterpret_cast<const float2*>(ctx->ybuf[0]), ctx->m, mode, out);
+  cudaEventRecord(b, ctx->stream);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *us_out = 1e3 * ms / iters;
+  CU(ctx, cudaGetLastError());
+  return IVHD_OK;
+}
+
+namespace {
 }  // namespace
 
 // ======================================================================= C ABI
@@ -791,7 +857,7 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   drop_graphs(ctx);
   for (auto& s : ctx->slots) {
-    dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.units);
+    dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.tile_dm); dfree(ctx, s.units);
   }
   dfree(ctx, ctx->perm); dfree(ctx, ctx->inv);
   dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial);
@@ -1165,6 +1231,12 @@ int ivhd_restore(ivhd_ctx* ctx) {
   TRY(push_ctrl(ctx));
   return IVHD_OK;  // asynchronous: ordered before the next launch on the stream
 }
+
+#ifdef IVHD_TIMELINE
+int ivhd_timeline_dump(long long* out) {
+  return cudaMemcpyFromSymbol(out, ivhd::g_tl, sizeof(long long) * 8 * 64 * 6) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 int ivhd_synchronize(ivhd_ctx* ctx) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");

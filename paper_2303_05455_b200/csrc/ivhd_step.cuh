@@ -32,6 +32,11 @@
 
 namespace ivhd {
 
+#ifdef IVHD_TIMELINE
+// per-unit phase timestamps of a few blocks: [block][unit][phase]
+__device__ long long g_tl[8][64][6];
+#endif
+
 
 #ifndef IVHD_BLOCK
 #define IVHD_BLOCK 256
@@ -44,6 +49,8 @@ constexpr int kBlock = IVHD_BLOCK;  // threads per block = vertices per tile
 // scheduling) and the aligned barrier then let early lanes through (observed
 // on B200 / CUDA 12.9).  The non-aligned barrier.sync counts threads.
 __device__ __forceinline__ void block_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+// Barrier over the first kBlock threads only (reductions run without the producer warp).
+__device__ __forceinline__ void group_sync() { asm volatile("barrier.sync 1, %0;" ::"n"(IVHD_BLOCK) : "memory"); }
 
 constexpr uint32_t kRandBit = 0x80000000u;
 constexpr uint32_t kIdMask = 0x7fffffffu;
@@ -86,7 +93,7 @@ struct StepArgs {
   Ctrl* ctrl;
   double* force_out;      // OPT_NONE only: (M, DIM) float64
   const uint8_t* tile_g;  // lanes per vertex of every (global) tile
-  const int* units;       // work unit -> tile << 8 | pass << 3 | log2(G), global unit order
+  const int* units;       // work unit -> tile << 12 | pass << 7 | min(maxdeg,15) << 3 | log2 G
   long long v_begin, v_end;
   int tile_v;
   int n_tiles;            // work units this launch processes
@@ -281,14 +288,14 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double4* sm /*[kBlock/3
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v.x = warp_dsum(v.x); v.y = warp_dsum(v.y); v.z = warp_dsum(v.z); v.w = warp_dsum(v.w);
   if (lane == 0) sm[warp] = v;
-  block_sync();
+  group_sync();
   double4 r = make_double4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     for (int w = 0; w < kBlock / 32; ++w) {
       r.x += sm[w].x; r.y += sm[w].y; r.z += sm[w].z; r.w += sm[w].w;
     }
   }
-  block_sync();
+  group_sync();
   return r;  // valid in thread 0
 }
 
@@ -499,6 +506,56 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 constexpr int kColCap = 2048;      // staged column entries per unit (larger units read global)
 constexpr int kUnitCache = 1024;   // unit words cached per block
 
+// Fast path for the dominant case (2-D, binary, L2, positions without look-ahead,
+// one lane per row): the unit's max row length D <= 8 is a template constant,
+// all D column reads and gathers are issued first, then ~26 instructions per
+// entry.  Slots past the row end are self pairs (zero contribution).
+template <int D>
+__device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int deg, const float* __restrict__ Yin,
+                                         uint32_t v, float y0, float y1, float c, long long gstep, float (&f)[2],
+                                         float& e) {
+  uint32_t cw[D];
+  float2 p[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) cw[q] = q < deg ? cb[q] : v;
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    p[q] = make_float2(y0, y1);
+    if (q < deg) p[q] = __ldg(reinterpret_cast<const float2*>(Yin) + (cw[q] & kIdMask));
+  }
+  float fx = f[0], fy = f[1], ee = e;
+  unsigned dmask = 0;
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    const float dx = y0 - p[q].x, dy = y1 - p[q].y;
+    const float d2 = fmaf(dx, dx, dy * dy);
+    const float rs = rsqrt_ftz(d2);
+    const bool rn = (int)cw[q] < 0, z = d2 == 0.f;
+    const float phi_rn = z ? 0.f : c * (rs - 1.f);   // c (1 - d) / d
+    const float de = z ? 0.f : d2 * rs;
+    const float r = 1.f - de;
+    const float phi = rn ? phi_rn : -1.f;
+    fx = fmaf(phi, dx, fx);
+    fy = fmaf(phi, dy, fy);
+    ee += rn ? c * r * r : d2;
+    dmask |= (unsigned)(rn && z) << q;
+  }
+  if (dmask) {  // degenerate random pairs (forces.py:167-174)
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      if ((dmask >> q) & 1u) {
+        float u[2];
+        degenerate_dir<2>(v, cw[q] & kIdMask, gstep, u);
+        fx = fmaf(c, u[0], fx);
+        fy = fmaf(c, u[1], fy);
+      }
+    }
+  }
+  f[0] = fx;
+  f[1] = fy;
+  e = ee;
+}
+
 // Shared-memory layout of one ring stage for (DIM, OPT).
 template <int DIM, int OPT>
 struct StageLayout {
@@ -519,7 +576,7 @@ constexpr int step_smem_bytes() {
 // Per-stage metadata written by the producer before it arrives on the
 // stage's barriers (release) and read by consumers after the wait (acquire).
 struct StageMeta {
-  int packed;       // unit word: tile << 8 | pass << 3 | log2 G
+  int packed;       // unit word: tile << 12 | pass << 7 | min(maxdeg,15) << 3 | log2 G
   int col_off;      // entries skipped at the front of the staged columns (alignment)
   int staged;       // 1 if the unit's columns are in shared memory
   int pad;
@@ -534,17 +591,21 @@ struct StageMeta {
 // unit k from shared memory; only the neighbour-position gathers go to
 // global memory (L2).  Tiles hold 256 vertices relabelled by degree; a unit
 // is one pass of a tile: 256/G vertices with G lanes each.
+constexpr int kThreads = kBlock + 32;  // 8 consumer warps + 1 TMA producer warp
+constexpr int kConsumerWarps = kBlock / 32;
+
 template <int DIM, int OPT, bool WEIGHTED, int NORM>
-__global__ void __launch_bounds__(kBlock, IVHD_MINBLOCKS) step_kernel(StepArgs A) {
+__global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs A) {
   using L = Layout<DIM, OPT>;
   using SL = StageLayout<DIM, OPT>;
   constexpr bool NEST = (OPT == OPT_NEST);
   constexpr int SSX = L::SS > 0 ? L::SS : 1;
   constexpr int YS = L::YS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar_a[kStages], bar_b[kStages];
+  __shared__ __align__(8) uint64_t bar_a[kStages], bar_b[kStages], bar_e[kStages];
   __shared__ StageMeta meta[kStages];
-  __shared__ double4 sm_unit[2][kBlock / 32];
+  __shared__ float4 sm_wp[kStages][kConsumerWarps];
+  __shared__ int sm_cnt[kStages];
   __shared__ double4 sm_red[kBlock / 32];
   __shared__ int sm_units[kUnitCache];  // this block's unit words (static schedule)
 
@@ -556,7 +617,7 @@ __global__ void __launch_bounds__(kBlock, IVHD_MINBLOCKS) step_kernel(StepArgs A
   const long long gstep = ctrl->gstep;
   const float* __restrict__ Yin = ycur ? A.ybuf1 : A.ybuf0;
   float* __restrict__ Yout = ycur ? A.ybuf0 : A.ybuf1;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   float bc1 = 1.f, bc2 = 1.f;  // Adam bias corrections (optim.py:203-204)
   if constexpr (OPT == OPT_ADAM) {
@@ -569,216 +630,249 @@ __global__ void __launch_bounds__(kBlock, IVHD_MINBLOCKS) step_kernel(StepArgs A
   const int grid = gridDim.x;
   const int my_units = blockIdx.x < n_units ? (n_units - 1 - blockIdx.x) / grid + 1 : 0;
 
-  for (int k = tid; k < min(my_units, kUnitCache); k += kBlock)
+  for (int k = tid; k < min(my_units, kUnitCache); k += kThreads)
     sm_units[k] = __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bar_a[s], 1);
       mbar_init(&bar_b[s], 1);
+      mbar_init(&bar_e[s], kConsumerWarps);
+      sm_cnt[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   block_sync();
 
-  // producer helpers (thread 0 only)
   auto unit_range = [&](int packed, long long& va, int& nv) {
-    const int tile = packed >> 8, pass = (packed >> 3) & 31, lgG = packed & 7;
+    const int tile = packed >> 12, pass = (packed >> 7) & 31, lgG = packed & 7;
     const int groups = kBlock >> lgG;
     va = (long long)tile * kBlock + (long long)pass * groups;
     nv = (int)max(0LL, min((long long)groups, A.v_end - va));
   };
-  auto issue_front = [&](int k) {  // row pointers + positions + state of local unit k
-    const int s = k % kStages;
-    unsigned char* st = smem_raw + s * SL::BYTES;
-    const int packed = k < kUnitCache ? sm_units[k] : __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
-    long long va;
-    int nv;
-    unit_range(packed, va, nv);
-    meta[s].packed = packed;
-    const uint32_t rp_bytes = (uint32_t)((nv + 1) * 4 + 15) / 16 * 16;
-    const uint32_t y_bytes = (uint32_t)nv * YS * 4;  // nv is a multiple of 8 except at the end
-    const uint32_t y_copy = (y_bytes + 15) / 16 * 16;
-    uint32_t s_copy = 0;
-    if constexpr (L::SS > 0) s_copy = ((uint32_t)nv * L::SS * 4 + 15) / 16 * 16;
-    mbar_expect_tx(&bar_a[s], rp_bytes + y_copy + s_copy);
-    bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_a[s]);
-    bulk_g2s(st + SL::Y_OFF, Yin + va * YS, y_copy, &bar_a[s]);
-    if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, A.state + va * L::SS, s_copy, &bar_a[s]);
-  };
-  auto issue_cols = [&](int k) {  // column segment of local unit k (its row pointers have landed)
-    const int s = k % kStages;
-    unsigned char* st = smem_raw + s * SL::BYTES;
-    mbar_wait(&bar_a[s], (uint32_t)(k / kStages) & 1);
-    long long va;
-    int nv;
-    unit_range(meta[s].packed, va, nv);
-    const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
-    const uint32_t e0 = rp[0], e1 = rp[nv];
-    const uint32_t a0 = e0 & ~3u, a1 = (e1 + 3u) & ~3u;  // 16-byte aligned cover
-    if (nv > 0 && e1 > e0 && a1 - a0 <= (uint32_t)kColCap + 4) {
-      meta[s].col_off = (int)(e0 - a0);
-      meta[s].staged = 1;
-      mbar_expect_tx(&bar_b[s], (a1 - a0) * 4);
-      bulk_g2s(st + SL::COL_OFF, A.col + a0, (a1 - a0) * 4, &bar_b[s]);
-    } else {
-      meta[s].col_off = 0;
-      meta[s].staged = 0;
-      mbar_arrive(&bar_b[s]);
-    }
-  };
 
-  if (tid == 0) {
-    if (my_units > 0) issue_front(0);
-    if (my_units > 1) issue_front(1);
-    if (my_units > 0) issue_cols(0);
-  }
-
-  int buf = 0;
-  for (int k = 0; k < my_units; ++k) {
-    const int u = blockIdx.x + k * grid;
-    const int s = k % kStages;
-    unsigned char* st = smem_raw + s * SL::BYTES;
-    if (tid == 0) {
-      if (k + 2 < my_units) issue_front(k + 2);
-      if (k + 1 < my_units) issue_cols(k + 1);
-    }
-    const uint32_t par = (uint32_t)(k / kStages) & 1;
-    mbar_wait(&bar_a[s], par);
-    mbar_wait(&bar_b[s], par);
-
-    const int packed = meta[s].packed;
-    const int lgG = packed & 7, G = 1 << lgG;
-    const int lg = tid & (G - 1), grp = tid >> lgG;
-    long long va;
-    int nv;
-    {
-      const int tile = packed >> 8, pass = (packed >> 3) & 31;
-      const int groups = kBlock >> lgG;
-      va = (long long)tile * kBlock + (long long)pass * groups;
-      nv = (int)max(0LL, min((long long)groups, A.v_end - va));
-    }
-    const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
-    const uint32_t* colst = reinterpret_cast<const uint32_t*>(st + SL::COL_OFF);
-    const float* ys = reinterpret_cast<const float*>(st + SL::Y_OFF);
-    const float* ss = reinterpret_cast<const float*>(st + SL::S_OFF);
-    const bool staged = meta[s].staged != 0;
-    const uint32_t e0 = rp[0];
-    const int coff = meta[s].col_off;
-
-    double acc_e = 0.0, acc_n = 0.0, acc_o = 0.0, acc_bad = 0.0;
-    const bool active = grp < nv;
-    if (active) {
-      const long long v = va + grp;
-      const uint32_t beg = rp[grp], end = rp[grp + 1];
-      float yi[DIM], li[DIM];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        yi[d] = ys[grp * YS + d];
-        li[d] = NEST ? ys[grp * YS + (DIM == 2 ? 2 : 4) + d] : yi[d];
-      }
-      float f[DIM];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) f[d] = 0.f;
-      float e = 0.f;
-      for (uint32_t k0 = beg + lg; k0 < end; k0 += (uint32_t)G * kUnroll) {
-        uint32_t cw[kUnroll];
-        float2 tw[WEIGHTED ? kUnroll : 1];
-        float gy[kUnroll][DIM], gl[kUnroll][DIM];
-        // A slot past the row end becomes a zero-target pair with the vertex
-        // itself: zero distance, zero force, zero stress — no masking needed.
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          const uint32_t kk = k0 + (uint32_t)(q * G);
-          cw[q] = (uint32_t)v;
-          if (kk < end) cw[q] = staged ? colst[kk - e0 + coff] : __ldg(A.col + kk);
+  if (warp == kConsumerWarps) {
+    // ---------------------------------------------------- TMA producer warp
+    if (lane == 0) {
+      auto issue_front = [&](int k) {  // row pointers + positions + state of local unit k
+        const int s = k % kStages;
+        unsigned char* st = smem_raw + s * SL::BYTES;
+        const int packed = k < kUnitCache ? sm_units[k] : __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
+        long long va;
+        int nv;
+        unit_range(packed, va, nv);
+        meta[s].packed = packed;
+        const uint32_t rp_bytes = (uint32_t)((nv + 1) * 4 + 15) / 16 * 16;
+        const uint32_t y_copy = ((uint32_t)nv * YS * 4 + 15) / 16 * 16;
+        uint32_t s_copy = 0;
+        if constexpr (L::SS > 0) s_copy = ((uint32_t)nv * L::SS * 4 + 15) / 16 * 16;
+        mbar_expect_tx(&bar_a[s], rp_bytes + y_copy + s_copy);
+        bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_a[s]);
+        bulk_g2s(st + SL::Y_OFF, Yin + va * YS, y_copy, &bar_a[s]);
+        if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, A.state + va * L::SS, s_copy, &bar_a[s]);
+      };
+      auto issue_cols = [&](int k) {  // column segment of local unit k (its row pointers have landed)
+        const int s = k % kStages;
+        unsigned char* st = smem_raw + s * SL::BYTES;
+        mbar_wait(&bar_a[s], (uint32_t)(k / kStages) & 1);
+        long long va;
+        int nv;
+        unit_range(meta[s].packed, va, nv);
+        const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
+        const uint32_t e0 = rp[0], e1 = rp[nv];
+        const uint32_t a0 = e0 & ~3u, a1 = (e1 + 3u) & ~3u;  // 16-byte aligned cover
+        if (nv > 0 && e1 > e0 && a1 - a0 <= (uint32_t)kColCap + 4) {
+          meta[s].col_off = (int)(e0 - a0);
+          meta[s].staged = 1;
+          mbar_expect_tx(&bar_b[s], (a1 - a0) * 4);
+          bulk_g2s(st + SL::COL_OFF, A.col + a0, (a1 - a0) * 4, &bar_b[s]);
+        } else {
+          meta[s].col_off = 0;
+          meta[s].staged = 0;
+          mbar_arrive(&bar_b[s]);
         }
-        if constexpr (WEIGHTED) {
+      };
+      for (int k = 0; k < my_units; ++k) {
+        const int s = k % kStages;
+        if (k >= kStages) mbar_wait(&bar_e[s], (uint32_t)(k / kStages - 1) & 1);  // consumers freed it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_front(k);
+        if (k >= 1) issue_cols(k - 1);
+      }
+      if (my_units > 0) issue_cols(my_units - 1);
+    }
+  } else {
+    // ----------------------------------------------------- consumer warps
+    for (int k = 0; k < my_units; ++k) {
+      const int u = blockIdx.x + k * grid;
+      const int s = k % kStages;
+      unsigned char* st = smem_raw + s * SL::BYTES;
+      const uint32_t par = (uint32_t)(k / kStages) & 1;
+      mbar_wait(&bar_a[s], par);
+      mbar_wait(&bar_b[s], par);
+    const int packed = meta[s].packed;
+      const int lgG = packed & 7, G = 1 << lgG;
+      const int lg = tid & (G - 1), grp = tid >> lgG;
+      long long va;
+      int nv;
+      {
+        const int tile = packed >> 12, pass = (packed >> 7) & 31;
+        const int groups = kBlock >> lgG;
+        va = (long long)tile * kBlock + (long long)pass * groups;
+        nv = (int)max(0LL, min((long long)groups, A.v_end - va));
+      }
+      const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
+      const uint32_t* colst = reinterpret_cast<const uint32_t*>(st + SL::COL_OFF);
+      const float* ys = reinterpret_cast<const float*>(st + SL::Y_OFF);
+      const float* ss = reinterpret_cast<const float*>(st + SL::S_OFF);
+      const bool staged = meta[s].staged != 0;
+      const uint32_t e0 = rp[0];
+      const int coff = meta[s].col_off;
+
+      double acc_e = 0.0, acc_n = 0.0, acc_o = 0.0, acc_bad = 0.0;
+      const bool active = grp < nv;
+      if (active) {
+        const long long v = va + grp;
+        const uint32_t beg = rp[grp], end = rp[grp + 1];
+        float yi[DIM], li[DIM];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          yi[d] = ys[grp * YS + d];
+          li[d] = NEST ? ys[grp * YS + (DIM == 2 ? 2 : 4) + d] : yi[d];
+        }
+        float f[DIM];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) f[d] = 0.f;
+        float e = 0.f;
+        constexpr bool kFast = DIM == 2 && !WEIGHTED && NORM == 0 && !NEST;
+        const int dmax = (packed >> 3) & 15;
+        bool fast = false;
+        if constexpr (kFast) fast = (G == 1) && staged && dmax <= 8;
+        if (fast) {
+          if constexpr (kFast) {
+            const uint32_t* cb = colst + (beg - e0 + coff);
+            const int deg = (int)(end - beg);
+            float ff[2] = {0.f, 0.f};
+            switch (dmax) {
+              case 1: fast_row<1>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              case 2: fast_row<2>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              case 3: fast_row<3>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              case 4: fast_row<4>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              case 5: fast_row<5>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              case 6: fast_row<6>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              case 7: fast_row<7>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              case 8: fast_row<8>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+              default: break;
+            }
+            f[0] = ff[0];
+            f[1] = ff[1];
+          }
+        } else
+        for (uint32_t k0 = beg + lg; k0 < end; k0 += (uint32_t)G * kUnroll) {
+          uint32_t cw[kUnroll];
+          float2 tw[WEIGHTED ? kUnroll : 1];
+          float gy[kUnroll][DIM], gl[kUnroll][DIM];
+          // A slot past the row end becomes a zero-target pair with the vertex
+          // itself: zero distance, zero force, zero stress — no masking needed.
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
             const uint32_t kk = k0 + (uint32_t)(q * G);
-            tw[q] = make_float2(0.f, 1.f);
-            if (kk < end) tw[q] = __ldg(A.ew + kk);
+            cw[q] = (uint32_t)v;
+            if (kk < end) cw[q] = staged ? colst[kk - e0 + coff] : __ldg(A.col + kk);
           }
-        }
+          if constexpr (WEIGHTED) {
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            gy[q][d] = yi[d];
-            gl[q][d] = li[d];
+            for (int q = 0; q < kUnroll; ++q) {
+              const uint32_t kk = k0 + (uint32_t)(q * G);
+              tw[q] = make_float2(0.f, 1.f);
+              if (kk < end) tw[q] = __ldg(A.ew + kk);
+            }
           }
-          if (k0 + (uint32_t)(q * G) < end) gather<DIM, NEST>(Yin, cw[q] & kIdMask, gy[q], gl[q]);
-        }
-        unsigned dmask = 0;
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          float2 twq = make_float2(0.f, 0.f);
-          if constexpr (WEIGHTED) twq = tw[q];
-          if (entry<DIM, NEST, NORM>(yi, li, gy[q], gl[q], cw[q], WEIGHTED, twq, c, true, f, e)) dmask |= 1u << q;
-        }
-        if (dmask) {  // degenerate random pairs (forces.py:167-174): measure-zero path
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
-            if ((dmask >> q) & 1u) {
-              const bool rn = cw[q] & kRandBit;
-              float t = rn ? 1.f : 0.f, w = rn ? c : 1.f;
-              if constexpr (WEIGHTED) {
-                t = tw[q].x;
-                w *= tw[q].y;
-              }
-              float uvec[DIM];
-              degenerate_dir<DIM>((uint32_t)v, cw[q] & kIdMask, gstep, uvec);
 #pragma unroll
-              for (int d = 0; d < DIM; ++d) f[d] = fmaf(w * t, uvec[d], f[d]);
+            for (int d = 0; d < DIM; ++d) {
+              gy[q][d] = yi[d];
+              gl[q][d] = li[d];
+            }
+            if (k0 + (uint32_t)(q * G) < end) gather<DIM, NEST>(Yin, cw[q] & kIdMask, gy[q], gl[q]);
+          }
+          unsigned dmask = 0;
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            float2 twq = make_float2(0.f, 0.f);
+            if constexpr (WEIGHTED) twq = tw[q];
+            if (entry<DIM, NEST, NORM>(yi, li, gy[q], gl[q], cw[q], WEIGHTED, twq, c, true, f, e)) dmask |= 1u << q;
+          }
+          if (dmask) {  // degenerate random pairs (forces.py:167-174): measure-zero path
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) {
+              if ((dmask >> q) & 1u) {
+                const bool rn = cw[q] & kRandBit;
+                float t = rn ? 1.f : 0.f, w = rn ? c : 1.f;
+                if constexpr (WEIGHTED) {
+                  t = tw[q].x;
+                  w *= tw[q].y;
+                }
+                float uvec[DIM];
+                degenerate_dir<DIM>((uint32_t)v, cw[q] & kIdMask, gstep, uvec);
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) f[d] = fmaf(w * t, uvec[d], f[d]);
+              }
             }
           }
         }
-      }
-      // fixed xor butterfly over the G lanes of the group (G uniform per unit);
-      // the mask names exactly this group's lanes (the walk leaves the warp diverged)
-      if (G > 1) {
-        const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((tid & 31) & ~(G - 1));
-        for (int o = G >> 1; o > 0; o >>= 1) {
+        // fixed xor butterfly over the G lanes of the group (G uniform per unit);
+        // the mask names exactly this group's lanes (the walk leaves the warp diverged)
+        if (G > 1) {
+          const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((tid & 31) & ~(G - 1));
+          for (int o = G >> 1; o > 0; o >>= 1) {
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) f[d] += __shfl_xor_sync(gmask, f[d], o);
-          e += __shfl_xor_sync(gmask, e, o);
+            for (int d = 0; d < DIM; ++d) f[d] += __shfl_xor_sync(gmask, f[d], o);
+            e += __shfl_xor_sync(gmask, e, o);
+          }
+        }
+        if (lg == 0) {
+          acc_e = (double)e;
+          if constexpr (OPT == OPT_NONE) {
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)f[d];
+          } else {
+            float sv[SSX];
+#pragma unroll
+            for (int q = 0; q < SSX; ++q) sv[q] = L::SS > 0 ? ss[grp * SSX + q] : 0.f;
+            apply_update<DIM, OPT>(A, Yout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
+          }
         }
       }
-      if (lg == 0) {
-        acc_e = (double)e;
-        if constexpr (OPT == OPT_NONE) {
+      // warp partial (fixed butterfly); the warp that completes the unit sums
+      // the 8 warp partials in warp order into the unit partial
+      float pe = (float)acc_e, pn = (float)acc_n, po = (float)acc_o, pb = (float)acc_bad;
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)f[d];
-        } else {
-          float sv[SSX];
+      for (int o = 16; o > 0; o >>= 1) {
+        pe += __shfl_xor_sync(0xffffffffu, pe, o);
+        pn += __shfl_xor_sync(0xffffffffu, pn, o);
+        po += __shfl_xor_sync(0xffffffffu, po, o);
+        pb += __shfl_xor_sync(0xffffffffu, pb, o);
+      }
+      if (lane == 0) {
+        sm_wp[s][warp] = make_float4(pe, pn, po, pb);
+        __threadfence_block();
+        if (atomicAdd(&sm_cnt[s], 1) == kConsumerWarps - 1) {
+          __threadfence_block();
+          double4 t = make_double4(0, 0, 0, 0);
 #pragma unroll
-          for (int q = 0; q < SSX; ++q) sv[q] = L::SS > 0 ? ss[grp * SSX + q] : 0.f;
-          apply_update<DIM, OPT>(A, Yout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
+          for (int w = 0; w < kConsumerWarps; ++w) {
+            const float4 q = sm_wp[s][w];
+            t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
+          }
+          A.partial[A.tile0 + u] = t;
+          sm_cnt[s] = 0;
+          __threadfence_block();
         }
+        mbar_arrive(&bar_e[s]);  // this warp is done with stage s
       }
+      __syncwarp();
     }
-    // unit partial: fixed float warp butterfly, then warps 0..7 in order in double
-    float pe = (float)acc_e, pn = (float)acc_n, po = (float)acc_o, pb = (float)acc_bad;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      pe += __shfl_xor_sync(0xffffffffu, pe, o);
-      pn += __shfl_xor_sync(0xffffffffu, pn, o);
-      po += __shfl_xor_sync(0xffffffffu, po, o);
-      pb += __shfl_xor_sync(0xffffffffu, pb, o);
-    }
-    if ((tid & 31) == 0) sm_unit[buf][tid >> 5] = make_double4(pe, pn, po, pb);
-    block_sync();  // also: every thread is done reading stage s before it is refilled
-    if (tid == 0) {
-      double4 t = make_double4(0, 0, 0, 0);
-#pragma unroll
-      for (int w = 0; w < kBlock / 32; ++w) {
-        const double4 q = sm_unit[buf][w];
-        t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
-      }
-      A.partial[A.tile0 + u] = t;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async refills
-    }
-    buf ^= 1;
   }
 
   if (!A.fuse_finalize) return;
@@ -788,7 +882,7 @@ __global__ void __launch_bounds__(kBlock, IVHD_MINBLOCKS) step_kernel(StepArgs A
   block_sync();
   if (tid == 0) sm_last = (atomicAdd(&ctrl->arrive, 1u) == gridDim.x - 1);
   block_sync();
-  if (!sm_last) return;
+  if (!sm_last || tid >= kBlock) return;
   __threadfence();
   finalize_block<OPT>(A, sm_red);
 }
