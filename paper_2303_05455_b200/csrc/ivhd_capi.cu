@@ -77,6 +77,7 @@ struct ivhd_ctx {
   float* ybuf[2] = {nullptr, nullptr};  // 8 floats/vertex capacity
   float* state = nullptr;               // 8 floats/vertex capacity
   double4* partial = nullptr;
+  double4* bpart = nullptr;  // one per resident block of the step kernel
   double2* trace = nullptr;
   int64_t trace_cap = 0;
   Ctrl* ctrl = nullptr;      // device
@@ -196,6 +197,8 @@ int occupancy(ivhd_ctx* ctx, KernelInfo k) {
   auto it = ctx->occ.find(k.fn);
   if (it != ctx->occ.end()) return it->second;
   cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
+  if (const char* cv = getenv("IVHD_CARVEOUT"))  // experiment: shared-memory carveout percent
+    cudaFuncSetAttribute(k.fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
   int n = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, kThreads, k.smem) != cudaSuccess || n < 1) n = 1;
   ctx->occ[k.fn] = n;
@@ -334,11 +337,6 @@ __global__ void k_degrees(const uint32_t* __restrict__ row_ptr, int64_t m, uint3
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
     deg[i] = row_ptr[i + 1] - row_ptr[i];
-}
-
-__global__ void k_hybrid_key(uint32_t* __restrict__ deg, int64_t m) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    deg[i] = deg[i] > (uint32_t)kUnroll ? deg[i] : 0u;
 }
 
 __global__ void k_inverse(const int32_t* __restrict__ perm, int64_t m, int32_t* __restrict__ inv) {
@@ -486,8 +484,6 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
     if ((e = dalloc(ctx, &perm, 4 * m)) != cudaSuccess) break;
     k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, deg);
     k_iota<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ids, m);
-    if (order && strcmp(order, "hybrid") == 0)  // experiment: light rows keep the caller's order
-      k_hybrid_key<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(deg, m);
     if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
         cudaSuccess) break;
     if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
@@ -630,6 +626,7 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   A.ybuf1 = ctx->ybuf[1];
   A.state = ctx->state;
   A.partial = ctx->partial;
+  A.bpart = ctx->bpart;
   A.trace = ctx->trace;
   A.ctrl = ctx->ctrl;
   A.force_out = nullptr;
@@ -658,8 +655,24 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
 
 int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
   const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, k) * ctx->sm_count));
-  k.fn<<<grid, kThreads, k.smem, ctx->stream>>>(A);
-  CU(ctx, cudaGetLastError());
+  // Programmatic dependent launch: this grid may become resident while the
+  // previous iteration drains; it prefetches graph constants and then waits
+  // (griddepcontrol.wait) before reading positions, state or ctrl.
+  static const bool pdl = [] {
+    const char* e = getenv("IVHD_PDL");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = k.smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CU(ctx, cudaLaunchKernelEx(&cfg, k.fn, A));
   return IVHD_OK;
 }
 
@@ -816,6 +829,7 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   alloc((void**)&ctx->ybuf[1], sizeof(float) * 8 * vc);
   alloc((void**)&ctx->state, sizeof(float) * 8 * vc);
   alloc((void**)&ctx->partial, sizeof(double4) * 32 * ctx->n_tiles_cap);  // <= 32 units per tile
+  alloc((void**)&ctx->bpart, sizeof(double4) * 8 * ctx->sm_count);  // <= 2048/288 blocks per SM
   alloc((void**)&ctx->ctrl, sizeof(Ctrl));
   alloc((void**)&ctx->opctrl, sizeof(Ctrl));
   alloc((void**)&ctx->red_out, sizeof(double4));
@@ -860,7 +874,7 @@ int ivhd_destroy(ivhd_ctx* ctx) {
     dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.tile_dm); dfree(ctx, s.units);
   }
   dfree(ctx, ctx->perm); dfree(ctx, ctx->inv);
-  dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial);
+  dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial); dfree(ctx, ctx->bpart);
   dfree(ctx, ctx->trace); dfree(ctx, ctx->ctrl); dfree(ctx, ctx->opctrl); dfree(ctx, ctx->red_out);
   dfree(ctx, ctx->stage); dfree(ctx, ctx->op_y); dfree(ctx, ctx->op_force);
   dfree(ctx, ctx->snap_y); dfree(ctx, ctx->snap_state);

@@ -89,6 +89,7 @@ struct StepArgs {
   float* ybuf1;
   float* state;
   double4* partial;
+  double4* bpart;         // fused mode: one partial per block (its units, in order)
   double2* trace;
   Ctrl* ctrl;
   double* force_out;      // OPT_NONE only: (M, DIM) float64
@@ -300,20 +301,23 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double4* sm /*[kBlock/3
 }
 
 // ---------------------------------------------------------------- finalize
-// Reduce all tile partials in a fixed order and take the iteration decision
+// Reduce n partials in a fixed order and take the iteration decision
 // (optim.py:80-92 + engine.py:373-384).  Executed by ONE whole block; each
-// thread keeps 8 tiles in flight so the tail is ~one memory round trip.
+// thread keeps 8 partials in flight.  Fused single-GPU mode reduces the
+// per-block partials (one per resident block); sharded mode reduces the
+// all-gathered per-unit partials, whose order does not depend on the rank
+// count.
 template <int OPT>
-__device__ void finalize_block(const StepArgs& A, double4* sm) {
+__device__ void finalize_block(const StepArgs& A, double4* sm, const double4* src, int n) {
   Ctrl* ctrl = A.ctrl;
-  const double2* p2 = reinterpret_cast<const double2*>(A.partial);
+  const double2* p2 = reinterpret_cast<const double2*>(src);
   double4 s = make_double4(0, 0, 0, 0);
-  for (int t0 = threadIdx.x; t0 < A.n_tiles_global; t0 += 8 * kBlock) {
+  for (int t0 = threadIdx.x; t0 < n; t0 += 8 * kBlock) {
     double2 a[8], b[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int t = t0 + u * kBlock;
-      if (t < A.n_tiles_global) {
+      if (t < n) {
         a[u] = __ldcg(p2 + 2 * t);
         b[u] = __ldcg(p2 + 2 * t + 1);
       } else {
@@ -469,7 +473,10 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
 #define IVHD_MINBLOCKS 3
 #endif
 constexpr int kUnroll = IVHD_UNROLL;
-constexpr int kStages = 3;         // TMA ring depth (units in flight per block)
+#ifndef IVHD_STAGES
+#define IVHD_STAGES 3
+#endif
+constexpr int kStages = IVHD_STAGES;  // TMA ring depth (units in flight per block)
 
 // ------------------------------------------------------------- TMA helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -494,6 +501,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// programmatic dependent launch (griddepcontrol): the next iteration's grid
+// may start once every block has signalled; it waits before reading data the
+// previous grid writes.  No-ops when the launch carries no PDL attribute.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// non-blocking probe of a phase (the producer polls two barrier kinds)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // global -> shared bulk copy (TMA, non-tensor); 16-byte aligned, size % 16 == 0
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -503,21 +529,35 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-constexpr int kColCap = 2048;      // staged column entries per unit (larger units read global)
-constexpr int kUnitCache = 1024;   // unit words cached per block
+#ifndef IVHD_COLCAP
+#define IVHD_COLCAP 2048
+#endif
+constexpr int kColCap = IVHD_COLCAP;  // staged column entries per unit (larger units read global)
+
+// column ids read straight from global: streamed, never allocated in L1 (L1
+// is kept for the neighbour-position gathers)
+__device__ __forceinline__ uint32_t ld_col(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+#ifndef IVHD_UNIT_CACHE
+#define IVHD_UNIT_CACHE 256
+#endif
+constexpr int kUnitCache = IVHD_UNIT_CACHE;  // unit words cached per block
 
 // Fast path for the dominant case (2-D, binary, L2, positions without look-ahead,
 // one lane per row): the unit's max row length D <= 8 is a template constant,
 // all D column reads and gathers are issued first, then ~26 instructions per
 // entry.  Slots past the row end are self pairs (zero contribution).
-template <int D>
+template <int D, bool GCOL>
 __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int deg, const float* __restrict__ Yin,
                                          uint32_t v, float y0, float y1, float c, long long gstep, float (&f)[2],
                                          float& e) {
   uint32_t cw[D];
   float2 p[D];
 #pragma unroll
-  for (int q = 0; q < D; ++q) cw[q] = q < deg ? cb[q] : v;
+  for (int q = 0; q < D; ++q) cw[q] = q < deg ? (GCOL ? ld_col(cb + q) : cb[q]) : v;
 #pragma unroll
   for (int q = 0; q < D; ++q) {
     p[q] = make_float2(y0, y1);
@@ -602,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   constexpr int SSX = L::SS > 0 ? L::SS : 1;
   constexpr int YS = L::YS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar_a[kStages], bar_b[kStages], bar_e[kStages];
+  __shared__ __align__(8) uint64_t bar_r[kStages], bar_a[kStages], bar_b[kStages], bar_e[kStages];
   __shared__ StageMeta meta[kStages];
   __shared__ float4 sm_wp[kStages][kConsumerWarps];
   __shared__ int sm_cnt[kStages];
@@ -610,36 +650,25 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   __shared__ int sm_units[kUnitCache];  // this block's unit words (static schedule)
 
   Ctrl* ctrl = A.ctrl;
-  if (ctrl->status != 0) return;  // diverged earlier: later iterations are no-ops
-  const int ycur = ctrl->cur;
-  const float c = (float)ctrl->c;
-  const float step = (float)ctrl->step;
-  const long long gstep = ctrl->gstep;
-  const float* __restrict__ Yin = ycur ? A.ybuf1 : A.ybuf0;
-  float* __restrict__ Yout = ycur ? A.ybuf0 : A.ybuf1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  float bc1 = 1.f, bc2 = 1.f;  // Adam bias corrections (optim.py:203-204)
-  if constexpr (OPT == OPT_ADAM) {
-    const double tt = (double)(ctrl->adam_t + 1);
-    bc1 = (float)(1.0 / (1.0 - pow((double)A.h.gv, tt)));
-    bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
-  }
-
   const int n_units = A.n_tiles;
   const int grid = gridDim.x;
   const int my_units = blockIdx.x < n_units ? (n_units - 1 - blockIdx.x) / grid + 1 : 0;
 
+  // ---- before the dependency wait: only graph constants (unit list, row
+  // pointers, columns) are read, so this overlaps the previous iteration's tail.
   for (int k = tid; k < min(my_units, kUnitCache); k += kThreads)
     sm_units[k] = __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bar_r[s], 1);
       mbar_init(&bar_a[s], 1);
       mbar_init(&bar_b[s], 1);
       mbar_init(&bar_e[s], kConsumerWarps);
       sm_cnt[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    griddep_launch_dependents();
   }
   block_sync();
 
@@ -653,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   if (warp == kConsumerWarps) {
     // ---------------------------------------------------- TMA producer warp
     if (lane == 0) {
-      auto issue_front = [&](int k) {  // row pointers + positions + state of local unit k
+      auto issue_rp = [&](int k) {  // row pointers of local unit k (graph constant)
         const int s = k % kStages;
         unsigned char* st = smem_raw + s * SL::BYTES;
         const int packed = k < kUnitCache ? sm_units[k] : __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
@@ -662,25 +691,19 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
         unit_range(packed, va, nv);
         meta[s].packed = packed;
         const uint32_t rp_bytes = (uint32_t)((nv + 1) * 4 + 15) / 16 * 16;
-        const uint32_t y_copy = ((uint32_t)nv * YS * 4 + 15) / 16 * 16;
-        uint32_t s_copy = 0;
-        if constexpr (L::SS > 0) s_copy = ((uint32_t)nv * L::SS * 4 + 15) / 16 * 16;
-        mbar_expect_tx(&bar_a[s], rp_bytes + y_copy + s_copy);
-        bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_a[s]);
-        bulk_g2s(st + SL::Y_OFF, Yin + va * YS, y_copy, &bar_a[s]);
-        if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, A.state + va * L::SS, s_copy, &bar_a[s]);
+        mbar_expect_tx(&bar_r[s], rp_bytes);
+        bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_r[s]);
       };
       auto issue_cols = [&](int k) {  // column segment of local unit k (its row pointers have landed)
         const int s = k % kStages;
         unsigned char* st = smem_raw + s * SL::BYTES;
-        mbar_wait(&bar_a[s], (uint32_t)(k / kStages) & 1);
         long long va;
         int nv;
         unit_range(meta[s].packed, va, nv);
         const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
         const uint32_t e0 = rp[0], e1 = rp[nv];
         const uint32_t a0 = e0 & ~3u, a1 = (e1 + 3u) & ~3u;  // 16-byte aligned cover
-        if (nv > 0 && e1 > e0 && a1 - a0 <= (uint32_t)kColCap + 4) {
+        if (kColCap > 0 && nv > 0 && e1 > e0 && a1 - a0 <= (uint32_t)kColCap + 4) {
           meta[s].col_off = (int)(e0 - a0);
           meta[s].staged = 1;
           mbar_expect_tx(&bar_b[s], (a1 - a0) * 4);
@@ -691,22 +714,69 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
           mbar_arrive(&bar_b[s]);
         }
       };
-      for (int k = 0; k < my_units; ++k) {
+      auto issue_ys = [&](int k, const float* Yin) {  // positions + optimizer state of unit k
         const int s = k % kStages;
-        if (k >= kStages) mbar_wait(&bar_e[s], (uint32_t)(k / kStages - 1) & 1);  // consumers freed it
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_front(k);
-        if (k >= 1) issue_cols(k - 1);
+        unsigned char* st = smem_raw + s * SL::BYTES;
+        long long va;
+        int nv;
+        unit_range(meta[s].packed, va, nv);
+        const uint32_t y_copy = ((uint32_t)nv * YS * 4 + 15) / 16 * 16;
+        uint32_t s_copy = 0;
+        if constexpr (L::SS > 0) s_copy = ((uint32_t)nv * L::SS * 4 + 15) / 16 * 16;
+        mbar_expect_tx(&bar_a[s], y_copy + s_copy);
+        bulk_g2s(st + SL::Y_OFF, Yin + va * YS, y_copy, &bar_a[s]);
+        if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, A.state + va * L::SS, s_copy, &bar_a[s]);
+      };
+      const int pre = min(my_units, kStages);
+      int nf = 0, nc = 0;
+      for (; nf < pre; ++nf) issue_rp(nf);
+      for (; nc < pre; ++nc) {
+        mbar_wait(&bar_r[nc], 0);
+        issue_cols(nc);
       }
-      if (my_units > 0) issue_cols(my_units - 1);
+      griddep_wait();  // the previous iteration (positions, state, ctrl) is complete
+      if (ctrl->status != 0) {  // diverged earlier: drain the prefetch and leave
+        for (int k = 0; k < pre; ++k) mbar_wait(&bar_b[k], 0);
+      } else {
+        const float* Yin = ctrl->cur ? A.ybuf1 : A.ybuf0;
+        for (int k = 0; k < pre; ++k) issue_ys(k, Yin);
+        // Event loop: stages are claimed as consumers free them; a unit's
+        // columns are requested the moment its row pointers land.
+        while (nc < my_units) {
+          if (nf < my_units && nf < nc + kStages && mbar_test(&bar_e[nf % kStages], (uint32_t)(nf / kStages - 1) & 1)) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_rp(nf);
+            issue_ys(nf, Yin);
+            ++nf;
+          }
+          if (nc < nf && mbar_test(&bar_r[nc % kStages], (uint32_t)(nc / kStages) & 1)) issue_cols(nc++);
+        }
+      }
     }
+    griddep_wait();
+    if (ctrl->status != 0) return;
   } else {
     // ----------------------------------------------------- consumer warps
+    griddep_wait();
+    if (ctrl->status != 0) return;  // diverged earlier: later iterations are no-ops
+    const int ycur = ctrl->cur;
+    const float c = (float)ctrl->c;
+    const float step = (float)ctrl->step;
+    const long long gstep = ctrl->gstep;
+    const float* __restrict__ Yin = ycur ? A.ybuf1 : A.ybuf0;
+    float* __restrict__ Yout = ycur ? A.ybuf0 : A.ybuf1;
+    float bc1 = 1.f, bc2 = 1.f;  // Adam bias corrections (optim.py:203-204)
+    if constexpr (OPT == OPT_ADAM) {
+      const double tt = (double)(ctrl->adam_t + 1);
+      bc1 = (float)(1.0 / (1.0 - pow((double)A.h.gv, tt)));
+      bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
+    }
     for (int k = 0; k < my_units; ++k) {
       const int u = blockIdx.x + k * grid;
       const int s = k % kStages;
       unsigned char* st = smem_raw + s * SL::BYTES;
       const uint32_t par = (uint32_t)(k / kStages) & 1;
+      mbar_wait(&bar_r[s], par);
       mbar_wait(&bar_a[s], par);
       mbar_wait(&bar_b[s], par);
     const int packed = meta[s].packed;
@@ -746,22 +816,31 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
         constexpr bool kFast = DIM == 2 && !WEIGHTED && NORM == 0 && !NEST;
         const int dmax = (packed >> 3) & 15;
         bool fast = false;
-        if constexpr (kFast) fast = (G == 1) && staged && dmax <= 8;
+        if constexpr (kFast) fast = (G == 1) && (staged || kColCap == 0) && dmax <= 8;
         if (fast) {
           if constexpr (kFast) {
-            const uint32_t* cb = colst + (beg - e0 + coff);
             const int deg = (int)(end - beg);
             float ff[2] = {0.f, 0.f};
-            switch (dmax) {
-              case 1: fast_row<1>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              case 2: fast_row<2>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              case 3: fast_row<3>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              case 4: fast_row<4>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              case 5: fast_row<5>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              case 6: fast_row<6>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              case 7: fast_row<7>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              case 8: fast_row<8>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-              default: break;
+            if (staged) {
+              const uint32_t* cb = colst + (beg - e0 + coff);
+              switch (dmax) {
+#define IVHD_FAST_CASE(D) \
+  case D: fast_row<D, false>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+                IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
+                IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
+#undef IVHD_FAST_CASE
+                default: break;
+              }
+            } else if constexpr (kColCap == 0) {
+              const uint32_t* cb = A.col + beg;
+              switch (dmax) {
+#define IVHD_FAST_CASE(D) \
+  case D: fast_row<D, true>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+                IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
+                IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
+#undef IVHD_FAST_CASE
+                default: break;
+              }
             }
             f[0] = ff[0];
             f[1] = ff[1];
@@ -777,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
           for (int q = 0; q < kUnroll; ++q) {
             const uint32_t kk = k0 + (uint32_t)(q * G);
             cw[q] = (uint32_t)v;
-            if (kk < end) cw[q] = staged ? colst[kk - e0 + coff] : __ldg(A.col + kk);
+            if (kk < end) cw[q] = staged ? colst[kk - e0 + coff] : ld_col(A.col + kk);
           }
           if constexpr (WEIGHTED) {
 #pragma unroll
@@ -876,6 +955,17 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   }
 
   if (!A.fuse_finalize) return;
+  // block partial: this block's unit partials in unit order (one warp)
+  block_sync();
+  if (warp == 0) {
+    double4 t = make_double4(0, 0, 0, 0);
+    for (int k = lane; k < my_units; k += 32) {
+      const double4 q = A.partial[A.tile0 + blockIdx.x + k * grid];
+      t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
+    }
+    t.x = warp_dsum(t.x); t.y = warp_dsum(t.y); t.z = warp_dsum(t.z); t.w = warp_dsum(t.w);
+    if (lane == 0) A.bpart[blockIdx.x] = t;
+  }
   // last-block-done: the block that retires last reduces and decides
   __shared__ bool sm_last;
   __threadfence();
@@ -884,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   block_sync();
   if (!sm_last || tid >= kBlock) return;
   __threadfence();
-  finalize_block<OPT>(A, sm_red);
+  finalize_block<OPT>(A, sm_red, A.bpart, (int)gridDim.x);
 }
 
 // Standalone finalizer (sharded mode, after the exchange): one block.
@@ -892,7 +982,7 @@ template <int OPT>
 __global__ void __launch_bounds__(kBlock) finalize_kernel(StepArgs A) {
   __shared__ double4 sm_red[kBlock / 32];
   if (A.ctrl->status != 0) return;
-  finalize_block<OPT>(A, sm_red);
+  finalize_block<OPT>(A, sm_red, A.partial, A.n_tiles_global);
 }
 
 }  // namespace ivhd

@@ -49,8 +49,9 @@ if __name__ == "__main__":
     for lib in sys.argv[1:]:
         for kind, m in graphs:
             env = dict(os.environ, IVHD_B200_LIB=os.path.abspath(lib.split("@")[0]))
-            if "@" in lib:
-                env["IVHD_ORDER"] = lib.split("@")[1]
+            for opt in lib.split("@")[1:]:  # lib.so@identity or lib.so@ENV=VAL
+                k, _, v = opt.partition("=")
+                env.update({k: v} if v else {"IVHD_ORDER": k})
             r = subprocess.run([sys.executable, __file__, "--child", "300", kind, str(m)], env=env,
                                capture_output=True, text=True)
             print(r.stdout.strip() or r.stderr[-800:], flush=True)
