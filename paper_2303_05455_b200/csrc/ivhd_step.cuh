@@ -679,6 +679,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
     nv = (int)max(0LL, min((long long)groups, A.v_end - va));
   };
 
+  float te = 0.f, tn = 0.f, to = 0.f, tb = 0.f;  // fused mode: this thread's running partials
   if (warp == kConsumerWarps) {
     // ---------------------------------------------------- TMA producer warp
     if (lane == 0) {
@@ -923,8 +924,17 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
           }
         }
       }
-      // warp partial (fixed butterfly); the warp that completes the unit sums
-      // the 8 warp partials in warp order into the unit partial
+      if (A.fuse_finalize) {
+        // single GPU: running per-thread sums (fixed vertex order); the block
+        // reduces them once after its last unit
+        te += (float)acc_e; tn += (float)acc_n; to += (float)acc_o; tb += (float)acc_bad;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_e[s]);  // this warp is done with stage s
+        continue;
+      }
+      // sharded: per-unit partials (rank-count independent order).  Warp
+      // partial by a fixed butterfly; the warp that completes the unit sums
+      // the 8 warp partials in warp order into the unit partial.
       float pe = (float)acc_e, pn = (float)acc_n, po = (float)acc_o, pb = (float)acc_bad;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -955,16 +965,21 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   }
 
   if (!A.fuse_finalize) return;
-  // block partial: this block's unit partials in unit order (one warp)
+  // block partial: warp sums in a fixed butterfly, then warps in order
   block_sync();
-  if (warp == 0) {
+  if (warp < kConsumerWarps) {
+    double4 v = make_double4(te, tn, to, tb);
+    v.x = warp_dsum(v.x); v.y = warp_dsum(v.y); v.z = warp_dsum(v.z); v.w = warp_dsum(v.w);
+    if (lane == 0) sm_red[warp] = v;
+  }
+  block_sync();
+  if (tid == 0) {
     double4 t = make_double4(0, 0, 0, 0);
-    for (int k = lane; k < my_units; k += 32) {
-      const double4 q = A.partial[A.tile0 + blockIdx.x + k * grid];
-      t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      t.x += sm_red[w].x; t.y += sm_red[w].y; t.z += sm_red[w].z; t.w += sm_red[w].w;
     }
-    t.x = warp_dsum(t.x); t.y = warp_dsum(t.y); t.z = warp_dsum(t.z); t.w = warp_dsum(t.w);
-    if (lane == 0) A.bpart[blockIdx.x] = t;
+    A.bpart[blockIdx.x] = t;
   }
   // last-block-done: the block that retires last reduces and decides
   __shared__ bool sm_last;

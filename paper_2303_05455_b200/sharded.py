@@ -13,8 +13,10 @@ the fused step kernel (ivhd_step_local), then all-gathers
 
 and every rank runs the same fixed-order finalizer (ivhd_step_finalize) over
 the full tile array — so the auto-adapt commit/rollback decision, the trace
-and the positions are identical on all ranks, and identical to a single-GPU
-run (tiles and their reduction order do not depend on the rank count).
+and the positions are identical on all ranks and for every rank count (tiles
+and their reduction order do not depend on it).  The fused single-GPU loop
+sums per-thread running partials instead, so its trace agrees with the
+sharded one to fp32 summation order (the per-vertex update is the same).
 
 The exchange goes through torch.distributed (NCCL over NVLink on GPUs, gloo
 for the CPU tests); the library launches on the caller's CUDA stream so the

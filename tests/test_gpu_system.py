@@ -26,7 +26,11 @@ def _problem(m=6000, seed=0):
     return synth.planted_graph(m, 3, seed=seed)
 
 
-def test_sharded_nccl_world1_is_bit_identical_to_single_gpu():
+def test_sharded_nccl_world1_matches_single_gpu():
+    """The sharded driver (per-unit partials, standalone finalizer) against the
+    fused single-GPU loop (per-thread running partials): same per-vertex math,
+    so positions and step decisions agree bit for bit here; the reported
+    stress differs only by the fp32 summation order of the partials."""
     import torch
     import torch.distributed as dist
 
@@ -57,7 +61,7 @@ def test_sharded_nccl_world1_is_bit_identical_to_single_gpu():
         s_sh, b_sh, done, div = sh.run(0, "l2", 0.1, 40)
         assert done == 40 and not div
         np.testing.assert_array_equal(sh.positions(), ref.positions())
-        np.testing.assert_array_equal(np.asarray(s_sh), s_ref)
+        np.testing.assert_allclose(np.asarray(s_sh), s_ref, rtol=1e-6)
         np.testing.assert_array_equal(np.asarray(b_sh), b_ref)
     finally:
         dist.destroy_process_group()
