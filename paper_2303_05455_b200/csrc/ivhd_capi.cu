@@ -29,7 +29,7 @@ struct CsrSlot {
   float2* ew = nullptr;         // [n] or nullptr (binary)
   uint8_t* tile_g = nullptr;    // [n_tiles_cap] lanes per vertex of each tile
   uint8_t* tile_dm = nullptr;   // [n_tiles_cap] max row length of each tile (clamped to 255)
-  int* units = nullptr;         // work units (tile << 12 | pass << 7 | min(maxdeg,15) << 3 | log2 G)
+  int* units = nullptr;         // work units (tile << 12 | pass << 7 | min(slots per lane,15) << 3 | log2 G)
   int n_units = 0;
   std::vector<int> unit_base;   // host: first unit of each tile (n_tiles_cap + 1)
   int64_t n = 0;                // entries (2 * connections)
@@ -594,7 +594,7 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
     for (int t = 0; t < ctx->n_tiles_cap; ++t) {
       S.unit_base[t + 1] = S.unit_base[t] + g[t];
       const int lg = __builtin_ctz((unsigned)g[t]);
-      const int d15 = std::min<int>(dm[t], 15);
+      const int d15 = std::min<int>((dm[t] + g[t] - 1) / g[t], 15);  // slots per lane
       for (int p = 0; p < g[t]; ++p) units.push_back(t << 12 | p << 7 | d15 << 3 | lg);
     }
     S.n_units = (int)units.size();

@@ -28,6 +28,7 @@
 // the next launch reads.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace ivhd {
@@ -94,7 +95,7 @@ struct StepArgs {
   Ctrl* ctrl;
   double* force_out;      // OPT_NONE only: (M, DIM) float64
   const uint8_t* tile_g;  // lanes per vertex of every (global) tile
-  const int* units;       // work unit -> tile << 12 | pass << 7 | min(maxdeg,15) << 3 | log2 G
+  const int* units;       // work unit -> tile << 12 | pass << 7 | min(slots,15) << 3 | log2 G
   long long v_begin, v_end;
   int tile_v;
   int n_tiles;            // work units this launch processes
@@ -473,6 +474,9 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
 #define IVHD_MINBLOCKS 3
 #endif
 constexpr int kUnroll = IVHD_UNROLL;
+#ifndef IVHD_BACKOFF_NS
+#define IVHD_BACKOFF_NS 0
+#endif
 #ifndef IVHD_STAGES
 #define IVHD_STAGES 3
 #endif
@@ -546,18 +550,19 @@ __device__ __forceinline__ uint32_t ld_col(const uint32_t* p) {
 #endif
 constexpr int kUnitCache = IVHD_UNIT_CACHE;  // unit words cached per block
 
-// Fast path for the dominant case (2-D, binary, L2, positions without look-ahead,
-// one lane per row): the unit's max row length D <= 8 is a template constant,
-// all D column reads and gathers are issued first, then ~26 instructions per
-// entry.  Slots past the row end are self pairs (zero contribution).
+// Fast path for the dominant case (2-D, binary, L2, positions without look-ahead):
+// a lane handles the entries cb[0], cb[G], ... (deg of them; G lanes per row);
+// the slot count D <= 8 is a template constant, all D column reads and gathers
+// are issued first, then ~20 instructions per entry.  Slots past the lane's
+// last entry are self pairs (zero contribution).
 template <int D, bool GCOL>
-__device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int deg, const float* __restrict__ Yin,
-                                         uint32_t v, float y0, float y1, float c, long long gstep, float (&f)[2],
-                                         float& e) {
+__device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G, int deg,
+                                         const float* __restrict__ Yin, uint32_t v, float y0, float y1, float c,
+                                         long long gstep, float (&f)[2], float& e) {
   uint32_t cw[D];
   float2 p[D];
 #pragma unroll
-  for (int q = 0; q < D; ++q) cw[q] = q < deg ? (GCOL ? ld_col(cb + q) : cb[q]) : v;
+  for (int q = 0; q < D; ++q) cw[q] = q < deg ? (GCOL ? ld_col(cb + q * G) : cb[q * G]) : v;
 #pragma unroll
   for (int q = 0; q < D; ++q) {
     p[q] = make_float2(y0, y1);
@@ -616,7 +621,7 @@ constexpr int step_smem_bytes() {
 // Per-stage metadata written by the producer before it arrives on the
 // stage's barriers (release) and read by consumers after the wait (acquire).
 struct StageMeta {
-  int packed;       // unit word: tile << 12 | pass << 7 | min(maxdeg,15) << 3 | log2 G
+  int packed;       // unit word: tile << 12 | pass << 7 | min(slots,15) << 3 | log2 G
   int col_off;      // entries skipped at the front of the staged columns (alignment)
   int staged;       // 1 if the unit's columns are in shared memory
   int pad;
@@ -744,13 +749,19 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
         // Event loop: stages are claimed as consumers free them; a unit's
         // columns are requested the moment its row pointers land.
         while (nc < my_units) {
+          bool idle = true;
           if (nf < my_units && nf < nc + kStages && mbar_test(&bar_e[nf % kStages], (uint32_t)(nf / kStages - 1) & 1)) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue_rp(nf);
             issue_ys(nf, Yin);
             ++nf;
+            idle = false;
           }
-          if (nc < nf && mbar_test(&bar_r[nc % kStages], (uint32_t)(nc / kStages) & 1)) issue_cols(nc++);
+          if (nc < nf && mbar_test(&bar_r[nc % kStages], (uint32_t)(nc / kStages) & 1)) {
+            issue_cols(nc++);
+            idle = false;
+          }
+          if (IVHD_BACKOFF_NS > 0 && idle) __nanosleep(IVHD_BACKOFF_NS);  // leave issue slots to the consumers
         }
       }
     }
@@ -815,34 +826,32 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
         for (int d = 0; d < DIM; ++d) f[d] = 0.f;
         float e = 0.f;
         constexpr bool kFast = DIM == 2 && !WEIGHTED && NORM == 0 && !NEST;
-        const int dmax = (packed >> 3) & 15;
+        const int slots = (packed >> 3) & 15;  // per lane: ceil(tile max degree / G), 15 = more
         bool fast = false;
-        if constexpr (kFast) fast = (G == 1) && (staged || kColCap == 0) && dmax <= 8;
+        if constexpr (kFast) fast = true;
         if (fast) {
           if constexpr (kFast) {
             const int deg = (int)(end - beg);
+            const int nl = deg > lg ? (deg - lg + G - 1) >> lgG : 0;  // this lane's entries
             float ff[2] = {0.f, 0.f};
-            if (staged) {
-              const uint32_t* cb = colst + (beg - e0 + coff);
-              switch (dmax) {
+            auto run = [&](auto gcol_tag, const uint32_t* cb) {
+              constexpr bool GC = decltype(gcol_tag)::value;
+              if (slots <= 8) {
+                switch (slots) {
 #define IVHD_FAST_CASE(D) \
-  case D: fast_row<D, false>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-                IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
-                IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
+  case D: fast_row<D, GC>(cb, G, nl, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+                  IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
+                  IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
 #undef IVHD_FAST_CASE
-                default: break;
+                  default: break;
+                }
+              } else {
+                for (int c0 = 0; c0 < nl; c0 += 8)
+                  fast_row<8, GC>(cb + c0 * G, G, nl - c0, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e);
               }
-            } else if constexpr (kColCap == 0) {
-              const uint32_t* cb = A.col + beg;
-              switch (dmax) {
-#define IVHD_FAST_CASE(D) \
-  case D: fast_row<D, true>(cb, deg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
-                IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
-                IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
-#undef IVHD_FAST_CASE
-                default: break;
-              }
-            }
+            };
+            if (staged) run(std::false_type{}, colst + (beg - e0 + coff) + lg);
+            else run(std::true_type{}, A.col + beg + lg);
             f[0] = ff[0];
             f[1] = ff[1];
           }
