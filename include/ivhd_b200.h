@@ -12,6 +12,8 @@
  *
  *   ivhd_create / ivhd_destroy      _Run.__init__ device state       engine.py:162-221
  *   ivhd_set_graph                  _Run._build_edges (binary)       engine.py:225-262
+ *   ivhd_set_graph_sampled          sample_random_neighbors + above  engine.py:132-146,225-262
+ *   ivhd_init_positions             init_layout (same PCG64 stream)  engine.py:124-129
  *   ivhd_set_connections            ConnectionSet(...)               forces.py:20-50
  *   ivhd_set_positions              init_layout result / observer    engine.py:124-129,214
  *   ivhd_get_positions              RunResult.embedding.points       engine.py:413
@@ -33,7 +35,7 @@
 extern "C" {
 #endif
 
-#define IVHD_ABI_VERSION 1
+#define IVHD_ABI_VERSION 2
 
 enum ivhd_status {
   IVHD_OK = 0,
@@ -83,6 +85,20 @@ const char* ivhd_last_error(const ivhd_ctx* ctx);
  * weight c.  Builds the symmetrised CSR on the device. */
 int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_stride,
                    int ncols, const int32_t* rn_ids, int rn);
+
+/* numpy's default bit generator (PCG64) on the device.  rng[6] =
+ * {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger} of the caller's
+ * numpy PCG64 state; it is read and advanced in place exactly as the
+ * reference's numpy draws advance it, so the caller's Generator can continue.
+ *
+ * init_positions: positions = gen.uniform(lo, hi, size=(m, dim)).
+ * set_graph_sampled: rn partners per vertex = gen.integers(0, m, (m, rn)) with
+ * the reference's row-major re-draw of picks equal to the row or one of its
+ * nn ids, then the binary connection set of ivhd_set_graph.  picks_out
+ * (m*rn, may be NULL) receives the partners. */
+int ivhd_init_positions(ivhd_ctx* ctx, uint64_t* rng, double lo, double hi);
+int ivhd_set_graph_sampled(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_stride,
+                           int ncols, int rn, uint64_t* rng, int32_t* picks_out);
 
 /* Generic connection set (edges (L,2) row-major).  targets/scale may be NULL
  * (NULL targets = binary: 0 for nn, 1 for random pairs). */

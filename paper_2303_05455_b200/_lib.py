@@ -19,6 +19,7 @@ OK, ERR_INVALID_ARG, ERR_CUDA, ERR_DIVERGED, ERR_STATE = range(5)
 NORM = {"l2": 0, "l1": 1}
 OPT_KIND = {"force-directed": 0, "sgd": 1, "momentum": 2, "nesterov": 3, "adam": 4, "adadelta": 5}
 
+ABI_VERSION = 2
 c_i32p = ctypes.POINTER(ctypes.c_int32)
 c_f64p = ctypes.POINTER(ctypes.c_double)
 c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -47,6 +48,9 @@ SIGNATURES = {
     "ivhd_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
     "ivhd_set_graph": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, ctypes.c_int64,
                                       ctypes.c_int, c_i32p, ctypes.c_int]),
+    "ivhd_init_positions": (ctypes.c_int, [ctypes.c_void_p, c_u64p, ctypes.c_double, ctypes.c_double]),
+    "ivhd_set_graph_sampled": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, ctypes.c_int64,
+                                              ctypes.c_int, ctypes.c_int, c_u64p, c_i32p]),
     "ivhd_set_connections": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, c_u8p, c_f64p,
                                             c_f64p, ctypes.c_int64]),
     "ivhd_set_positions": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),
@@ -92,7 +96,7 @@ def load():
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
-            if lib.ivhd_abi_version() != 1:
+            if lib.ivhd_abi_version() != ABI_VERSION:
                 raise DeviceError("libivhd_b200.so ABI version mismatch")
             _lib = lib
         return _lib

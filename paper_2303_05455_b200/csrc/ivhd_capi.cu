@@ -4,18 +4,21 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
 
 #include "../../include/ivhd_b200.h"
 #include "ivhd_step.cuh"
+#include "ivhd_rng.cuh"
 
 using namespace ivhd;
 
@@ -118,6 +121,31 @@ inline cudaError_t dalloc(ivhd_ctx* ctx, T** p, size_t bytes) {
 template <class T>
 inline void dfree(ivhd_ctx* ctx, T* p) {
   if (p) cudaFreeAsync(reinterpret_cast<void*>(const_cast<typename std::remove_const<T>::type*>(p)), ctx->stream);
+}
+
+// Pinned host mirrors of Ctrl come from a process-wide pool: cudaFreeHost
+// synchronises the device and can take 100+ ms, so blocks are recycled and
+// never returned to the driver (one page serves 32 live contexts).
+std::mutex g_pinned_mu;
+std::vector<Ctrl*> g_pinned_free;
+
+Ctrl* pinned_ctrl_get() {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  if (g_pinned_free.empty()) {
+    constexpr int kPer = 32;
+    Ctrl* page = nullptr;
+    if (cudaMallocHost(&page, sizeof(Ctrl) * kPer) != cudaSuccess) return nullptr;
+    for (int i = kPer - 1; i >= 0; --i) g_pinned_free.push_back(page + i);
+  }
+  Ctrl* c = g_pinned_free.back();
+  g_pinned_free.pop_back();
+  *c = Ctrl{};
+  return c;
+}
+
+void pinned_ctrl_put(Ctrl* c) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(c);
 }
 
 int fail(ivhd_ctx* ctx, int code, const char* fmt, ...) {
@@ -840,7 +868,7 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   k_iota<<<grid_for(vc, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->perm, vc);  // identity until the first CSR
   k_iota<<<grid_for(vc, ctx->sm_count), 256, 0, ctx->stream>>>(ctx->inv, vc);
   cudaStreamSynchronize(ctx->stream);
-  if (cudaMallocHost(&ctx->ctrl_h, sizeof(Ctrl)) != cudaSuccess)
+  if ((ctx->ctrl_h = pinned_ctrl_get()) == nullptr)
     return bail(fail(ctx, IVHD_ERR_CUDA, "pinned alloc failed"));
   memset(ctx->ctrl_h, 0, sizeof(Ctrl));
   ctx->ctrl_h->c = 0.1;
@@ -867,9 +895,19 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
 
 int ivhd_destroy(ivhd_ctx* ctx) {
   if (!ctx) return IVHD_OK;
+  static const bool dbg = getenv("IVHD_DEBUG_DESTROY") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[ivhd_destroy] %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  lap("sync");
   drop_graphs(ctx);
+  lap("graphs");
   for (auto& s : ctx->slots) {
     dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.tile_dm); dfree(ctx, s.units);
   }
@@ -878,10 +916,35 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   dfree(ctx, ctx->trace); dfree(ctx, ctx->ctrl); dfree(ctx, ctx->opctrl); dfree(ctx, ctx->red_out);
   dfree(ctx, ctx->stage); dfree(ctx, ctx->op_y); dfree(ctx, ctx->op_force);
   dfree(ctx, ctx->snap_y); dfree(ctx, ctx->snap_state);
-  if (ctx->ctrl_h) cudaFreeHost(ctx->ctrl_h);
+  lap("frees");
+  if (ctx->ctrl_h) pinned_ctrl_put(ctx->ctrl_h);
+  lap("free_host");
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  lap("stream");
   delete ctx;
   return IVHD_OK;
+}
+
+// binary connection set from device-resident nn ids [m, nn_stride] and random
+// partners [m, rn] (engine.py:165-221 with distance_mode == "binary")
+static int graph_from_device(ivhd_ctx* ctx, int slot, const int32_t* d_nn, int64_t nn_stride, int ncols,
+                             const int32_t* d_rn, int rn) {
+  const int64_t m = ctx->m, n_nn = m * ncols, L = n_nn + m * rn;
+  int32_t *d_src = nullptr, *d_dst = nullptr;
+  cudaError_t e = cudaSuccess;
+  do {
+    if ((e = dalloc(ctx, &d_src, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_dst, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
+    if (L > 0)
+      k_binary_edges<<<grid_for(L, ctx->sm_count), 256, 0, ctx->stream>>>(d_nn, nn_stride, ncols, d_rn, rn,
+                                                                          m, d_src, d_dst);
+    e = cudaGetLastError();
+  } while (0);
+  int rc = IVHD_OK;
+  if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "set_graph: %s", cudaGetErrorString(e));
+  else rc = build_csr(ctx, slot, d_src, d_dst, nullptr, n_nn, nullptr, nullptr, L);
+  dfree(ctx, d_src); dfree(ctx, d_dst);
+  return rc;
 }
 
 int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_stride, int ncols,
@@ -891,8 +954,8 @@ int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_st
   if (ncols < 0 || rn < 0 || nn_stride < ncols || (ncols > 0 && !nn_ids) || (rn > 0 && !rn_ids))
     return fail(ctx, IVHD_ERR_INVALID_ARG, "bad graph arguments");
   CU(ctx, cudaSetDevice(ctx->device));
-  const int64_t m = ctx->m, n_nn = m * ncols, L = n_nn + m * rn;
-  int32_t *d_nn = nullptr, *d_rn = nullptr, *d_src = nullptr, *d_dst = nullptr;
+  const int64_t m = ctx->m;
+  int32_t *d_nn = nullptr, *d_rn = nullptr;
   cudaError_t e = cudaSuccess;
   do {
     if (ncols > 0) {
@@ -905,17 +968,214 @@ int ivhd_set_graph(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_st
       if ((e = cudaMemcpyAsync(d_rn, rn_ids, sizeof(int32_t) * m * rn, cudaMemcpyHostToDevice,
                                ctx->stream)) != cudaSuccess) break;
     }
-    if ((e = dalloc(ctx, &d_src, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
-    if ((e = dalloc(ctx, &d_dst, sizeof(int32_t) * std::max<int64_t>(L, 1))) != cudaSuccess) break;
-    if (L > 0)
-      k_binary_edges<<<grid_for(L, ctx->sm_count), 256, 0, ctx->stream>>>(d_nn, nn_stride, ncols, d_rn, rn,
-                                                                          m, d_src, d_dst);
-    e = cudaGetLastError();
   } while (0);
   int rc = IVHD_OK;
-  if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "set_graph: %s", cudaGetErrorString(e));
-  else rc = build_csr(ctx, slot, d_src, d_dst, nullptr, n_nn, nullptr, nullptr, L);
-  dfree(ctx, d_nn); dfree(ctx, d_rn); dfree(ctx, d_src); dfree(ctx, d_dst);
+  if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "set_graph upload: %s", cudaGetErrorString(e));
+  else rc = graph_from_device(ctx, slot, d_nn, nn_stride, ncols, d_rn, rn);
+  dfree(ctx, d_nn); dfree(ctx, d_rn);
+  return rc;
+}
+
+// ------------------------------------------------------ device RNG (PCG64)
+
+__global__ void k_accept_scatter(const int32_t* __restrict__ val, const int32_t* __restrict__ ok,
+                                 const int32_t* __restrict__ pos, int64_t n_cand, int64_t N, int32_t* __restrict__ picks,
+                                 int64_t* __restrict__ last_q) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_cand; q += (int64_t)gridDim.x * blockDim.x) {
+    if (!ok[q]) continue;
+    const int64_t r = pos[q];  // inclusive rank among accepted draws
+    if (r <= N) picks[r - 1] = val[q];
+    if (r == N) *last_q = q;
+  }
+}
+
+__global__ void k_flag_to_index(const int32_t* __restrict__ flag, const int32_t* __restrict__ pos, int64_t n,
+                                int64_t* __restrict__ idx) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    if (flag[k]) idx[pos[k] - 1] = k;
+}
+
+__global__ void k_u8_to_i32(const uint8_t* __restrict__ a, int64_t n, int32_t* __restrict__ b) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    b[k] = a[k];
+}
+
+__global__ void k_scatter_i32(const int64_t* __restrict__ idx, const int32_t* __restrict__ v, int64_t n,
+                              int32_t* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    out[idx[k]] = v[k];
+}
+
+// inclusive prefix sum of int32 flags (n < 2^31)
+static cudaError_t scan_flags(ivhd_ctx* ctx, const int32_t* in, int32_t* out, int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, (int)n, ctx->stream);
+  if (e != cudaSuccess) return e;
+  void* tmp = nullptr;
+  if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) return e;
+  e = cub::DeviceScan::InclusiveSum(tmp, tb, in, out, (int)n, ctx->stream);
+  dfree(ctx, tmp);
+  return e;
+}
+
+int ivhd_init_positions(ivhd_ctx* ctx, uint64_t* rng, double lo, double hi) {
+  if (!ctx || !rng) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  pcg::State st = pcg::load(rng);
+  const int64_t n = ctx->m * ctx->dim;
+  const int64_t chunks = (n + pcg::kChunk - 1) / pcg::kChunk;
+  pcg::k_uniform<<<grid_for(chunks, ctx->sm_count), 256, 0, ctx->stream>>>(
+      rng[0], rng[1], rng[2], rng[3], n, lo, hi - lo, ctx->stage);
+  CU(ctx, cudaGetLastError());
+  const int ys = ys_of(ctx->dim, ctx->opt.kind);
+  const bool nest = ctx->opt.kind == IVHD_OPT_NESTEROV;
+  k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
+      ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
+      (float)ctx->hyper.beta, ctx->ybuf[ctx->ctrl_h->cur]);
+  CU(ctx, cudaGetLastError());
+  ctx->ctrl_h->status = 0;
+  ctx->ctrl_h->last_commit = 0;
+  TRY(push_ctrl(ctx));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->pos_set = true;
+  st.s = pcg::advance(st.s, st.inc, (uint64_t)n);  // uniform() leaves the buffered half alone
+  pcg::store(st, rng);
+  return IVHD_OK;
+}
+
+int ivhd_set_graph_sampled(ivhd_ctx* ctx, int slot, const int32_t* nn_ids, int64_t nn_stride, int ncols, int rn,
+                           uint64_t* rng, int32_t* picks_out) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (slot < 0 || slot > 1) return fail(ctx, IVHD_ERR_INVALID_ARG, "slot must be 0 or 1");
+  if (!rng || ncols < 0 || rn < 0 || nn_stride < ncols || (ncols > 0 && !nn_ids))
+    return fail(ctx, IVHD_ERR_INVALID_ARG, "bad graph arguments");
+  const int64_t m = ctx->m, N = m * rn;
+  if (m <= (int64_t)ncols + rn)
+    return fail(ctx, IVHD_ERR_INVALID_ARG, "M=%lld too small for nn=%d plus rn=%d", (long long)m, ncols, rn);
+  CU(ctx, cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  pcg::State gs = pcg::load(rng);
+  const uint32_t mu = (uint32_t)m;
+  const uint32_t thr = (uint32_t)(((1ull << 32) - (uint64_t)m) % (uint64_t)m);
+  int32_t *d_nn = nullptr, *d_rn = nullptr, *val = nullptr, *ok = nullptr, *pos = nullptr;
+  uint8_t* ok8 = nullptr;
+  int64_t *d_last = nullptr, *d_idx = nullptr;
+  cudaError_t e = cudaSuccess;
+  int rc = IVHD_OK;
+  do {
+    if (ncols > 0) {
+      if ((e = dalloc(ctx, &d_nn, sizeof(int32_t) * m * nn_stride)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(d_nn, nn_ids, sizeof(int32_t) * m * nn_stride, cudaMemcpyHostToDevice, st)) !=
+          cudaSuccess) break;
+    }
+    if (N == 0) break;
+    if ((e = dalloc(ctx, &d_rn, sizeof(int32_t) * N)) != cudaSuccess) break;
+    if ((e = dalloc(ctx, &d_last, sizeof(int64_t))) != cudaSuccess) break;
+    // first batch: the first N accepted Lemire draws of the stream
+    int64_t n_cand = N + N / 32 + 1024, consumed = 0;
+    for (;;) {
+      if (n_cand >= (1ll << 31)) { e = cudaErrorInvalidValue; break; }
+      dfree(ctx, val); dfree(ctx, ok8); dfree(ctx, ok); dfree(ctx, pos);
+      val = nullptr; ok8 = nullptr; ok = nullptr; pos = nullptr;
+      if ((e = dalloc(ctx, &val, sizeof(int32_t) * n_cand)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &ok8, n_cand)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &ok, sizeof(int32_t) * n_cand)) != cudaSuccess) break;
+      if ((e = dalloc(ctx, &pos, sizeof(int32_t) * n_cand)) != cudaSuccess) break;
+      const int64_t outs = (n_cand + 1) / 2 + 1;
+      pcg::k_lemire_candidates<<<grid_for((outs + pcg::kChunk - 1) / pcg::kChunk, ctx->sm_count), 256, 0, st>>>(
+          rng[0], rng[1], rng[2], rng[3], gs.has, gs.ub, n_cand, mu, thr, val, ok8);
+      k_u8_to_i32<<<grid_for(n_cand, ctx->sm_count), 256, 0, st>>>(ok8, n_cand, ok);
+      if ((e = scan_flags(ctx, ok, pos, n_cand)) != cudaSuccess) break;
+      int32_t got = 0;
+      if ((e = cudaMemcpyAsync(&got, pos + n_cand - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        break;
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+      if (got >= N) {
+        k_accept_scatter<<<grid_for(n_cand, ctx->sm_count), 256, 0, st>>>(val, ok, pos, n_cand, N, d_rn, d_last);
+        int64_t last = 0;
+        if ((e = cudaMemcpyAsync(&last, d_last, sizeof(int64_t), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+        consumed = last + 1;
+        break;
+      }
+      n_cand *= 2;
+    }
+    if (e != cudaSuccess) break;
+    // generator state after `consumed` 32-bit draws
+    {
+      const int64_t c64 = consumed - (gs.has ? 1 : 0);  // draws taken from fresh 64-bit outputs
+      const int64_t outs = (c64 + 1) / 2;
+      gs.s = pcg::advance(gs.s, gs.inc, (uint64_t)outs);
+      gs.has = (int)(c64 & 1);
+      if (outs > 0) gs.ub = (uint32_t)(pcg::output(gs.s) >> 32);  // last high half drawn
+    }
+    // picks that hit their own row or an nn id are re-drawn in row-major order
+    // from the continued stream until none is left (engine.py:141-146)
+    {
+      uint8_t* bad8 = ok8;  // reuse (n_cand >= N)
+      pcg::k_pick_collisions<<<grid_for(N, ctx->sm_count), 256, 0, st>>>(d_rn, m, rn, d_nn, nn_stride, ncols, bad8);
+      k_u8_to_i32<<<grid_for(N, ctx->sm_count), 256, 0, st>>>(bad8, N, ok);
+      if ((e = scan_flags(ctx, ok, pos, N)) != cudaSuccess) break;
+      int32_t n_bad = 0;
+      if ((e = cudaMemcpyAsync(&n_bad, pos + N - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        break;
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+      if (n_bad > 0) {
+        if ((e = dalloc(ctx, &d_idx, sizeof(int64_t) * n_bad)) != cudaSuccess) break;
+        k_flag_to_index<<<grid_for(N, ctx->sm_count), 256, 0, st>>>(ok, pos, N, d_idx);
+        std::vector<int64_t> idx(n_bad);
+        if ((e = cudaMemcpyAsync(idx.data(), d_idx, sizeof(int64_t) * n_bad, cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+        std::vector<int64_t> fix_idx;
+        std::vector<int32_t> fix_val;
+        std::vector<int64_t> cur = idx;
+        while (!cur.empty()) {
+          std::vector<int64_t> next;
+          for (int64_t k : cur) {
+            const int32_t v = (int32_t)pcg::bounded(gs, mu, thr);
+            const int64_t row = k / rn;
+            bool b = v == (int32_t)row;
+            for (int c = 0; c < ncols; ++c) b |= v == nn_ids[row * nn_stride + c];
+            fix_idx.push_back(k);
+            fix_val.push_back(v);
+            if (b) next.push_back(k);
+          }
+          cur.swap(next);
+        }
+        // later writes win: apply in order
+        int64_t* d_fi = nullptr;
+        int32_t* d_fv = nullptr;
+        const int64_t nf = (int64_t)fix_idx.size();
+        if ((e = dalloc(ctx, &d_fi, sizeof(int64_t) * nf)) != cudaSuccess) break;
+        if ((e = dalloc(ctx, &d_fv, sizeof(int32_t) * nf)) != cudaSuccess) { dfree(ctx, d_fi); break; }
+        e = cudaMemcpyAsync(d_fi, fix_idx.data(), sizeof(int64_t) * nf, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(d_fv, fix_val.data(), sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) {
+          k_scatter_i32<<<1, 1, 0, st>>>(d_fi, d_fv, nf, d_rn);  // one thread: sequential, last write wins
+          e = cudaStreamSynchronize(st);  // host vectors die at scope end
+        }
+        dfree(ctx, d_fi); dfree(ctx, d_fv);
+        if (e != cudaSuccess) break;
+      }
+    }
+    if (picks_out) {
+      if ((e = cudaMemcpyAsync(picks_out, d_rn, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        break;
+    }
+    e = cudaGetLastError();
+  } while (0);
+  if (e != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "random-neighbor sampling: %s", cudaGetErrorString(e));
+  else rc = graph_from_device(ctx, slot, d_nn, nn_stride, ncols, d_rn, rn);
+  if (rc == IVHD_OK && picks_out) {
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (e2 != cudaSuccess) rc = fail(ctx, IVHD_ERR_CUDA, "random-neighbor sampling: %s", cudaGetErrorString(e2));
+  }
+  if (rc == IVHD_OK) pcg::store(gs, rng);
+  dfree(ctx, d_nn); dfree(ctx, d_rn); dfree(ctx, val); dfree(ctx, ok8); dfree(ctx, ok); dfree(ctx, pos);
+  dfree(ctx, d_last); dfree(ctx, d_idx);
   return rc;
 }
 

@@ -11,8 +11,34 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import c_f64p, c_i32p, c_i64p, c_u8p, check, f64, i32, ptr
+from ._lib import c_f64p, c_i32p, c_i64p, c_u8p, c_u64p, check, f64, i32, ptr
 from .errors import InvalidArgumentError
+
+
+_M64 = (1 << 64) - 1
+
+
+def is_pcg64(gen):
+    return type(getattr(gen, "bit_generator", None)).__name__ == "PCG64"
+
+
+def pcg_state(gen):
+    """numpy PCG64 state as the C ABI's rng[6] words."""
+    if not is_pcg64(gen):
+        raise InvalidArgumentError("device draws need a numpy Generator backed by PCG64")
+    st = gen.bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    return np.array([s >> 64, s & _M64, inc >> 64, inc & _M64, int(st["has_uint32"]), int(st["uinteger"])],
+                    dtype=np.uint64)
+
+
+def pcg_store(gen, words):
+    st = gen.bit_generator.state
+    st["state"]["state"] = (int(words[0]) << 64) | int(words[1])
+    st["state"]["inc"] = (int(words[2]) << 64) | int(words[3])
+    st["has_uint32"] = int(words[4])
+    st["uinteger"] = int(words[5])
+    gen.bit_generator.state = st
 
 
 class DeviceEmbedding:
@@ -46,9 +72,7 @@ class DeviceEmbedding:
         check(code, self.h)
 
     # ---------------------------------------------------------- connections
-    def set_graph(self, slot, nn_sets, rn_assign):
-        """Binary-mode connections: nn (M, ncols) view (row stride honoured)
-        and rn (M, rn).  engine.py:225-262."""
+    def _nn_view(self, nn_sets):
         nn = np.asarray(nn_sets)
         if nn.ndim != 2 or nn.shape[0] != self.m:
             raise InvalidArgumentError("nn_sets must be (M, ncols)")
@@ -57,11 +81,39 @@ class DeviceEmbedding:
         if base.strides[0] % 4 or stride < base.shape[1]:
             base = i32(nn)
             stride = base.shape[1]
+        return base, stride
+
+    def set_graph(self, slot, nn_sets, rn_assign):
+        """Binary-mode connections: nn (M, ncols) view (row stride honoured)
+        and rn (M, rn).  engine.py:225-262."""
+        base, stride = self._nn_view(nn_sets)
         rn = i32(rn_assign)
         self._check(self.lib.ivhd_set_graph(
             self.h, int(slot), base.ctypes.data_as(c_i32p) if base.size else None, int(stride),
             int(base.shape[1]), rn.ctypes.data_as(c_i32p) if rn.size else None,
             int(rn.shape[1]) if rn.ndim == 2 else 0))
+
+    def set_graph_sampled(self, slot, nn_sets, rn, gen):
+        """Draw rn random partners per vertex on the device from the numpy
+        Generator `gen` (PCG64) exactly as sample_random_neighbors would
+        (engine.py:132-146), advance `gen` accordingly, and build the binary
+        connection set.  Returns the (M, rn) int32 partners."""
+        base, stride = self._nn_view(nn_sets)
+        st = pcg_state(gen)
+        picks = np.empty((self.m, int(rn)), dtype=np.int32)
+        self._check(self.lib.ivhd_set_graph_sampled(
+            self.h, int(slot), base.ctypes.data_as(c_i32p) if base.size else None, int(stride),
+            int(base.shape[1]), int(rn), st.ctypes.data_as(c_u64p),
+            picks.ctypes.data_as(c_i32p) if picks.size else None))
+        pcg_store(gen, st)
+        return picks
+
+    def init_positions(self, gen, low=-1.0, high=1.0):
+        """positions = gen.uniform(low, high, (M, dim)) drawn on the device
+        (engine.py:124-129); `gen` (PCG64) is advanced accordingly."""
+        st = pcg_state(gen)
+        self._check(self.lib.ivhd_init_positions(self.h, st.ctypes.data_as(c_u64p), float(low), float(high)))
+        pcg_store(gen, st)
 
     def set_connections(self, slot, edges, is_random, targets=None, scale=None):
         e = i32(edges).reshape(-1, 2)

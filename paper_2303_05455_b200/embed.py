@@ -19,7 +19,7 @@ import numpy as np
 
 from .config import EmbeddingConfig, coerce_config, resolve_optimizer
 from .config import OPTIMIZER_KINDS
-from .device import DeviceEmbedding
+from .device import DeviceEmbedding, is_pcg64
 from .errors import (DimensionMismatchError, InvalidArgumentError,
                      NumericalDivergenceError)
 
@@ -226,16 +226,37 @@ class _Session:
                 raise InvalidArgumentError(
                     "euclidean mode needs the dataset to measure random-pair targets")
 
-        # one PCG64 stream, reference order (engine.py:165, 214-215)
-        self.y0 = init_layout(m, config.target_dim, self.rng)
-        self.rn = sample_random_neighbors(m, self.nn_sets, config.rn, self.rng)
         self.c = config.c
         self.target_scale = None
+        self.dim = config.target_dim
+        if m <= self.nn_sets.shape[1] + config.rn:
+            raise InvalidArgumentError(f"M={m} too small for nn={self.nn_sets.shape[1]} plus rn={config.rn}")
 
         self.dev = DeviceEmbedding(m, config.target_dim, device=device)
         self.dev.set_optimizer(resolve_optimizer(config.optimizer, m, config.integrator, config.opt))
-        self.dev.set_positions(self.y0)
-        self._upload_connections()
+        # one PCG64 stream, reference order (engine.py:165, 214-215): the
+        # layout, then the random partners — drawn on the device (numpy's
+        # PCG64 reproduced bit for bit; the host Generator is advanced to match)
+        self.device_rng = is_pcg64(self.rng)
+        self._y0 = None
+        if self.device_rng:
+            self._y0_state = self.rng.bit_generator.state
+            self.dev.init_positions(self.rng)
+        else:
+            self._y0 = init_layout(m, config.target_dim, self.rng)
+            self.dev.set_positions(self._y0)
+        self.rn = None
+        self._upload_connections(sample=True)
+
+    @property
+    def y0(self):
+        """The initial layout (host copy, replayed from the saved generator
+        state when the device drew it)."""
+        if self._y0 is None:
+            g = np.random.Generator(np.random.PCG64())
+            g.bit_generator.state = self._y0_state
+            self._y0 = init_layout(self.m, self.dim, g)
+        return self._y0
 
     # connection sets ------------------------------------------------------
     def _targets(self):
@@ -262,11 +283,18 @@ class _Session:
                                     self.rn.reshape(-1).astype(np.int32)])
         return nn_edges, rn_edges
 
-    def _upload_connections(self):
+    def _upload_connections(self, sample=False):
         self.filtered_ready = False
         if not self.euclid:
+            if sample and self.device_rng:
+                self.rn = self.dev.set_graph_sampled(0, self.nn_sets, self.config.rn, self.rng)
+                return
+            if sample:
+                self.rn = sample_random_neighbors(self.m, self.nn_sets, self.config.rn, self.rng)
             self.dev.set_graph(0, self.nn_sets, self.rn)
             return
+        if sample:
+            self.rn = sample_random_neighbors(self.m, self.nn_sets, self.config.rn, self.rng)
         nn_t, rn_t = self._targets()
         nn_edges, rn_edges = self._edge_arrays()
         self.dev.set_connections(
@@ -297,8 +325,7 @@ class _Session:
 
     def resample(self):
         """engine.py:264-268: new random partners from the same stream."""
-        self.rn = sample_random_neighbors(self.m, self.nn_sets, self.config.rn, self.rng)
-        self._upload_connections()
+        self._upload_connections(sample=True)
 
     def set_optimizer(self, kind):
         self.config.optimizer = kind
@@ -361,8 +388,7 @@ def run_embedding(graph=None, config=None, dataset=None, helper_graph=None, obse
     l1_from = total - config.l1_final_steps if config.l1_final_steps > 0 else None
     rnn_from = total - config.rnn_final_steps if config.rnn_final_steps > 0 else None
     period = config.rn_resample_period
-    state = EmbeddingState(positions=sess.y0, deltas=np.zeros_like(sess.y0),
-                           rn_assignments=sess.rn, iteration=0)
+    state = EmbeddingState(positions=None, deltas=None, rn_assignments=sess.rn, iteration=0)
 
     def diverged(it0, stress, done):
         state.positions = dev.positions()
@@ -432,8 +458,7 @@ def run_embedding(graph=None, config=None, dataset=None, helper_graph=None, obse
     positions = dev.positions() if ran else sess.y0.copy()
     state.positions = positions
     state.rn_assignments = sess.rn
-    if ran:
-        state.deltas = dev.deltas()
+    state.deltas = dev.deltas() if ran else np.zeros((sess.m, sess.dim))
     if total == 0 or state.stress != state.stress:
         state.stress = dev.stress(0, "l2", sess.c, positions)
     dev.close()

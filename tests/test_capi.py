@@ -36,7 +36,9 @@ def test_header_and_binding_agree():
 def test_library_exports_every_declared_symbol(lib):
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.ivhd_abi_version() == 1
+    from paper_2303_05455_b200._lib import ABI_VERSION
+    assert lib.ivhd_abi_version() == ABI_VERSION
+    assert f"#define IVHD_ABI_VERSION {ABI_VERSION}" in open(HEADER).read()
 
 
 def test_library_is_sm100a():
