@@ -101,6 +101,26 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        # NVML from a thread (10 ms period) so short timed regions still get
+        # many samples; nvidia-smi -lms as the fallback
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            try:
+                import torch
+
+                bus = torch.cuda.get_device_properties(self.index).pci_bus_id
+                h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv, self.h = nv, h
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -112,6 +132,20 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self.nv
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+            except Exception:
+                pass
+            self.stop.wait(0.01)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -119,6 +153,9 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def __exit__(self, *exc):
+        if getattr(self, "nv", None) is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -136,6 +173,23 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the step kernel from the newest committed
+    `ncu --set full` summary (profiles/r*_step_kernel_ncu.json, written by
+    tools/ncu_to_profile.py); None if there is none."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_step_kernel_ncu.json")))
+    if not files:
+        return None
+    try:
+        d = json.load(open(files[-1]))
+        return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": "profiles/" + os.path.basename(files[-1]),
+                "note": "dram__bytes_read.sum + dram__bytes_write.sum, one C3 launch under ncu (cold caches)"}
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -352,7 +406,9 @@ def gpu_arm(args, w):
                              f"{(nbytes + 8 * m) / 1e6:.0f} MB/iteration may stay L2-resident within a step"},
             "s_per_embed": tot / args.steps, "it_per_s": 1.0 / s_iter,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": (ncu_traffic() or {}).get("bytes_per_launch"),
+                         "traffic_source": (ncu_traffic() or {}).get("source"),
+                         "algorithmic_bytes_per_launch": nbytes,
                          "note": f"algorithmic bytes {nbytes} per iteration (8L+36M) / device time "
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
             "cpu_baseline": cpu, "e2e": e2e,
