@@ -1508,7 +1508,7 @@ int ivhd_restore(ivhd_ctx* ctx) {
 
 #ifdef IVHD_TIMELINE
 int ivhd_timeline_dump(long long* out) {
-  return cudaMemcpyFromSymbol(out, ivhd::g_tl, sizeof(long long) * 8 * 64 * 6) == cudaSuccess ? 0 : 2;
+  return cudaMemcpyFromSymbol(out, ivhd::g_tl, sizeof(ivhd::g_tl)) == cudaSuccess ? 0 : 2;
 }
 #endif
 

@@ -34,8 +34,25 @@
 namespace ivhd {
 
 #ifdef IVHD_TIMELINE
-// per-unit phase timestamps of a few blocks: [block][unit][phase]
-__device__ long long g_tl[8][64][6];
+// Debug build only: %globaltimer stamps of iterations 10 and 11, per block:
+// [0] entry, [1] after the dependency wait, [2+k] consumer warp 0 done with
+// unit k (k < 34), [36] all warps done, [37] arrival, [38] warp 0 loop end,
+// [39] finalize end (last block only).
+constexpr int kTlBlocks = 1024, kTlSlots = 40;
+__device__ long long g_tl[2][kTlBlocks][kTlSlots];
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define IVHD_TL(slot)                                                                      \
+  do {                                                                                     \
+    if (tl_rec && lane == 0 && warp == 0 && blockIdx.x < kTlBlocks) tl_rec[(slot)] = gtime(); \
+  } while (0)
+#else
+#define IVHD_TL(slot) \
+  do {                \
+  } while (0)
 #endif
 
 
@@ -301,6 +318,41 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double4* sm /*[kBlock/3
   return r;  // valid in thread 0
 }
 
+// The iteration decision from the reduced partials {stress, sum|dnew|^2,
+// sum|dold|^2, #non-finite} (optim.py:80-92 + engine.py:373-384); one thread.
+template <int OPT>
+__device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
+  Ctrl* ctrl = A.ctrl;
+  const double E = 0.5 * s.x;
+  double step = ctrl->step;
+  bool commit = true;
+  if (OPT == OPT_FD && A.h.adapt) {
+    const double dT = s.y - s.z;
+    if (dT > A.h.tau) {
+      step *= (double)A.h.g2;
+      commit = false;
+    } else if (dT < -A.h.tau) {
+      step *= (double)A.h.g1;
+      commit = false;
+    }
+  }
+  const long long it = ctrl->iter;
+  if (A.trace) A.trace[it] = make_double2(E, step);
+  if (commit && s.w > 0.0) {
+    ctrl->status = 1;
+    ctrl->diverged_at = it;
+  } else {
+    if (commit) ctrl->cur ^= 1;
+    ctrl->last_commit = commit ? 1 : 0;
+    ctrl->step = step;
+    ctrl->iter = it + 1;
+  }
+  ctrl->gstep += 1;
+  if (OPT == OPT_ADAM) ctrl->adam_t += 1;
+  ctrl->next_tile = 0;
+  ctrl->arrive = 0;  // the next launch is ordered after this grid completes
+}
+
 // ---------------------------------------------------------------- finalize
 // Reduce n partials in a fixed order and take the iteration decision
 // (optim.py:80-92 + engine.py:373-384).  Executed by ONE whole block; each
@@ -331,37 +383,36 @@ __device__ void finalize_block(const StepArgs& A, double4* sm, const double4* sr
     }
   }
   s = block_sum4(s, sm);
-  if (threadIdx.x == 0) {
-    const double E = 0.5 * s.x;
-    double step = ctrl->step;
-    bool commit = true;
-    if (OPT == OPT_FD && A.h.adapt) {
-      const double dT = s.y - s.z;
-      if (dT > A.h.tau) {
-        step *= (double)A.h.g2;
-        commit = false;
-      } else if (dT < -A.h.tau) {
-        step *= (double)A.h.g1;
-        commit = false;
+  if (threadIdx.x == 0) decide<OPT>(A, s);
+}
+
+// Fused single-GPU finalizer: ONE warp reduces the n per-block partials
+// (lane l sums l, l+32, ... in order, then a fixed butterfly) and lane 0
+// decides.  The caller (lane 0) has acquired every block's arrival.
+template <int OPT>
+__device__ void finalize_warp(const StepArgs& A, const double4* src, int n) {
+  const int lane = threadIdx.x & 31;
+  const double2* p2 = reinterpret_cast<const double2*>(src);
+  double4 s = make_double4(0, 0, 0, 0);
+  constexpr int kBatch = 8;  // loads in flight per lane (L2, bypassing L1)
+  for (int t0 = lane; t0 < n; t0 += 32 * kBatch) {
+    double2 a[kBatch], b[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int t = t0 + 32 * j;
+      a[j] = b[j] = make_double2(0.0, 0.0);
+      if (t < n) {
+        a[j] = __ldcg(p2 + 2 * t);
+        b[j] = __ldcg(p2 + 2 * t + 1);
       }
     }
-    const long long it = ctrl->iter;
-    if (A.trace) A.trace[it] = make_double2(E, step);
-    if (commit && s.w > 0.0) {
-      ctrl->status = 1;
-      ctrl->diverged_at = it;
-    } else {
-      if (commit) ctrl->cur ^= 1;
-      ctrl->last_commit = commit ? 1 : 0;
-      ctrl->step = step;
-      ctrl->iter = it + 1;
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      s.x += a[j].x; s.y += a[j].y; s.z += b[j].x; s.w += b[j].y;
     }
-    ctrl->gstep += 1;
-    if (OPT == OPT_ADAM) ctrl->adam_t += 1;
-    ctrl->next_tile = 0;
-    __threadfence();
-    ctrl->arrive = 0;
   }
+  s.x = warp_dsum(s.x); s.y = warp_dsum(s.y); s.z = warp_dsum(s.z); s.w = warp_dsum(s.w);
+  if (lane == 0) decide<OPT>(A, s);
 }
 
 template <int SS>
@@ -656,6 +707,10 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
 
   Ctrl* ctrl = A.ctrl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef IVHD_TIMELINE
+  const long long tl_entry = gtime();
+  long long* tl_rec = nullptr;
+#endif
   const int n_units = A.n_tiles;
   const int grid = gridDim.x;
   const int my_units = blockIdx.x < n_units ? (n_units - 1 - blockIdx.x) / grid + 1 : 0;
@@ -771,6 +826,13 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
     // ----------------------------------------------------- consumer warps
     griddep_wait();
     if (ctrl->status != 0) return;  // diverged earlier: later iterations are no-ops
+#ifdef IVHD_TIMELINE
+    if (A.fuse_finalize && (ctrl->iter == 10 || ctrl->iter == 11) && blockIdx.x < kTlBlocks) {
+      tl_rec = g_tl[ctrl->iter - 10][blockIdx.x];
+      if (warp == 0 && lane == 0) tl_rec[0] = tl_entry;
+    }
+    IVHD_TL(1);
+#endif
     const int ycur = ctrl->cur;
     const float c = (float)ctrl->c;
     const float step = (float)ctrl->step;
@@ -939,6 +1001,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
         te += (float)acc_e; tn += (float)acc_n; to += (float)acc_o; tb += (float)acc_bad;
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_e[s]);  // this warp is done with stage s
+        if (k < 34) IVHD_TL(2 + k);
         continue;
       }
       // sharded: per-unit partials (rank-count independent order).  Warp
@@ -974,31 +1037,41 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   }
 
   if (!A.fuse_finalize) return;
+  IVHD_TL(38);
   // block partial: warp sums in a fixed butterfly, then warps in order
   block_sync();
+  IVHD_TL(36);
   if (warp < kConsumerWarps) {
-    double4 v = make_double4(te, tn, to, tb);
-    v.x = warp_dsum(v.x); v.y = warp_dsum(v.y); v.z = warp_dsum(v.z); v.w = warp_dsum(v.w);
-    if (lane == 0) sm_red[warp] = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // fp32 butterfly, then fp64 across warps
+      te += __shfl_xor_sync(0xffffffffu, te, o);
+      tn += __shfl_xor_sync(0xffffffffu, tn, o);
+      to += __shfl_xor_sync(0xffffffffu, to, o);
+      tb += __shfl_xor_sync(0xffffffffu, tb, o);
+    }
+    if (lane == 0) sm_red[warp] = make_double4(te, tn, to, tb);
   }
   block_sync();
-  if (tid == 0) {
+  if (warp != 0) return;
+  // last-block-done: lane 0 publishes the block partial with a release
+  // arrival; the block that arrives last (acquire) reduces and decides
+  int last = 0;
+  if (lane == 0) {
     double4 t = make_double4(0, 0, 0, 0);
 #pragma unroll
     for (int w = 0; w < kConsumerWarps; ++w) {
       t.x += sm_red[w].x; t.y += sm_red[w].y; t.z += sm_red[w].z; t.w += sm_red[w].w;
     }
     A.bpart[blockIdx.x] = t;
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&ctrl->arrive) : "memory");
+    last = old == gridDim.x - 1;
   }
-  // last-block-done: the block that retires last reduces and decides
-  __shared__ bool sm_last;
-  __threadfence();
-  block_sync();
-  if (tid == 0) sm_last = (atomicAdd(&ctrl->arrive, 1u) == gridDim.x - 1);
-  block_sync();
-  if (!sm_last || tid >= kBlock) return;
-  __threadfence();
-  finalize_block<OPT>(A, sm_red, A.bpart, (int)gridDim.x);
+  IVHD_TL(37);
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __syncwarp();
+  finalize_warp<OPT>(A, A.bpart, (int)gridDim.x);
+  IVHD_TL(39);
 }
 
 // Standalone finalizer (sharded mode, after the exchange): one block.
