@@ -450,17 +450,17 @@ template <int DIM, int OPT>
 __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restrict__ Yout, long long v,
                                              const float (&yi)[DIM], float (&sv)[Layout<DIM, OPT>::SS > 0 ? Layout<DIM, OPT>::SS : 1],
                                              const float (&f)[DIM], float step, float bc1, float bc2,
-                                             double& acc_n, double& acc_o, double& acc_bad) {
+                                             float& acc_n, float& acc_o, float& acc_bad) {
   using L = Layout<DIM, OPT>;
   constexpr int V = DIM == 2 ? 2 : 4;
   float yn[DIM];
   if constexpr (OPT == OPT_FD) {
-    double so = 0.0, sn = 0.0;
+    float so = 0.f, sn = 0.f;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       const float dn = fmaf(A.h.a, sv[d], step * f[d]);
-      so += (double)sv[d] * (double)sv[d];
-      sn += (double)dn * (double)dn;
+      so = fmaf(sv[d], sv[d], so);
+      sn = fmaf(dn, dn, sn);
       sv[d] = dn;
       yn[d] = yi[d] + dn;
     }
@@ -507,7 +507,7 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
   } else {
     st_vec<DIM>(Yout + (size_t)v * L::YS, yn);
   }
-  acc_bad += all_finite(yn, DIM) ? 0.0 : 1.0;
+  acc_bad += all_finite(yn, DIM) ? 0.f : 1.f;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -547,14 +547,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
+#ifndef IVHD_WAIT_HINT_NS
+#define IVHD_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
+  if constexpr (IVHD_WAIT_HINT_NS > 0) {  // sleep until the phase flips (or the hint expires)
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "n"(IVHD_WAIT_HINT_NS)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+  }
 }
 // programmatic dependent launch (griddepcontrol): the next iteration's grid
 // may start once every block has signalled; it waits before reading data the
@@ -675,7 +688,9 @@ struct StageMeta {
   int packed;       // unit word: tile << 12 | pass << 7 | min(slots,15) << 3 | log2 G
   int col_off;      // entries skipped at the front of the staged columns (alignment)
   int staged;       // 1 if the unit's columns are in shared memory
-  int pad;
+  int va;           // first vertex of the unit (vertex ids < 2^31)
+  int nv;           // vertices in the unit
+  int pad[3];
 };
 
 // ------------------------------------------------------------------ kernel
@@ -751,6 +766,8 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
         int nv;
         unit_range(packed, va, nv);
         meta[s].packed = packed;
+        meta[s].va = (int)va;
+        meta[s].nv = nv;
         const uint32_t rp_bytes = (uint32_t)((nv + 1) * 4 + 15) / 16 * 16;
         mbar_expect_tx(&bar_r[s], rp_bytes);
         bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_r[s]);
@@ -856,14 +873,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
     const int packed = meta[s].packed;
       const int lgG = packed & 7, G = 1 << lgG;
       const int lg = tid & (G - 1), grp = tid >> lgG;
-      long long va;
-      int nv;
-      {
-        const int tile = packed >> 12, pass = (packed >> 7) & 31;
-        const int groups = kBlock >> lgG;
-        va = (long long)tile * kBlock + (long long)pass * groups;
-        nv = (int)max(0LL, min((long long)groups, A.v_end - va));
-      }
+      const int va = meta[s].va, nv = meta[s].nv;
       const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
       const uint32_t* colst = reinterpret_cast<const uint32_t*>(st + SL::COL_OFF);
       const float* ys = reinterpret_cast<const float*>(st + SL::Y_OFF);
@@ -872,7 +882,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
       const uint32_t e0 = rp[0];
       const int coff = meta[s].col_off;
 
-      double acc_e = 0.0, acc_n = 0.0, acc_o = 0.0, acc_bad = 0.0;
+      float acc_e = 0.f, acc_n = 0.f, acc_o = 0.f, acc_bad = 0.f;
       const bool active = grp < nv;
       if (active) {
         const long long v = va + grp;
@@ -983,7 +993,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
           }
         }
         if (lg == 0) {
-          acc_e = (double)e;
+          acc_e = e;
           if constexpr (OPT == OPT_NONE) {
 #pragma unroll
             for (int d = 0; d < DIM; ++d) A.force_out[(size_t)v * DIM + d] = (double)f[d];
@@ -998,7 +1008,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
       if (A.fuse_finalize) {
         // single GPU: running per-thread sums (fixed vertex order); the block
         // reduces them once after its last unit
-        te += (float)acc_e; tn += (float)acc_n; to += (float)acc_o; tb += (float)acc_bad;
+        te += acc_e; tn += acc_n; to += acc_o; tb += acc_bad;
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_e[s]);  // this warp is done with stage s
         if (k < 34) IVHD_TL(2 + k);
@@ -1007,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
       // sharded: per-unit partials (rank-count independent order).  Warp
       // partial by a fixed butterfly; the warp that completes the unit sums
       // the 8 warp partials in warp order into the unit partial.
-      float pe = (float)acc_e, pn = (float)acc_n, po = (float)acc_o, pb = (float)acc_bad;
+      float pe = acc_e, pn = acc_n, po = acc_o, pb = acc_bad;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         pe += __shfl_xor_sync(0xffffffffu, pe, o);
