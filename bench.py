@@ -107,13 +107,13 @@ class ClockSampler:
             import pynvml as nv
 
             nv.nvmlInit()
-            try:
-                import torch
-
-                bus = torch.cuda.get_device_properties(self.index).pci_bus_id
-                h = nv.nvmlDeviceGetHandleByPciBusId(bus)
-            except Exception:
-                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            idx = self.index  # CUDA ordinal -> NVML index through CUDA_VISIBLE_DEVICES
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            if vis:
+                ids = [v.strip() for v in vis.split(",")]
+                if idx < len(ids) and ids[idx].isdigit():
+                    idx = int(ids[idx])
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
             self.nv, self.h = nv, h
             self.stop = threading.Event()
             self.thread = threading.Thread(target=self._poll, daemon=True)
