@@ -292,7 +292,17 @@ def gpu_arm(args, w):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
+        if world == 1:  # --sharded on one GPU: a one-rank NCCL group
+            import socket
+
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                os.environ.setdefault("MASTER_PORT", str(so.getsockname()[1]))
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nb = make_graph(w, f"cuda:{local}")
     m, L, iters = w["m"], (w["nn"] + w["rn"]) * w["m"], w["iterations"]
@@ -305,7 +315,7 @@ def gpu_arm(args, w):
 
     stream = torch.cuda.Stream(device=local)  # the library launches on this stream
     torch.cuda.set_stream(stream)
-    if world > 1:
+    if sharded:
         from paper_2303_05455_b200.sharded import ShardedEmbedding
 
         dev = ShardedEmbedding(m, 2, rank, world, device=local, stream=stream.cuda_stream)
@@ -401,7 +411,7 @@ def gpu_arm(args, w):
                                    f"nn={w['nn']} rn={w['rn']} c={w['c']} {w['optimizer']}, "
                                    f"{iters} iterations per step",
                        "m": m, "connections": L, "iterations_per_step": iters,
-                       "parallelism": f"vertex-range shards x{world}" if world > 1 else "single GPU",
+                       "parallelism": f"vertex-range shards x{world}" if sharded else "single GPU",
                        "l2": "flushed between steps (256 MB write); working set ~"
                              f"{(nbytes + 8 * m) / 1e6:.0f} MB/iteration may stay L2-resident within a step"},
             "s_per_embed": tot / args.steps, "it_per_s": 1.0 / s_iter,
@@ -412,11 +422,11 @@ def gpu_arm(args, w):
                          "note": f"algorithmic bytes {nbytes} per iteration (8L+36M) / device time "
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * iters, "clocks": clk.summary(),
+            "gpu_launches": args.steps * iters * (2 if sharded else 1), "clocks": clk.summary(),
             "final_stress_e2e": final_stress,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 
@@ -431,6 +441,8 @@ def main():
     ap.add_argument("--iterations", type=int, default=None, help="override (profiling)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU (sharded, NCCL) loop even on one GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-iters", type=int, default=4, help="reference arm: iterations per step")

@@ -153,6 +153,22 @@ int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c);
 int ivhd_step_finalize(ivhd_ctx* ctx, double* stress_out, double* step_out,
                        int* committed_out);
 
+/* Asynchronous sharded loop (no host round trip per iteration; the caller
+ * all-gathers between step and finalize on the context's stream):
+ *   ivhd_shard_begin(ctx, slot, c, n, &cur, &ep) once per segment (syncs; cur =
+ *                                                current buffer index; ep changes
+ *                                                when captured launches go stale)
+ *   n times: ivhd_shard_step(ctx, slot, norm, &buf)   local update -> buf
+ *            <all-gather buf slices and the unit partials>
+ *            ivhd_shard_finalize(ctx)                decision on the device
+ *   ivhd_shard_end(ctx, stress[n], step[n], &done)   syncs; DIVERGED like ivhd_run
+ * buf (device pointer, m_cap*floats_per_vertex floats) alternates by parity. */
+int ivhd_shard_begin(ivhd_ctx* ctx, int slot, double c, int64_t n_iter, int* cur_out,
+                     int64_t* epoch_out);
+int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out);
+int ivhd_shard_finalize(ivhd_ctx* ctx);
+int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out);
+
 #ifdef __cplusplus
 }
 #endif

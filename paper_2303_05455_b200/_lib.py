@@ -51,6 +51,11 @@ SIGNATURES = {
     "ivhd_init_positions": (ctypes.c_int, [ctypes.c_void_p, c_u64p, ctypes.c_double, ctypes.c_double]),
     "ivhd_set_graph_sampled": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, ctypes.c_int64,
                                               ctypes.c_int, ctypes.c_int, c_u64p, c_i32p]),
+    "ivhd_shard_begin": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
+                                        ctypes.POINTER(ctypes.c_int), c_i64p]),
+    "ivhd_shard_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_u64p]),
+    "ivhd_shard_finalize": (ctypes.c_int, [ctypes.c_void_p]),
+    "ivhd_shard_end": (ctypes.c_int, [ctypes.c_void_p, c_f64p, c_f64p, c_i64p]),
     "ivhd_set_connections": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, c_u8p, c_f64p,
                                             c_f64p, ctypes.c_int64]),
     "ivhd_set_positions": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),

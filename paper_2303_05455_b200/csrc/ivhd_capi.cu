@@ -104,6 +104,9 @@ struct ivhd_ctx {
 
   int64_t shard_begin = 0, shard_end = 0;  // sharded mode range (0,0 = whole)
   bool sharded = false;
+  int shard_cur = 0;    // async sharded loop: host-side copy of the current buffer index
+  int shard_slot = 0;   // connection slot of the last ivhd_shard_step
+  int64_t graph_epoch = 0;  // bumped whenever captured launch arguments go stale
 
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int graph_chunk = 64;
@@ -482,6 +485,7 @@ int ensure_slot(ivhd_ctx* ctx, CsrSlot& s, int64_t n, bool weighted) {
 void drop_graphs(ivhd_ctx* ctx) {
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
   ctx->graphs.clear();
+  ++ctx->graph_epoch;  // callers' own captures (sharded loop) must be redone too
 }
 
 int ys_now(ivhd_ctx* ctx);
@@ -1569,13 +1573,14 @@ int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c) {
   StepArgs A = make_args(ctx, slot, norm, 0);
   const CsrSlot& S = ctx->slots[slot];
   if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
+  ctx->shard_slot = slot;
   return IVHD_OK;
 }
 
 int ivhd_step_finalize(ivhd_ctx* ctx, double* stress_out, double* step_out, int* committed_out) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
   CU(ctx, cudaSetDevice(ctx->device));
-  StepArgs A = make_args(ctx, 0, 0, 0);
+  StepArgs A = make_args(ctx, ctx->shard_slot, 0, 0);
   pick_finalize(ctx->opt.kind)<<<1, kBlock, 0, ctx->stream>>>(A);
   CU(ctx, cudaGetLastError());
   TRY(pull_ctrl(ctx));
@@ -1585,6 +1590,87 @@ int ivhd_step_finalize(ivhd_ctx* ctx, double* stress_out, double* step_out, int*
   if (step_out) *step_out = tr.y;
   if (committed_out) *committed_out = ctx->ctrl_h->last_commit;
   if (ctx->ctrl_h->status != 0) return fail(ctx, IVHD_ERR_DIVERGED, "embedding diverged");
+  return IVHD_OK;
+}
+
+// ---- asynchronous sharded loop: no host round trip per iteration.  The
+// host picks the buffers by parity (read ybuf[cur], write ybuf[cur^1]); the
+// finalizer makes the written buffer current (refilling it on a rollback),
+// so the exchange buffer of every iteration is known without reading ctrl.
+
+int ivhd_shard_begin(ivhd_ctx* ctx, int slot, double c, int64_t n_iter, int* cur_out, int64_t* epoch_out) {
+  TRY(check_ready(ctx, slot));
+  if (!ctx->sharded) return fail(ctx, IVHD_ERR_STATE, "call ivhd_shard_set_range first");
+  if (!ctx->pos_set) return fail(ctx, IVHD_ERR_STATE, "positions not set");
+  if (n_iter < 0) return fail(ctx, IVHD_ERR_INVALID_ARG, "n_iter must be >= 0");
+  TRY(ensure_trace(ctx, std::max<int64_t>(n_iter, 1)));
+  TRY(pull_ctrl(ctx));
+  if (ctx->ctrl_h->status != 0) return fail(ctx, IVHD_ERR_DIVERGED, "context already diverged");
+  ctx->ctrl_h->c = c;
+  ctx->ctrl_h->iter = 0;
+  ctx->ctrl_h->arrive = 0;
+  ctx->ctrl_h->next_tile = 0;
+  TRY(push_ctrl(ctx));
+  ctx->shard_cur = ctx->ctrl_h->cur;
+  ctx->shard_slot = slot;
+  if (cur_out) *cur_out = ctx->shard_cur;
+  if (epoch_out) *epoch_out = ctx->graph_epoch;
+  return IVHD_OK;
+}
+
+static void shard_io(ivhd_ctx* ctx, StepArgs& A) {
+  A.fixed_io = 1;
+  A.ybuf0 = ctx->ybuf[ctx->shard_cur];
+  A.ybuf1 = ctx->ybuf[ctx->shard_cur ^ 1];
+  A.out_index = ctx->shard_cur ^ 1;
+  A.v_cap_floats = ctx->v_cap * ys_of(ctx->dim, ctx->opt.kind);
+}
+
+int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (slot < 0 || slot > 1 || !ctx->slots[slot].valid) return fail(ctx, IVHD_ERR_STATE, "connection slot %d not set", slot);
+  if (norm != IVHD_NORM_L2 && norm != IVHD_NORM_L1) return fail(ctx, IVHD_ERR_INVALID_ARG, "unknown norm %d", norm);
+  if (!ctx->sharded) return fail(ctx, IVHD_ERR_STATE, "call ivhd_shard_set_range first");
+  CU(ctx, cudaSetDevice(ctx->device));
+  StepArgs A = make_args(ctx, slot, norm, 0);
+  shard_io(ctx, A);
+  const CsrSlot& S = ctx->slots[slot];
+  if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
+  ctx->shard_slot = slot;
+  if (exchange_out) *exchange_out = reinterpret_cast<uint64_t>(ctx->ybuf[ctx->shard_cur ^ 1]);
+  return IVHD_OK;
+}
+
+int ivhd_shard_finalize(ivhd_ctx* ctx) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  StepArgs A = make_args(ctx, ctx->shard_slot, 0, 0);
+  shard_io(ctx, A);
+  pick_finalize(ctx->opt.kind)<<<1, kBlock, 0, ctx->stream>>>(A);
+  CU(ctx, cudaGetLastError());
+  ctx->shard_cur ^= 1;
+  return IVHD_OK;
+}
+
+int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  const Ctrl& C = *ctx->ctrl_h;
+  const bool diverged = C.status != 0;
+  const int64_t done = diverged ? C.diverged_at : C.iter;
+  const int64_t ntr = diverged ? done + 1 : done;
+  if (ntr > 0 && (stress_out || step_out)) {
+    std::vector<double2> tr(ntr);
+    CU(ctx, cudaMemcpy(tr.data(), ctx->trace, sizeof(double2) * ntr, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < ntr; ++i) {
+      if (stress_out) stress_out[i] = tr[i].x;
+      if (step_out) step_out[i] = tr[i].y;
+    }
+  }
+  if (done_out) *done_out = done;
+  ctx->shard_cur = C.cur;
+  if (diverged) return fail(ctx, IVHD_ERR_DIVERGED, "embedding diverged at local iteration %lld", (long long)done);
   return IVHD_OK;
 }
 

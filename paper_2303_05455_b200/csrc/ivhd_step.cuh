@@ -120,6 +120,9 @@ struct StepArgs {
   int n_tiles_global;     // work-unit partials reduced by the finalizer
   int norm;               // 0 = L2, 1 = L1
   int fuse_finalize;      // last block reduces + decides (single GPU)
+  int fixed_io;           // sharded async mode: read ybuf0, write ybuf1 (host-chosen parity)
+  int out_index;          // fixed_io: which context buffer ybuf1 is (becomes ctrl->cur)
+  long long v_cap_floats; // fixed_io: floats per position buffer (rollback copy)
   Hyper h;
 };
 
@@ -342,7 +345,8 @@ __device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
     ctrl->status = 1;
     ctrl->diverged_at = it;
   } else {
-    if (commit) ctrl->cur ^= 1;
+    if (A.fixed_io) ctrl->cur = A.out_index;  // the rollback copy (finalize_kernel) refills it
+    else if (commit) ctrl->cur ^= 1;
     ctrl->last_commit = commit ? 1 : 0;
     ctrl->step = step;
     ctrl->iter = it + 1;
@@ -816,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
       if (ctrl->status != 0) {  // diverged earlier: drain the prefetch and leave
         for (int k = 0; k < pre; ++k) mbar_wait(&bar_b[k], 0);
       } else {
-        const float* Yin = ctrl->cur ? A.ybuf1 : A.ybuf0;
+        const float* Yin = (A.fixed_io || !ctrl->cur) ? A.ybuf0 : A.ybuf1;
         for (int k = 0; k < pre; ++k) issue_ys(k, Yin);
         // Event loop: stages are claimed as consumers free them; a unit's
         // columns are requested the moment its row pointers land.
@@ -850,7 +854,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
     }
     IVHD_TL(1);
 #endif
-    const int ycur = ctrl->cur;
+    const int ycur = A.fixed_io ? 0 : ctrl->cur;
     const float c = (float)ctrl->c;
     const float step = (float)ctrl->step;
     const long long gstep = ctrl->gstep;
@@ -1090,6 +1094,16 @@ __global__ void __launch_bounds__(kBlock) finalize_kernel(StepArgs A) {
   __shared__ double4 sm_red[kBlock / 32];
   if (A.ctrl->status != 0) return;
   finalize_block<OPT>(A, sm_red, A.partial, A.n_tiles_global);
+  if (!A.fixed_io) return;
+  // async sharded mode: the buffer just written becomes current; after a
+  // rollback (rare) it is refilled with the unchanged positions
+  block_sync();  // CTA-scope ordering after thread 0's decision
+  const volatile Ctrl* vc = A.ctrl;
+  if (vc->status != 0 || vc->last_commit) return;
+  const float4* src = reinterpret_cast<const float4*>(A.ybuf0);
+  float4* dst = reinterpret_cast<float4*>(A.ybuf1);
+  const long long n4 = (A.v_cap_floats + 3) / 4;
+  for (long long i = threadIdx.x; i < n4; i += kBlock) dst[i] = src[i];
 }
 
 }  // namespace ivhd

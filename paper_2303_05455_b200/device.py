@@ -222,5 +222,37 @@ class DeviceEmbedding:
         self._check(code)
         return e.value, s.value, bool(com.value), False
 
+    # asynchronous sharded loop (include/ivhd_b200.h, ivhd_shard_*)
+    def shard_begin(self, slot, c, n_iter):
+        """Returns (index of the buffer holding the current positions, graph
+        epoch — changes whenever previously captured launches went stale)."""
+        self._n_shard = int(n_iter)
+        cur, ep = ctypes.c_int(), ctypes.c_int64()
+        self._check(self.lib.ivhd_shard_begin(self.h, int(slot), float(c), int(n_iter), ctypes.byref(cur),
+                                              ctypes.byref(ep)))
+        return cur.value, ep.value
+
+    def shard_step(self, slot, norm):
+        """Queue the local update; returns the device pointer of the buffer
+        to all-gather (no host synchronisation)."""
+        ptr_ = ctypes.c_uint64()
+        self._check(self.lib.ivhd_shard_step(self.h, int(slot), _lib.NORM[norm], ctypes.byref(ptr_)))
+        return ptr_.value
+
+    def shard_finalize(self):
+        self._check(self.lib.ivhd_shard_finalize(self.h))
+
+    def shard_end(self):
+        n = max(self._n_shard, 1)
+        stress, step = np.empty(n), np.empty(n)
+        done = ctypes.c_int64(0)
+        code = self.lib.ivhd_shard_end(self.h, stress.ctypes.data_as(c_f64p), step.ctypes.data_as(c_f64p),
+                                       ctypes.byref(done))
+        if code == _lib.ERR_DIVERGED:
+            d = done.value
+            return stress[: d + 1], step[: d + 1], d, True
+        self._check(code)
+        return stress[: done.value], step[: done.value], done.value, False
+
 
 __all__ = ["DeviceEmbedding", "c_i64p", "c_u8p"]

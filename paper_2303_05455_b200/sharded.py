@@ -47,21 +47,31 @@ class _CudaArray:
 class DeviceShardBackend:
     """The real backend: one DeviceEmbedding (C ABI) per rank."""
 
-    def __init__(self, dev):
+    def __init__(self, dev, stream=0):
         self.dev = dev
+        self.stream = int(stream)
 
     def __getattr__(self, name):
         return getattr(self.dev, name)
 
-    def exchange_views(self):
+    def _views(self, yptr=None):
         import torch
 
-        b = self.dev.shard_buffers()
-        tile_v, n_tiles = self.dev.tiles()
-        n_floats = n_tiles * tile_v * b["floats_per_vertex"]
-        ynext = torch.as_tensor(_CudaArray(b["ybuf"][1 - b["cur"]], n_floats, "<f4"), device="cuda")
-        parts = torch.as_tensor(_CudaArray(b["partials"], n_tiles * 4, "<f8"), device="cuda")
+        if not hasattr(self, "_layout"):
+            b = self.dev.shard_buffers()
+            tile_v, n_tiles = self.dev.tiles()
+            self._layout = (b, n_tiles * tile_v * b["floats_per_vertex"], n_tiles)
+        b, n_floats, n_tiles = self._layout
+        if yptr is None:  # synchronous path: the buffer the step wrote
+            cur = self.dev.shard_buffers()["cur"]
+            yptr = b["ybuf"][1 - cur]
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ynext = torch.as_tensor(_CudaArray(yptr, n_floats, "<f4"), device=dev)
+        parts = torch.as_tensor(_CudaArray(b["partials"], n_tiles * 4, "<f8"), device=dev)
         return ynext, parts
+
+    def exchange_views(self, yptr=None):
+        return self._views(yptr)
 
 
 def _allgather_inplace(buf, rank, world, group=None):
@@ -72,7 +82,8 @@ def _allgather_inplace(buf, rank, world, group=None):
     chunk = buf.numel() // world
     mine = buf[rank * chunk:(rank + 1) * chunk]
     if buf.is_cuda:
-        dist.all_gather_into_tensor(buf, mine.clone(), group=group)
+        # NCCL runs in place when sendbuff == recvbuff + rank * count: no copy
+        dist.all_gather_into_tensor(buf, mine, group=group)
     else:
         parts = [torch.empty_like(mine) for _ in range(world)]
         dist.all_gather(parts, mine.clone(), group=group)
@@ -87,8 +98,9 @@ class ShardedEmbedding:
         if backend is None:
             from .device import DeviceEmbedding
 
-            backend = DeviceShardBackend(DeviceEmbedding(m, dim, device=device, stream=stream))
+            backend = DeviceShardBackend(DeviceEmbedding(m, dim, device=device, stream=stream), stream)
         self.backend = backend
+        self._graphs = {}
         self.m, self.dim, self.rank, self.world, self.group = int(m), int(dim), int(rank), int(world), group
         tile_v, n_tiles_cap = backend.tiles()
         self.ranges = shard_ranges(n_tiles_cap, tile_v, self.world)
@@ -118,20 +130,80 @@ class ShardedEmbedding:
         self.backend.restore()
 
     def step(self, slot, norm, c):
-        """One iteration: local update, exchange, fixed-order decision."""
+        """One synchronous iteration: local update, exchange, fixed-order
+        decision read back to the host -> (stress, b, committed, diverged)."""
         self.backend.step_local(slot, norm, c)
         ynext, parts = self.backend.exchange_views()
         _allgather_inplace(ynext, self.rank, self.world, self.group)
         _allgather_inplace(parts, self.rank, self.world, self.group)
         return self.backend.step_finalize()
 
-    def run(self, slot, norm, c, n_iter):
-        """Same contract as DeviceEmbedding.run: (stress[], step[], done, diverged)."""
-        stress, step = [], []
-        for it in range(int(n_iter)):
-            e, b, _committed, div = self.step(slot, norm, c)
-            stress.append(e)
-            step.append(b)
-            if div:
-                return np.array(stress), np.array(step), it, True
-        return np.array(stress), np.array(step), int(n_iter), False
+    def _iteration(self, slot, norm):
+        be = self.backend
+        yptr = be.shard_step(slot, norm)
+        ynext, parts = be.exchange_views(yptr)
+        _allgather_inplace(ynext, self.rank, self.world, self.group)
+        _allgather_inplace(parts, self.rank, self.world, self.group)
+        be.shard_finalize()
+
+    def run(self, slot, norm, c, n_iter, graph_chunk=None):
+        """Same contract as DeviceEmbedding.run: (stress[], step[], done, diverged).
+
+        Asynchronous: per iteration the local update, the two all-gathers and
+        the finalizer are queued on the stream without reading anything back
+        (the exchange buffer alternates by parity, see ivhd_shard_step); the
+        trace and the divergence status are read once at the end.  On CUDA the
+        sequence of `graph_chunk` (even) iterations is captured once as a CUDA
+        graph (kernels + NCCL collectives) and replayed, so the host issues one
+        launch per chunk instead of ~5 calls per iteration."""
+        be = self.backend
+        n_iter = int(n_iter)
+        parity, epoch = be.shard_begin(slot, c, n_iter)
+        chunk = self.graph_chunk if graph_chunk is None else int(graph_chunk)
+        chunk -= chunk % 2  # a replay must leave the buffer parity unchanged
+        done = 0
+        if chunk >= 2 and n_iter >= 3 + chunk and self._can_capture():
+            key = (slot, norm, chunk)
+            g = self._graphs.get(key)
+            if g is not None and g[2] != epoch:  # CSR / optimizer / trace buffer changed
+                g = None
+            # warm-up (kernel attributes, NCCL communicator, allocator pools) and
+            # alignment to the parity the cached graph was captured at
+            warm = 2 if g is None else (0 if g[1] == parity else 1)
+            for _ in range(warm):
+                self._iteration(slot, norm)
+            parity ^= warm & 1
+            done = warm
+            if g is None:
+                g = (self._capture(chunk, slot, norm), parity, epoch)
+                self._graphs[key] = g
+            while n_iter - done >= chunk:
+                g[0].replay()
+                done += chunk
+        for _ in range(n_iter - done):
+            self._iteration(slot, norm)
+        return be.shard_end()
+
+    graph_chunk = 32
+
+    def _can_capture(self):
+        # the context must launch on the caller's stream (not a private one)
+        try:
+            import torch
+
+            return (isinstance(self.backend, DeviceShardBackend) and self.backend.stream != 0
+                    and torch.cuda.is_available())
+        except Exception:
+            return False
+
+    def _capture(self, chunk, slot, norm):
+        import torch
+
+        stream = torch.cuda.ExternalStream(self.backend.stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            stream.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(chunk):
+                    self._iteration(slot, norm)
+        return g

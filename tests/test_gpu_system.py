@@ -67,6 +67,53 @@ def test_sharded_nccl_world1_matches_single_gpu():
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("integ,iters,diverges", [
+    ({"b": 0.5, "tau": 1e-6}, 30, False),   # rollback-heavy auto-adapt
+    ({"b": 1e6, "auto_adapt": False}, 40, True),  # blow-up
+])
+def test_sharded_async_loop_rollback_and_divergence(integ, iters, diverges):
+    """The asynchronous sharded loop (parity buffers, rollback refill on the
+    device, status read once at the end) against the fused single-GPU loop."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_05455_b200.config import IntegratorParams, resolve_optimizer
+    from paper_2303_05455_b200.device import DeviceEmbedding
+    from paper_2303_05455_b200.embed import init_layout, sample_random_neighbors
+    from paper_2303_05455_b200.sharded import ShardedEmbedding
+
+    nb = _problem(3000)
+    m = nb.shape[0]
+    rng = np.random.default_rng(2)
+    y0 = init_layout(m, 2, rng)
+    rn = sample_random_neighbors(m, nb, 1, rng)
+    opt = resolve_optimizer("force-directed", m, IntegratorParams(**integ))
+    ref = DeviceEmbedding(m, 2)
+    ref.set_optimizer(opt)
+    ref.set_positions(y0)
+    ref.set_graph(0, nb, rn)
+    s_ref, b_ref, d_ref, div_ref = ref.run(0, "l2", 0.1, iters)
+    assert div_ref == diverges
+    if not diverges:
+        assert (b_ref[1:] != b_ref[:-1]).sum() >= 3
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        stream = torch.cuda.current_stream()
+        sh = ShardedEmbedding(m, 2, 0, 1, stream=stream.cuda_stream)
+        sh.set_optimizer(opt)
+        sh.set_positions(y0)
+        sh.set_graph(0, nb, rn)
+        s_sh, b_sh, done, div = sh.run(0, "l2", 0.1, iters)
+        assert div == diverges and done == d_ref
+        np.testing.assert_array_equal(np.asarray(b_sh), b_ref)
+        np.testing.assert_allclose(np.asarray(s_sh)[np.isfinite(s_ref)], s_ref[np.isfinite(s_ref)], rtol=1e-5)
+        np.testing.assert_array_equal(sh.positions(), ref.positions())
+    finally:
+        dist.destroy_process_group()
+
+
 def _knn_preservation(Y, nb, k=2):
     """Fraction of graph neighbours among each point's k nearest in 2-D."""
     from scipy.spatial import cKDTree

@@ -69,8 +69,43 @@ class NumpyShardBackend:
                 acc += [e_row[v], new @ new, old @ old, 0.0 if np.isfinite(ynext[v]).all() else 1.0]
             parts[t] = acc
 
-    def exchange_views(self):
-        return self.Y[1 - self.cur], self.parts
+    def exchange_views(self, token=None):
+        return self.Y[1 - self.cur if token is None else token], self.parts
+
+    # asynchronous contract (ivhd_shard_*): read Y[cur], write Y[cur^1], the
+    # finalizer makes the written buffer current and refills it on rollback
+    def shard_begin(self, slot, c, n_iter):
+        self.trace, self.status, self.diverged_at = [], 0, None
+        self.shard_cur = self.cur
+        return self.cur, 0
+
+    def shard_step(self, slot, norm):
+        if not self.status:
+            self.step_local(slot, norm, self.c)
+        return self.shard_cur ^ 1
+
+    def shard_finalize(self):
+        out = self.shard_cur ^ 1
+        self.shard_cur = out
+        if self.status:
+            return
+        before = self.cur
+        e, b, commit, div = self.step_finalize()
+        self.trace.append((e, b))
+        if div:
+            self.status, self.diverged_at = 1, len(self.trace) - 1
+            self.cur = before
+            return
+        if not commit:  # refill the written buffer with the unchanged positions
+            self.Y[out][:] = self.Y[before]
+        self.cur = out
+
+    def shard_end(self):
+        st = np.array([t[0] for t in self.trace])
+        bb = np.array([t[1] for t in self.trace])
+        if self.status:
+            return st, bb, self.diverged_at, True
+        return st, bb, len(self.trace), False
 
     def step_finalize(self):
         s = self.parts.numpy().reshape(-1, 4).sum(axis=0)
@@ -87,19 +122,19 @@ class NumpyShardBackend:
         return E, self.b, commit, False
 
 
-def _problem(m=700, seed=0):
+def _problem(m=700, seed=0, integ=None):
     rng = np.random.default_rng(seed)
     nb = ((np.arange(m)[:, None] + rng.integers(1, 30, size=(m, 2))) % m).astype(np.int32)
-    orc = OracleRun(nb, nn=2, rn=1, c=0.1, iterations=30, seed=seed)
+    orc = OracleRun(nb, nn=2, rn=1, c=0.1, iterations=30, seed=seed, integrator=integ)
     return nb, orc
 
 
-def _worker(rank, world, port, iters, out):
+def _worker(rank, world, port, iters, out, integ=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        nb, orc = _problem()
-        be = NumpyShardBackend(orc.m, orc.full)
+        nb, orc = _problem(integ=integ)
+        be = NumpyShardBackend(orc.m, orc.full, **(integ or {}))
         sh = ShardedEmbedding(orc.m, 2, rank, world, backend=be)
         sh.set_positions(orc.Y)
         stress, steps, done, div = sh.run(0, "l2", 0.1, iters)
@@ -137,6 +172,27 @@ def test_two_gloo_ranks_match_one_rank_and_oracle(tmp_path):
     np.testing.assert_allclose(a["y"], orc.Y, rtol=0, atol=1e-12)
     np.testing.assert_allclose(a["stress"], orc.trace_stress, rtol=1e-12)
     np.testing.assert_allclose(a["b"], orc.trace_b, rtol=1e-14)
+
+
+@pytest.mark.timeout(300)
+def test_async_loop_rollbacks_match_oracle(tmp_path):
+    """Rollback-heavy auto-adapt (tiny tau, large b): the asynchronous loop's
+    parity buffers and rollback refill follow the oracle on 1 and 2 ranks."""
+    iters, integ = 12, {"b": 0.5, "tau": 1e-6}
+    for world in (1, 2):
+        mp.start_processes(_worker, args=(world, _free_port(), iters, str(tmp_path), integ), nprocs=world,
+                           start_method="spawn", join=True)
+    r1 = np.load(tmp_path / "rank0_of1.npz")
+    a = np.load(tmp_path / "rank0_of2.npz")
+    np.testing.assert_array_equal(a["y"], r1["y"])
+    np.testing.assert_array_equal(a["b"], r1["b"])
+    _, orc = _problem(integ=integ)
+    for _ in range(iters):
+        orc.step()
+    b = np.asarray(orc.trace_b)
+    assert (b[1:] != b[:-1]).sum() >= 3, "expected several auto-adapt rollbacks"
+    np.testing.assert_allclose(a["y"], orc.Y, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(a["b"], b, rtol=1e-14)
 
 
 def test_shard_plan_covers_all_vertices():
