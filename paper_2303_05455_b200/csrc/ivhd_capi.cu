@@ -189,7 +189,7 @@ inline int ys_of(int dim, int opt) { return (opt == OPT_NEST) ? (dim == 2 ? 4 : 
 
 template <int DIM, int OPT, bool W, int N>
 KernelInfo kinfo() {
-  return KernelInfo{step_kernel<DIM, OPT, W, N>, step_smem_bytes<DIM, OPT>()};
+  return KernelInfo{step_kernel<DIM, OPT, W, N>, step_smem_bytes<DIM, OPT, W, N>()};
 }
 
 template <int DIM, bool W, int N>

@@ -613,6 +613,22 @@ __device__ __forceinline__ uint32_t ld_col(const uint32_t* p) {
   asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+#ifndef IVHD_GATHER_LD
+#define IVHD_GATHER_LD 0
+#endif
+// neighbour-position gather: 0 = ld.global.nc (L1 allocate), 1 = no L1
+// allocation, 2 = L2 only (.cg)
+__device__ __forceinline__ float2 ld_pos(const float2* p) {
+  float2 v;
+  if constexpr (IVHD_GATHER_LD == 1) {
+    asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  } else if constexpr (IVHD_GATHER_LD == 2) {
+    asm("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  } else {
+    v = __ldg(p);
+  }
+  return v;
+}
 #ifndef IVHD_UNIT_CACHE
 #define IVHD_UNIT_CACHE 256
 #endif
@@ -623,10 +639,11 @@ constexpr int kUnitCache = IVHD_UNIT_CACHE;  // unit words cached per block
 // the slot count D <= 8 is a template constant, all D column reads and gathers
 // are issued first, then ~20 instructions per entry.  Slots past the lane's
 // last entry are self pairs (zero contribution).
-template <int D, bool GCOL>
+template <int D, bool GCOL, bool SPOS = false>
 __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G, int deg,
                                          const float* __restrict__ Yin, uint32_t v, float y0, float y1, float c,
-                                         long long gstep, float (&f)[2], float& e) {
+                                         long long gstep, float (&f)[2], float& e,
+                                         const float2* __restrict__ gp = nullptr) {
   uint32_t cw[D];
   float2 p[D];
 #pragma unroll
@@ -634,7 +651,15 @@ __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G,
 #pragma unroll
   for (int q = 0; q < D; ++q) {
     p[q] = make_float2(y0, y1);
-    if (q < deg) p[q] = __ldg(reinterpret_cast<const float2*>(Yin) + (cw[q] & kIdMask));
+    if constexpr (SPOS) {  // neighbour positions already staged in shared memory
+      if (q < deg) p[q] = gp[q * G];
+    } else {
+#ifdef IVHD_ABLATE_GATHER  // timing experiment only: no random traffic (wrong results)
+      if (q < deg) p[q] = __ldg(reinterpret_cast<const float2*>(Yin) + (v ^ 1u));
+#else
+      if (q < deg) p[q] = ld_pos(reinterpret_cast<const float2*>(Yin) + (cw[q] & kIdMask));
+#endif
+    }
   }
   float fx = f[0], fy = f[1], ee = e;
   unsigned dmask = 0;
@@ -669,22 +694,55 @@ __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G,
   e = ee;
 }
 
-// Shared-memory layout of one ring stage for (DIM, OPT).
-template <int DIM, int OPT>
+#ifndef IVHD_GATHER_STAGING
+#define IVHD_GATHER_STAGING 0
+#endif
+#ifndef IVHD_GS_STAGES
+#define IVHD_GS_STAGES 3
+#endif
+// Gather staging (2-D, binary, L2, no look-ahead — every BASELINE config):
+// each consumer thread copies the neighbour positions of ITS entries of unit
+// k+1 into that unit's stage with 8-byte cp.async before computing unit k, so
+// the random loads are in flight during a whole unit of compute (software
+// pipelining; a thread later reads back only what it gathered itself).
+template <int DIM, int OPT, bool WEIGHTED, int NORM>
+__host__ __device__ constexpr bool gather_staged() {
+  return IVHD_GATHER_STAGING && DIM == 2 && !WEIGHTED && NORM == 0 && OPT != OPT_NEST;
+}
+
+// Shared-memory layout of one ring stage.
+template <int DIM, int OPT, bool GS>
 struct StageLayout {
+  static constexpr int STAGES = GS ? IVHD_GS_STAGES : kStages;
   static constexpr int YS = Layout<DIM, OPT>::YS, SS = Layout<DIM, OPT>::SS;
   static constexpr int RP_BYTES = ((kBlock + 1) * 4 + 15) / 16 * 16 + 16;
   static constexpr int COL_BYTES = kColCap * 4 + 32;
+  static constexpr int GP_BYTES = GS ? kColCap * 8 + 16 : 0;
   static constexpr int Y_BYTES = kBlock * YS * 4;
   static constexpr int S_BYTES = kBlock * (SS > 0 ? SS : 1) * 4;
-  static constexpr int RP_OFF = 0, COL_OFF = RP_BYTES, Y_OFF = COL_OFF + COL_BYTES, S_OFF = Y_OFF + Y_BYTES;
+  static constexpr int RP_OFF = 0, COL_OFF = RP_BYTES, GP_OFF = COL_OFF + COL_BYTES, Y_OFF = GP_OFF + GP_BYTES,
+                       S_OFF = Y_OFF + Y_BYTES;
   static constexpr int BYTES = S_OFF + S_BYTES;
 };
 
-template <int DIM, int OPT>
-constexpr int step_smem_bytes() {
-  return kStages * StageLayout<DIM, OPT>::BYTES;
+template <int DIM, int OPT, bool WEIGHTED, int NORM>
+__host__ __device__ constexpr int step_smem_bytes() {
+  using SL = StageLayout<DIM, OPT, gather_staged<DIM, OPT, WEIGHTED, NORM>()>;
+  return SL::STAGES * SL::BYTES;
 }
+
+template <int DIM, int OPT, bool WEIGHTED, int NORM>
+__host__ __device__ constexpr int step_min_blocks() {
+  return gather_staged<DIM, OPT, WEIGHTED, NORM>() && IVHD_GS_STAGES >= 3 ? 2 : IVHD_MINBLOCKS;
+}
+
+// 8-byte cp.async gather into shared memory, per-thread commit groups
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Per-stage metadata written by the producer before it arrives on the
 // stage's barriers (release) and read by consumers after the wait (acquire).
@@ -710,9 +768,11 @@ constexpr int kThreads = kBlock + 32;  // 8 consumer warps + 1 TMA producer warp
 constexpr int kConsumerWarps = kBlock / 32;
 
 template <int DIM, int OPT, bool WEIGHTED, int NORM>
-__global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs A) {
+__global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, NORM>()) step_kernel(StepArgs A) {
+  constexpr bool GS = gather_staged<DIM, OPT, WEIGHTED, NORM>();
   using L = Layout<DIM, OPT>;
-  using SL = StageLayout<DIM, OPT>;
+  using SL = StageLayout<DIM, OPT, GS>;
+  constexpr int kStages = SL::STAGES;
   constexpr bool NEST = (OPT == OPT_NEST);
   constexpr int SSX = L::SS > 0 ? L::SS : 1;
   constexpr int YS = L::YS;
@@ -761,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
   float te = 0.f, tn = 0.f, to = 0.f, tb = 0.f;  // fused mode: this thread's running partials
   if (warp == kConsumerWarps) {
     // ---------------------------------------------------- TMA producer warp
-    if (lane == 0) {
+    // Lane 0 issues the bulk copies (the whole warp runs the loop).
       auto issue_rp = [&](int k) {  // row pointers of local unit k (graph constant)
         const int s = k % kStages;
         unsigned char* st = smem_raw + s * SL::BYTES;
@@ -810,37 +870,43 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
         if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, A.state + va * L::SS, s_copy, &bar_a[s]);
       };
       const int pre = min(my_units, kStages);
-      int nf = 0, nc = 0;
-      for (; nf < pre; ++nf) issue_rp(nf);
-      for (; nc < pre; ++nc) {
-        mbar_wait(&bar_r[nc], 0);
-        issue_cols(nc);
+      int nf = pre, nc = pre;
+      if (lane == 0) {
+        for (int k = 0; k < pre; ++k) issue_rp(k);
+        for (int k = 0; k < pre; ++k) {
+          mbar_wait(&bar_r[k], 0);
+          issue_cols(k);
+        }
       }
+      __syncwarp();
       griddep_wait();  // the previous iteration (positions, state, ctrl) is complete
       if (ctrl->status != 0) {  // diverged earlier: drain the prefetch and leave
         for (int k = 0; k < pre; ++k) mbar_wait(&bar_b[k], 0);
       } else {
         const float* Yin = (A.fixed_io || !ctrl->cur) ? A.ybuf0 : A.ybuf1;
-        for (int k = 0; k < pre; ++k) issue_ys(k, Yin);
+        if (lane == 0)
+          for (int k = 0; k < pre; ++k) issue_ys(k, Yin);
         // Event loop: stages are claimed as consumers free them; a unit's
         // columns are requested the moment its row pointers land.
         while (nc < my_units) {
-          bool idle = true;
-          if (nf < my_units && nf < nc + kStages && mbar_test(&bar_e[nf % kStages], (uint32_t)(nf / kStages - 1) & 1)) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_rp(nf);
-            issue_ys(nf, Yin);
-            ++nf;
-            idle = false;
+          int ok = 0;
+          if (lane == 0) {
+            if (nf < my_units && nf < nc + kStages && mbar_test(&bar_e[nf % kStages], (uint32_t)(nf / kStages - 1) & 1))
+              ok |= 1;
+            if (nc < nf && mbar_test(&bar_r[nc % kStages], (uint32_t)(nc / kStages) & 1)) ok |= 2;
+            if (ok & 1) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              issue_rp(nf);
+              issue_ys(nf, Yin);
+            }
+            if (ok & 2) issue_cols(nc);
           }
-          if (nc < nf && mbar_test(&bar_r[nc % kStages], (uint32_t)(nc / kStages) & 1)) {
-            issue_cols(nc++);
-            idle = false;
-          }
-          if (IVHD_BACKOFF_NS > 0 && idle) __nanosleep(IVHD_BACKOFF_NS);  // leave issue slots to the consumers
+          ok = __shfl_sync(0xffffffffu, ok, 0);
+          nf += ok & 1;
+          nc += (ok >> 1) & 1;
+          if (IVHD_BACKOFF_NS > 0 && !ok) __nanosleep(IVHD_BACKOFF_NS);
         }
       }
-    }
     griddep_wait();
     if (ctrl->status != 0) return;
   } else {
@@ -866,11 +932,42 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
       bc1 = (float)(1.0 / (1.0 - pow((double)A.h.gv, tt)));
       bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
     }
+    // gather staging: this thread's neighbour positions of unit k -> stage
+    auto own_gathers = [&](int k) {
+      const int s = k % kStages;
+      const uint32_t par = (uint32_t)(k / kStages) & 1;
+      mbar_wait(&bar_r[s], par);
+      mbar_wait(&bar_b[s], par);
+      if (meta[s].staged) {
+        unsigned char* st = smem_raw + s * SL::BYTES;
+        const int pk = meta[s].packed, lgG = pk & 7, G = 1 << lgG, lg = tid & (G - 1), grp = tid >> lgG;
+        if (grp < meta[s].nv) {
+          const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
+          const uint32_t* cols = reinterpret_cast<const uint32_t*>(st + SL::COL_OFF) + meta[s].col_off;
+          float2* gp = reinterpret_cast<float2*>(st + SL::GP_OFF);
+          const float2* Y2 = reinterpret_cast<const float2*>(Yin);
+          const int e0 = (int)rp[0], b = (int)rp[grp] - e0, deg = (int)rp[grp + 1] - e0 - b;
+          for (int e = b + lg; e < b + deg; e += G) cp_async8(gp + e, Y2 + (cols[e] & kIdMask));
+        }
+      }
+      cp_async_commit();
+    };
+    if constexpr (GS) {
+      if (my_units > 0) own_gathers(0);
+    }
     for (int k = 0; k < my_units; ++k) {
       const int u = blockIdx.x + k * grid;
       const int s = k % kStages;
       unsigned char* st = smem_raw + s * SL::BYTES;
       const uint32_t par = (uint32_t)(k / kStages) & 1;
+      if constexpr (GS) {
+        if (k + 1 < my_units) {
+          own_gathers(k + 1);
+          cp_async_wait<1>();  // unit k's positions have landed (in flight during unit k-1)
+        } else {
+          cp_async_wait<0>();
+        }
+      }
       mbar_wait(&bar_r[s], par);
       mbar_wait(&bar_a[s], par);
       mbar_wait(&bar_b[s], par);
@@ -926,8 +1023,31 @@ __global__ void __launch_bounds__(kThreads, IVHD_MINBLOCKS) step_kernel(StepArgs
                   fast_row<8, GC>(cb + c0 * G, G, nl - c0, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e);
               }
             };
-            if (staged) run(std::false_type{}, colst + (beg - e0 + coff) + lg);
-            else run(std::true_type{}, A.col + beg + lg);
+            if constexpr (GS) {
+              if (staged) {  // columns and neighbour positions both in shared memory
+                const uint32_t* cb = colst + (beg - e0 + coff) + lg;
+                const float2* gpb = reinterpret_cast<const float2*>(st + SL::GP_OFF) + (beg - e0) + lg;
+                if (slots <= 8) {
+                  switch (slots) {
+#define IVHD_FAST_CASE(D) \
+  case D: fast_row<D, false, true>(cb, G, nl, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e, gpb); break;
+                    IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
+                    IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
+#undef IVHD_FAST_CASE
+                    default: break;
+                  }
+                } else {
+                  for (int c0 = 0; c0 < nl; c0 += 8)
+                    fast_row<8, false, true>(cb + c0 * G, G, nl - c0, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e,
+                                             gpb + c0 * G);
+                }
+              } else {
+                run(std::true_type{}, A.col + beg + lg);
+              }
+            } else {
+              if (staged) run(std::false_type{}, colst + (beg - e0 + coff) + lg);
+              else run(std::true_type{}, A.col + beg + lg);
+            }
             f[0] = ff[0];
             f[1] = ff[1];
           }
