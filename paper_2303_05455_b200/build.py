@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "ivhd_capi.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "ivhd_step.cuh"), os.path.join(ROOT, "include", "ivhd_b200.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", "ivhd_step.cuh"), os.path.join(HERE, "csrc", "ivhd_rng.cuh"), os.path.join(ROOT, "include", "ivhd_b200.h")]
 OUT = os.path.join(HERE, "libivhd_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -35,6 +35,11 @@ struct CsrSlot {
   int* units = nullptr;         // work units (tile << 12 | pass << 7 | min(slots per lane,15) << 3 | log2 G)
   int n_units = 0;
   std::vector<int> unit_base;   // host: first unit of each tile (n_tiles_cap + 1)
+  std::vector<int> unit_words;  // host copy of units
+  std::vector<int> unit_cost;   // host: modelled cost of each unit (slot rounds per lane)
+  int sched_grid = 0;           // grid the cost-balanced schedule below was built for
+  int* sched_units = nullptr;   // units regrouped per block (fused mode)
+  int* sched_off = nullptr;     // [sched_grid + 1]
   int64_t n = 0;                // entries (2 * connections)
   int64_t cap = 0;
   bool valid = false;
@@ -629,6 +634,13 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
       const int d15 = std::min<int>((dm[t] + g[t] - 1) / g[t], 15);  // slots per lane
       for (int p = 0; p < g[t]; ++p) units.push_back(t << 12 | p << 7 | d15 << 3 | lg);
     }
+    S.unit_words = units;
+    S.unit_cost.resize(units.size());
+    for (size_t u = 0; u < units.size(); ++u) {
+      const int t = units[u] >> 12, G = 1 << (units[u] & 7);
+      S.unit_cost[u] = (dm[t] + G - 1) / G;  // slots per lane (clamped degree for hubs)
+    }
+    S.sched_grid = 0;
     S.n_units = (int)units.size();
     if (S.units) dfree(ctx, S.units);
     S.units = nullptr;
@@ -647,6 +659,54 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
 }
 
 // ---------------------------------------------------------- launch helpers
+
+// Cost-balanced static schedule for the fused loop: longest-processing-time
+// greedy over the modelled unit costs (slot rounds per lane + a fixed
+// per-unit overhead), ties to the lowest block; each block then runs its
+// units heavy first.  Deterministic for a given graph and grid, so the
+// per-thread partial sums keep a fixed order.
+int build_schedule(ivhd_ctx* ctx, CsrSlot& S, int grid) {
+  if (S.sched_grid == grid) return IVHD_OK;
+  static const int c0 = [] {
+    const char* e = getenv("IVHD_LPT_C0");
+    return e ? atoi(e) : 3;
+  }();
+  const int n = S.n_units;
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return S.unit_cost[a] > S.unit_cost[b]; });
+  std::vector<std::vector<int>> per(grid);
+  std::vector<std::pair<int64_t, int>> heap;  // (load, block), min-heap
+  for (int b = 0; b < grid; ++b) heap.push_back({0, b});
+  auto cmp = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) { return x > y; };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  for (int u : order) {
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    auto& top = heap.back();
+    per[top.second].push_back(u);
+    top.first += S.unit_cost[u] + c0;
+    std::push_heap(heap.begin(), heap.end(), cmp);
+  }
+  std::vector<int> words, off(grid + 1, 0);
+  words.reserve(n);
+  for (int b = 0; b < grid; ++b) {
+    for (int u : per[b]) words.push_back(S.unit_words[u]);
+    off[b + 1] = (int)words.size();
+  }
+  drop_graphs(ctx);  // captured launches hold the old schedule pointers
+  dfree(ctx, S.sched_units);
+  dfree(ctx, S.sched_off);
+  S.sched_units = nullptr;
+  S.sched_off = nullptr;
+  S.sched_grid = 0;
+  CU(ctx, dalloc(ctx, &S.sched_units, sizeof(int) * std::max(n, 1)));
+  CU(ctx, dalloc(ctx, &S.sched_off, sizeof(int) * (grid + 1)));
+  CU(ctx, cudaMemcpyAsync(S.sched_units, words.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(S.sched_off, off.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+  S.sched_grid = grid;
+  return IVHD_OK;
+}
 
 StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   const CsrSlot& S = ctx->slots[slot];
@@ -914,6 +974,7 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   lap("graphs");
   for (auto& s : ctx->slots) {
     dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.tile_dm); dfree(ctx, s.units);
+    dfree(ctx, s.sched_units); dfree(ctx, s.sched_off);
   }
   dfree(ctx, ctx->perm); dfree(ctx, ctx->inv);
   dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial); dfree(ctx, ctx->bpart);
@@ -1374,7 +1435,17 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   TRY(push_ctrl(ctx));
   const CsrSlot& S = ctx->slots[slot];
   KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm);
-  const StepArgs A = make_args(ctx, slot, norm, 1);
+  StepArgs A = make_args(ctx, slot, norm, 1);
+  static const bool lpt = [] {
+    const char* e = getenv("IVHD_LPT");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  if (lpt) {
+    const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
+    TRY(build_schedule(ctx, ctx->slots[slot], grid));
+    A.units = S.sched_units;
+    A.boff = S.sched_off;
+  }
   int64_t left = n_iter;
   const int chunk = ctx->graph_chunk;
   if (left >= chunk) {

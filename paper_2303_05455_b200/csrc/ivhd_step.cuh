@@ -113,6 +113,8 @@ struct StepArgs {
   double* force_out;      // OPT_NONE only: (M, DIM) float64
   const uint8_t* tile_g;  // lanes per vertex of every (global) tile
   const int* units;       // work unit -> tile << 12 | pass << 7 | min(slots,15) << 3 | log2 G
+  const int* boff;        // fused mode: block b runs units[boff[b] .. boff[b+1]) (cost-balanced
+                          // static schedule); nullptr: round robin u = b + k * grid
   long long v_begin, v_end;
   int tile_v;
   int n_tiles;            // work units this launch processes
@@ -792,12 +794,22 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
 #endif
   const int n_units = A.n_tiles;
   const int grid = gridDim.x;
-  const int my_units = blockIdx.x < n_units ? (n_units - 1 - blockIdx.x) / grid + 1 : 0;
+  // this block's unit list: a cost-balanced contiguous range (fused mode) or
+  // round robin over the heavy-first unit order (sharded mode)
+  const int* ulist = A.units + A.tile0 + blockIdx.x;
+  int ustride = grid;
+  int my_units = blockIdx.x < n_units ? (n_units - 1 - blockIdx.x) / grid + 1 : 0;
+  if (A.boff) {
+    const int b0 = __ldg(A.boff + blockIdx.x);
+    my_units = __ldg(A.boff + blockIdx.x + 1) - b0;
+    ulist = A.units + b0;
+    ustride = 1;
+  }
 
   // ---- before the dependency wait: only graph constants (unit list, row
   // pointers, columns) are read, so this overlaps the previous iteration's tail.
   for (int k = tid; k < min(my_units, kUnitCache); k += kThreads)
-    sm_units[k] = __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
+    sm_units[k] = __ldg(ulist + k * ustride);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bar_r[s], 1);
@@ -825,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       auto issue_rp = [&](int k) {  // row pointers of local unit k (graph constant)
         const int s = k % kStages;
         unsigned char* st = smem_raw + s * SL::BYTES;
-        const int packed = k < kUnitCache ? sm_units[k] : __ldg(A.units + A.tile0 + blockIdx.x + k * grid);
+        const int packed = k < kUnitCache ? sm_units[k] : __ldg(ulist + k * ustride);
         long long va;
         int nv;
         unit_range(packed, va, nv);
