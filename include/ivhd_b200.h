@@ -25,6 +25,8 @@
  *   ivhd_get_deltas                 EmbeddingState.deltas            engine.py:379
  *   ivhd_snapshot / ivhd_restore    (new) device-side checkpoint     SURVEY.md §5 checkpoint row
  *   ivhd_shard_* / ivhd_step_*      (new) vertex-range sharding
+ *   ivhd_knn_build                  knng.build_exact_knn             knng.py:158-194
+ *                                   (euclidean / cosine)
  */
 #ifndef IVHD_B200_H
 #define IVHD_B200_H
@@ -168,6 +170,19 @@ int ivhd_shard_begin(ivhd_ctx* ctx, int slot, double c, int64_t n_iter, int* cur
 int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out);
 int ivhd_shard_finalize(ivhd_ctx* ctx);
 int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out);
+
+/* Exact kNN graph of the rows of a host (m, n) float64 matrix, computed on
+ * `device` (knng.build_exact_knn, knng.py:158-194): row i lists its k nearest
+ * other rows by (distance, index); metric 0 = euclidean (distance), 1 =
+ * cosine (1 - cos, rows normalised first; a zero row is IVHD_ERR_INVALID_ARG
+ * with "zero-norm vector" in the message).  1 <= k < m, k <= 64.
+ * nbr_out (m, k) int32 and dist_out (m, k) float64 are host buffers.
+ * stats_out (optional, 4 doubles): tensor-core pass seconds, re-rank seconds,
+ * rows re-scanned exactly (uncertified), total seconds.  Errors: message in
+ * ivhd_knn_last_error(). */
+int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k, int32_t metric,
+                   int32_t* nbr_out, double* dist_out, double* stats_out);
+const char* ivhd_knn_last_error(void);
 
 #ifdef __cplusplus
 }

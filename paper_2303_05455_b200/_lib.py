@@ -81,6 +81,9 @@ SIGNATURES = {
                                        ctypes.c_double]),
     "ivhd_step_finalize": (ctypes.c_int, [ctypes.c_void_p, c_f64p, c_f64p,
                                           ctypes.POINTER(ctypes.c_int)]),
+    "ivhd_knn_last_error": (ctypes.c_char_p, []),
+    "ivhd_knn_build": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, c_i32p, c_f64p, c_f64p]),
 }
 
 _lock = threading.Lock()

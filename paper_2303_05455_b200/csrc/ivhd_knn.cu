@@ -1,0 +1,622 @@
+// ivhd_knn.cu — exact kNN graph construction on B200.
+//
+// Replaces knng.build_exact_knn (/root/reference/pkg/src/ivhd/knng.py:158-194)
+// for the "euclidean" and "cosine" metrics: every row's k nearest other rows,
+// ordered by (distance, index) — on exact distance ties the smaller index wins
+// (knng.py:1-6, _row_topk knng.py:122-155).
+//
+// Three kernels:
+//   1. k_pack      fp64 rows -> tf32-rounded fp32 tiles in the tcgen05
+//                  canonical K-major no-swizzle layout (one contiguous image
+//                  per 128-row tile and 32-float K chunk, so every shared-memory
+//                  fill is ONE cp.async.bulk), plus fp32 squared norms.
+//   2. k_knn_tc    candidate pass on the 5th-generation tensor cores: a CTA
+//                  owns 128 queries and streams every 128-row candidate tile;
+//                  tcgen05.mma (kind::tf32, M=128 N=128, fp32 accumulators in
+//                  TMEM, double buffered) computes the 128x128 dot products,
+//                  four epilogue warps read them back with tcgen05.ld and keep
+//                  each query's KMAX smallest approximate squared distances.
+//                  Warp roles: 0 = TMA producer, 1 = MMA issuer (one lane),
+//                  2..5 = epilogue (TMEM lane quarter = warp % 4).
+//   3. k_rerank    exact fp64 distances to the KMAX candidates, (distance,
+//                  index) order, and a certificate: the candidate pass cannot
+//                  have dropped a closer row if the error-bounded lower bound
+//                  of every rejected row's distance exceeds the k-th exact
+//                  distance.  Uncertified rows (rare) go to
+//   4. k_exact     fp64 brute force over all rows for that query (block per
+//                  query, per-thread sorted lists merged in a fixed tree).
+//
+// No CPU fallback: every distance is computed on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ivhd_b200.h"
+
+namespace knn {
+
+constexpr int TQ = 128;       // queries per CTA (UMMA M)
+constexpr int TCN = 128;      // candidates per tile (UMMA N)
+constexpr int KC = 32;        // floats per K chunk (128 bytes per row)
+constexpr int KMAX = 32;      // approximate candidates kept per query
+constexpr int STAGES = 4;     // smem ring depth (A chunk + B chunk per stage)
+constexpr int THREADS = 192;  // 6 warps
+constexpr int CHUNK_BYTES = TQ * KC * 4;                // 16 KB
+constexpr int STAGE_BYTES = 2 * CHUNK_BYTES;            // A + B chunk
+constexpr int LIST_BYTES = 2 * KMAX * TQ * 4;           // sorted (d2, id) lists
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + LIST_BYTES + 1024;
+
+// byte offset of element (r, k) inside a chunk image with kc floats per row:
+// core matrices of 8 rows x 16 bytes; K-chunk stride (LBO) 128 bytes, 8-row
+// group stride (SBO) kc * 32 bytes.
+__host__ __device__ __forceinline__ uint32_t img_off(int r, int k, int kc) {
+  return (uint32_t)((r >> 3) * (kc * 32) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// tcgen05 helpers (PTX ISA 8.7, sm_100a)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // SWIZZLE_NONE K-major: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
+  // version 1 at bit 46, base offset 0, legacy LBO mode, layout type 0.
+  return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major both, N, M
+__host__ __device__ constexpr uint32_t umma_idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ pack
+// One warp per row: tf32-rounded values into the tile images, fp32 norm of
+// the rounded row.  Padding rows get norm +inf (never a candidate).
+__global__ void k_pack(const double* __restrict__ X, int64_t m, int n, int kp, int64_t m_pad,
+                       float* __restrict__ P, float* __restrict__ nrm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < m_pad; r += nw) {
+    const int64_t t = r / TQ;
+    const int rr = (int)(r % TQ);
+    float s = 0.f;
+    for (int k = lane; k < kp; k += 32) {
+      const float v = (r < m && k < n) ? tf32_round((float)X[r * n + k]) : 0.f;
+      s = fmaf(v, v, s);
+      const int c = k / KC, kk = k % KC, kc = min(KC, kp - c * KC);
+      const int64_t off = t * (int64_t)TQ * kp * 4 + (int64_t)c * CHUNK_BYTES + img_off(rr, kk, kc);
+      P[off >> 2] = v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) nrm[r] = r < m ? s : INFINITY;
+  }
+}
+
+// Rows scaled to unit norm (cosine metric, knng.py:105-115); a zero row sets *bad.
+__global__ void k_normalize(double* __restrict__ X, int64_t m, int n, long long* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < m; r += nw) {
+    double s = 0.0;
+    for (int k = lane; k < n; k += 32) s = fma(X[r * n + k], X[r * n + k], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double nr = sqrt(s);
+    if (nr == 0.0) {
+      if (lane == 0) atomicMin(bad, (long long)r);
+      continue;
+    }
+    for (int k = lane; k < n; k += 32) X[r * n + k] /= nr;
+  }
+}
+
+// ---------------------------------------------------------- candidate pass
+__global__ void __launch_bounds__(THREADS, 1)
+    k_knn_tc(const float* __restrict__ P, const float* __restrict__ nrm, int64_t m, int kp, int n_tiles, int keep,
+             int32_t* __restrict__ cand_id, float* __restrict__ cand_d2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* ring = smem;
+  float* lst_d = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);  // [KMAX][TQ]
+  int* lst_i = reinterpret_cast<int*>(lst_d + KMAX * TQ);               // [KMAX][TQ]
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accf[2], acce[2];
+  __shared__ uint32_t tmem_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x;
+  const int nchunks = (kp + KC - 1) / KC;
+  const int64_t tile_floats = (int64_t)TQ * kp;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // 2 x 128 fp32 accumulator columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_sh)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    tc_fence_before();
+  }
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const float* Aq = P + (int64_t)qt * tile_floats;
+      int it = 0;
+      for (int j = 0; j < n_tiles; ++j) {
+        const float* Bt = P + (int64_t)j * tile_floats;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          const uint32_t bytes = (uint32_t)TQ * min(KC, kp - c * KC) * 4;
+          uint8_t* st = ring + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], 2 * bytes);
+          bulk_g2s(st, Aq + (int64_t)c * TQ * KC, bytes, &full[s]);
+          bulk_g2s(st + CHUNK_BYTES, Bt + (int64_t)c * TQ * KC, bytes, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_tf32(TQ, TCN);
+      int it = 0;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int b = j & 1;
+        if (j >= 2) mbar_wait(&acce[b], ((j >> 1) - 1) & 1);  // epilogue drained buffer b
+        tc_fence_after();
+        const uint32_t dt = tbase + (uint32_t)(b * TCN);
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const int kc = min(KC, kp - c * KC);
+          const uint32_t sa = smem_u32(ring + s * STAGE_BYTES), sb = sa + CHUNK_BYTES;
+          for (int ks = 0; ks < kc / 8; ++ks) {
+            const uint64_t ad = umma_desc(sa + ks * 256, 128, (uint32_t)kc * 32);
+            const uint64_t bd = umma_desc(sb + ks * 256, 128, (uint32_t)kc * 32);
+            umma_tf32(dt, ad, bd, idesc, (c | ks) != 0);
+          }
+          umma_commit(&empty[s]);  // stage free once these MMAs have read it
+        }
+        umma_commit(&accf[b]);  // accumulator b complete
+      }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int r = q * 32 + lane;
+    const int64_t qid = (int64_t)qt * TQ + r;
+    const float nq = qid < m ? nrm[qid] : 0.f;
+    for (int i = 0; i < keep; ++i) {
+      lst_d[i * TQ + r] = INFINITY;
+      lst_i[i * TQ + r] = -1;
+    }
+    float thr = INFINITY;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int b = j & 1;
+      mbar_wait(&accf[b], (j >> 1) & 1);
+      tc_fence_after();
+      const float4* nc4 = reinterpret_cast<const float4*>(nrm + (int64_t)j * TCN);
+#pragma unroll 1
+      for (int h = 0; h < TCN / 32; ++h) {
+        uint32_t v[32];
+        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TCN + h * 32), v);
+        if (h == TCN / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acce[b]);
+        }
+        const int64_t c0 = (int64_t)j * TCN + h * 32;
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) {
+          const float4 nc = __ldg(nc4 + h * 8 + i4);
+          const float ncv[4] = {nc.x, nc.y, nc.z, nc.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i4 * 4 + u;
+            const float d2 = fmaf(-2.f, __uint_as_float(v[i]), nq + ncv[u]);
+            const int64_t cid = c0 + i;
+            if (d2 < thr && cid != qid) {  // sorted insert; equal distances keep the smaller id first
+              int p = keep - 1;
+              while (p > 0 && lst_d[(p - 1) * TQ + r] > d2) {
+                lst_d[p * TQ + r] = lst_d[(p - 1) * TQ + r];
+                lst_i[p * TQ + r] = lst_i[(p - 1) * TQ + r];
+                --p;
+              }
+              lst_d[p * TQ + r] = d2;
+              lst_i[p * TQ + r] = (int)cid;
+              thr = lst_d[(keep - 1) * TQ + r];
+            }
+          }
+        }
+      }
+    }
+    if (qid < m) {
+      for (int i = 0; i < keep; ++i) {
+        cand_id[qid * KMAX + i] = lst_i[i * TQ + r];
+        cand_d2[qid * KMAX + i] = lst_d[i * TQ + r];
+      }
+    }
+  }
+  // non-aligned barrier: the producer and MMA warps arrive diverged (lane 0 ran the loop)
+  asm volatile("barrier.sync 0;" ::: "memory");
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256) : "memory");
+  }
+}
+
+// --------------------------------------------------------------- re-rank
+// Exact fp64 distance between rows a and b (euclidean: sqrt of the summed
+// squared differences; cosine on unit rows: max(1 - dot, 0), knng.py:185-189).
+__device__ __forceinline__ double exact_dist(const double* __restrict__ X, int n, int64_t a, int64_t b, int metric) {
+  const double* xa = X + a * n;
+  const double* xb = X + b * n;
+  double s = 0.0;
+  if (metric == 0) {
+    for (int k = 0; k < n; ++k) {
+      const double d = xa[k] - xb[k];
+      s = fma(d, d, s);
+    }
+    return sqrt(s);
+  }
+  for (int k = 0; k < n; ++k) s = fma(xa[k], xb[k], s);
+  return fmax(1.0 - s, 0.0);
+}
+
+__device__ __forceinline__ bool before(double da, int ia, double db, int ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+// One warp per query: lane i re-scores candidate i in fp64, ranks by
+// (distance, index), writes the first k, and certifies the result.
+__global__ void k_rerank(const double* __restrict__ X, int64_t m, int n, int metric, int k, int keep,
+                         const int32_t* __restrict__ cand_id, const float* __restrict__ cand_d2,
+                         const float* __restrict__ nrm, float rmax, float gamma, float eps_in,
+                         int32_t* __restrict__ out_id, double* __restrict__ out_d, int* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t qy = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; qy < m; qy += nw) {
+    int id = lane < keep ? cand_id[qy * KMAX + lane] : -1;
+    double d = INFINITY;
+    if (id >= 0) d = exact_dist(X, n, qy, id, metric);
+    else id = 0x7fffffff;
+    int rank = 0;
+    for (int o = 0; o < 32; ++o) {
+      const double od = __shfl_sync(0xffffffffu, d, o);
+      const int oi = __shfl_sync(0xffffffffu, id, o);
+      rank += (o != lane && before(od, oi, d, id)) ? 1 : 0;
+    }
+    if (rank < k) {
+      out_id[qy * k + rank] = id;
+      out_d[qy * k + rank] = d;
+    }
+    // certificate: every row outside the kept list had approximate squared
+    // distance >= T (the last kept value); its true distance is at least
+    //   sqrt(max(T - gamma (|q~| + R)^2, 0)) - eps_in (|q| + R)
+    // (gamma: fp32 Gram-expansion error, eps_in: tf32 input rounding).
+    const double dk = __shfl_sync(0xffffffffu, d, __ffs(__ballot_sync(0xffffffffu, rank == k - 1)) - 1);
+    if (lane == 0) {
+      bool ok = true;
+      if (m - 1 > keep) {
+        const double T = (double)cand_d2[qy * KMAX + keep - 1];
+        const double qn = sqrt((double)nrm[qy]) * (1.0 + 1e-6);
+        const double s = qn + (double)rmax;
+        double lb = sqrt(fmax(T - (double)gamma * s * s, 0.0)) - (double)eps_in * s;
+        double dke = dk;
+        if (metric == 1) dke = sqrt(2.0 * dk);  // cosine distance -> unit-row euclidean
+        ok = isfinite(T) && lb > dke;
+      }
+      if (!ok) flag[qy] = 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------ exact scan
+// Block per flagged query: every thread keeps a sorted (distance, index) list
+// of its strided rows; lists are merged pairwise in a fixed tree.
+constexpr int EX_THREADS = 128;
+constexpr int EX_K = 64;
+
+__global__ void __launch_bounds__(EX_THREADS) k_exact(const double* __restrict__ X, int64_t m, int n, int metric,
+                                                     int k, const int* __restrict__ list, int n_list,
+                                                     int32_t* __restrict__ out_id, double* __restrict__ out_d) {
+  extern __shared__ __align__(16) unsigned char exs[];
+  double* sd = reinterpret_cast<double*>(exs);               // [EX_THREADS][k]
+  int* si = reinterpret_cast<int*>(sd + EX_THREADS * k);     // [EX_THREADS][k]
+  double* td = reinterpret_cast<double*>(si + EX_THREADS * k);  // merge scratch [EX_THREADS][k]
+  int* ti = reinterpret_cast<int*>(td + EX_THREADS * k);
+  const int t = threadIdx.x;
+  for (int qi = blockIdx.x; qi < n_list; qi += gridDim.x) {
+    const int64_t qy = list[qi];
+    double* md = sd + t * k;
+    int* mi = si + t * k;
+    for (int i = 0; i < k; ++i) {
+      md[i] = INFINITY;
+      mi[i] = 0x7fffffff;
+    }
+    for (int64_t c = t; c < m; c += EX_THREADS) {
+      if (c == qy) continue;
+      const double d = exact_dist(X, n, qy, c, metric);
+      if (before(d, (int)c, md[k - 1], mi[k - 1])) {
+        int p = k - 1;
+        while (p > 0 && before(d, (int)c, md[p - 1], mi[p - 1])) {
+          md[p] = md[p - 1];
+          mi[p] = mi[p - 1];
+          --p;
+        }
+        md[p] = d;
+        mi[p] = (int)c;
+      }
+    }
+    __syncthreads();
+    for (int w = 1; w < EX_THREADS; w <<= 1) {  // merge list t + w into t
+      if ((t & (2 * w - 1)) == 0) {
+        const double* ad = sd + t * k;
+        const int* ai = si + t * k;
+        const double* bd = sd + (t + w) * k;
+        const int* bi = si + (t + w) * k;
+        double* od = td + t * k;
+        int* oi = ti + t * k;
+        int a = 0, b = 0;
+        for (int o = 0; o < k; ++o) {
+          if (before(ad[a], ai[a], bd[b], bi[b])) {
+            od[o] = ad[a];
+            oi[o] = ai[a++];
+          } else {
+            od[o] = bd[b];
+            oi[o] = bi[b++];
+          }
+        }
+        for (int o = 0; o < k; ++o) {
+          sd[t * k + o] = od[o];
+          si[t * k + o] = oi[o];
+        }
+      }
+      __syncthreads();
+    }
+    if (t < k) {
+      out_id[qy * k + t] = si[t];
+      out_d[qy * k + t] = sd[t];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_flag_list(const int* __restrict__ flag, int64_t m, int* __restrict__ list, int* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m && flag[i]) list[atomicAdd(cnt, 1)] = (int)i;
+}
+
+__global__ void k_max_norm(const float* __restrict__ nrm, int64_t m, unsigned int* __restrict__ out) {
+  float mx = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, nrm[i]);
+  atomicMax(out, __float_as_uint(mx));  // non-negative floats order like their bits
+}
+
+thread_local std::string g_knn_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_knn_error = buf;
+  return code;
+}
+
+}  // namespace knn
+
+using namespace knn;
+
+extern "C" {
+
+const char* ivhd_knn_last_error(void) { return g_knn_error.c_str(); }
+
+int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k, int32_t metric,
+                   int32_t* nbr_out, double* dist_out, double* stats_out) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  if (!x || !nbr_out || !dist_out) return fail(IVHD_ERR_INVALID_ARG, "null pointer");
+  if (!(1 <= k && k < m)) return fail(IVHD_ERR_INVALID_ARG, "k must satisfy 1 <= k < M, got k=%d, M=%lld", k, (long long)m);
+  if (n < 1) return fail(IVHD_ERR_INVALID_ARG, "need at least one feature column");
+  if (metric != 0 && metric != 1) return fail(IVHD_ERR_INVALID_ARG, "metric must be euclidean (0) or cosine (1)");
+  if (m >= 0x7fffffffLL) return fail(IVHD_ERR_INVALID_ARG, "M too large for 31-bit ids");
+  if (k > EX_K) return fail(IVHD_ERR_INVALID_ARG, "k=%d above the supported %d", k, EX_K);
+  if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail(IVHD_ERR_CUDA, "stream");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+
+  const int kp = (n + 7) / 8 * 8;
+  const int64_t n_tiles = (m + TQ - 1) / TQ, m_pad = n_tiles * TQ;
+  // candidates kept per query by the tensor-core pass; beyond KMAX-8 (or for
+  // tiny inputs) every query goes to the exact scan
+  const bool tc = k <= KMAX - 8 && m > 2 * (int64_t)KMAX;
+  const int keep = tc ? KMAX : 0;
+
+  double *dX = nullptr, *dD = nullptr;
+  float *dP = nullptr, *dN = nullptr, *cd2 = nullptr;
+  int32_t *dI = nullptr, *cid = nullptr;
+  int *flag = nullptr, *list = nullptr, *cnt = nullptr;
+  long long* bad = nullptr;
+  unsigned int* rmax_bits = nullptr;
+  int rc = IVHD_OK;
+  int n_fallback = 0;
+  double t_tc = 0, t_rr = 0;
+  cudaError_t e = cudaSuccess;
+  do {
+#define KTRY(call) \
+  if ((e = (call)) != cudaSuccess) break
+    KTRY(cudaMallocAsync(&dX, sizeof(double) * m * n, st));
+    KTRY(cudaMallocAsync(&dI, sizeof(int32_t) * m * k, st));
+    KTRY(cudaMallocAsync(&dD, sizeof(double) * m * k, st));
+    KTRY(cudaMallocAsync(&flag, sizeof(int) * m, st));
+    KTRY(cudaMallocAsync(&list, sizeof(int) * m, st));
+    KTRY(cudaMallocAsync(&cnt, sizeof(int), st));
+    KTRY(cudaMallocAsync(&bad, sizeof(long long), st));
+    KTRY(cudaMemcpyAsync(dX, x, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+    KTRY(cudaMemsetAsync(flag, 0, sizeof(int) * m, st));
+    KTRY(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+    const long long big = 0x7fffffffffffffffLL;
+    KTRY(cudaMemcpyAsync(bad, &big, sizeof big, cudaMemcpyHostToDevice, st));
+    if (metric == 1) {
+      k_normalize<<<sms * 8, 256, 0, st>>>(dX, m, n, bad);
+      long long hb = big;
+      KTRY(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, st));
+      KTRY(cudaStreamSynchronize(st));
+      if (hb != big) {
+        rc = fail(IVHD_ERR_INVALID_ARG, "zero-norm vector under cosine metric (row %lld)", hb);
+        break;
+      }
+    }
+    if (tc) {
+      KTRY(cudaMallocAsync(&dP, sizeof(float) * m_pad * kp, st));
+      KTRY(cudaMallocAsync(&dN, sizeof(float) * m_pad, st));
+      KTRY(cudaMallocAsync(&cid, sizeof(int32_t) * m * KMAX, st));
+      KTRY(cudaMallocAsync(&cd2, sizeof(float) * m * KMAX, st));
+      KTRY(cudaMallocAsync(&rmax_bits, sizeof(unsigned int), st));
+      KTRY(cudaMemsetAsync(rmax_bits, 0, sizeof(unsigned int), st));
+      k_pack<<<sms * 16, 256, 0, st>>>(dX, m, n, kp, m_pad, dP, dN);
+      k_max_norm<<<sms, 256, 0, st>>>(dN, m, rmax_bits);
+      unsigned int hr = 0;
+      KTRY(cudaMemcpyAsync(&hr, rmax_bits, sizeof hr, cudaMemcpyDeviceToHost, st));
+      KTRY(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+      KTRY(cudaStreamSynchronize(st));
+      const auto a = clk::now();
+      k_knn_tc<<<(unsigned)n_tiles, THREADS, SMEM_BYTES, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
+      KTRY(cudaGetLastError());
+      KTRY(cudaStreamSynchronize(st));
+      const auto b = clk::now();
+      t_tc = std::chrono::duration<double>(b - a).count();
+      float hrf;
+      memcpy(&hrf, &hr, sizeof hrf);
+      float rmax = sqrtf(hrf) * (1.f + 1e-6f);
+      if (metric == 1) rmax = 1.f + 1e-6f;
+      // error model (see k_rerank): fp32 sums of kp terms, generous factor 8
+      const float gamma = 8.f * (float)(kp + 8) * 5.96e-8f;
+      const float eps_in = 4.9e-4f;  // 2^-11 relative tf32 rounding, per coordinate
+      k_rerank<<<sms * 8, 256, 0, st>>>(dX, m, n, metric, k, keep, cid, cd2, dN, rmax, gamma, eps_in, dI, dD, flag);
+      KTRY(cudaGetLastError());
+      KTRY(cudaStreamSynchronize(st));
+      t_rr = std::chrono::duration<double>(clk::now() - b).count();
+    } else {
+      KTRY(cudaMemsetAsync(flag, 1, sizeof(int) * m, st));  // nonzero bytes: every row flagged
+    }
+    k_flag_list<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(flag, m, list, cnt);
+    KTRY(cudaMemcpyAsync(&n_fallback, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    KTRY(cudaStreamSynchronize(st));
+    if (n_fallback > 0) {
+      const size_t shb = (size_t)EX_THREADS * k * (8 + 4) * 2;
+      KTRY(cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+      k_exact<<<std::min(n_fallback, sms * 4), EX_THREADS, shb, st>>>(dX, m, n, metric, k, list, n_fallback, dI, dD);
+      KTRY(cudaGetLastError());
+    }
+    KTRY(cudaMemcpyAsync(nbr_out, dI, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, st));
+    KTRY(cudaMemcpyAsync(dist_out, dD, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
+    KTRY(cudaStreamSynchronize(st));
+#undef KTRY
+  } while (0);
+  cudaFreeAsync(dX, st); cudaFreeAsync(dI, st); cudaFreeAsync(dD, st); cudaFreeAsync(flag, st);
+  cudaFreeAsync(list, st); cudaFreeAsync(cnt, st); cudaFreeAsync(bad, st);
+  if (dP) cudaFreeAsync(dP, st);
+  if (dN) cudaFreeAsync(dN, st);
+  if (cid) cudaFreeAsync(cid, st);
+  if (cd2) cudaFreeAsync(cd2, st);
+  if (rmax_bits) cudaFreeAsync(rmax_bits, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (rc != IVHD_OK) return rc;
+  if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "kNN build: %s", cudaGetErrorString(e));
+  if (stats_out) {
+    stats_out[0] = t_tc;
+    stats_out[1] = t_rr;
+    stats_out[2] = (double)n_fallback;
+    stats_out[3] = std::chrono::duration<double>(clk::now() - t0).count();
+  }
+  return IVHD_OK;
+}
+
+}  // extern "C"

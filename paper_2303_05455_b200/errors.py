@@ -45,3 +45,24 @@ class NumericalDivergenceError(*_bases("NumericalDivergenceError", IvhdError)):
         Exception.__init__(self, f"embedding diverged at iteration {iteration}")
         self.iteration = iteration
         self.state = state
+
+
+class DegenerateMetricError(*_bases("DegenerateMetricError", IvhdError)):
+    """The metric cannot be evaluated on a row (zero-norm vector under cosine;
+    reference errors.py:30-38)."""
+
+    def __init__(self, message, row=None):
+        if row is not None:
+            message = f"{message} (row {row})"
+        Exception.__init__(self, message)
+        self.row = row
+
+
+class MalformedInputError(*_bases("MalformedInputError", IvhdError)):
+    """A file failed to parse (reference errors.py:12-20)."""
+
+    def __init__(self, message, row=None):
+        if row is not None:
+            message = f"{message} (row {row})"
+        Exception.__init__(self, message)
+        self.row = row
