@@ -46,13 +46,17 @@ namespace knn {
 constexpr int TQ = 128;       // queries per CTA (UMMA M)
 constexpr int TCN = 128;      // candidates per tile (UMMA N)
 constexpr int KC = 32;        // floats per K chunk (128 bytes per row)
-constexpr int KMAX = 32;      // approximate candidates kept per query
+constexpr int KMAX = 32;      // list slots per (epilogue group, query)
+constexpr int UMAX = 128;     // union of the group lists handed to the re-rank
 constexpr int STAGES = 4;     // smem ring depth (A chunk + B chunk per stage)
-constexpr int THREADS = 192;  // 6 warps
+#ifndef KNN_EPI_GROUPS
+#define KNN_EPI_GROUPS 4
+#endif
+constexpr int EG = KNN_EPI_GROUPS;       // epilogue groups: group g owns columns [g*TCN/EG, (g+1)*TCN/EG)
+constexpr int THREADS = 64 + 128 * EG;   // producer warp, MMA warp, 4*EG epilogue warps
 constexpr int CHUNK_BYTES = TQ * KC * 4;                // 16 KB
 constexpr int STAGE_BYTES = 2 * CHUNK_BYTES;            // A + B chunk
-constexpr int LIST_BYTES = 2 * KMAX * TQ * 4;           // sorted (d2, id) lists
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + LIST_BYTES + 1024;
+constexpr int LIST_BYTES = EG * 2 * KMAX * TQ * 4;      // per-group (d2, id) lists (host sizes them by keep)
 
 // byte offset of element (r, k) inside a chunk image with kc floats per row:
 // core matrices of 8 rows x 16 bytes; K-chunk stride (LBO) 128 bytes, 8-row
@@ -177,15 +181,46 @@ __global__ void k_normalize(double* __restrict__ X, int64_t m, int n, long long*
 }
 
 // ---------------------------------------------------------- candidate pass
+// RES: the query tile (all K chunks) is loaded once and stays in shared
+// memory (kp <= KP_RES); otherwise each ring stage carries the query chunk
+// next to the candidate chunk.
+constexpr int KP_RES = 256;
+constexpr int STAGES_RES = 4;
+// dynamic shared memory: [query tile (RES)] [ring] [EG x 2 x keep x TQ lists]
+inline int tc_smem_bytes(bool res, int kp, int keep) {
+  const int a = res ? (TQ * kp * 4 + 1023) / 1024 * 1024 : 0;
+  return a + (res ? STAGES_RES * CHUNK_BYTES : STAGES * STAGE_BYTES) + EG * 2 * keep * TQ * 4 + 1024;
+}
+
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  // producer-side wait: back off so the spin does not take issue slots from
+  // the epilogue warps sharing the SM sub-partition
+  uint32_t ok;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
+}
+
+template <bool RES>
 __global__ void __launch_bounds__(THREADS, 1)
     k_knn_tc(const float* __restrict__ P, const float* __restrict__ nrm, int64_t m, int kp, int n_tiles, int keep,
              int32_t* __restrict__ cand_id, float* __restrict__ cand_d2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* ring = smem;
-  float* lst_d = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);  // [KMAX][TQ]
-  int* lst_i = reinterpret_cast<int*>(lst_d + KMAX * TQ);               // [KMAX][TQ]
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accf[2], acce[2];
+  constexpr int NST = RES ? STAGES_RES : STAGES;
+  constexpr int SB = RES ? CHUNK_BYTES : STAGE_BYTES;  // bytes per ring stage
+  uint8_t* aq = smem;                                   // RES: resident query tile
+  uint8_t* ring = smem + (RES ? (TQ * kp * 4 + 1023) / 1024 * 1024 : 0);
+  float* lst_base = reinterpret_cast<float*>(ring + NST * SB);  // [EG][2][keep][TQ]
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[2], acce[2], abar;
   __shared__ uint32_t tmem_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -194,14 +229,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t tile_floats = (int64_t)TQ * kp;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 4);
+      mbar_init(&acce[b], 4 * EG);
     }
+    mbar_init(&abar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // 2 x 128 fp32 accumulator columns
@@ -219,17 +255,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
       const float* Aq = P + (int64_t)qt * tile_floats;
+      if constexpr (RES) {  // the whole query tile: one contiguous copy
+        mbar_expect_tx(&abar, (uint32_t)(tile_floats * 4));
+        bulk_g2s(aq, Aq, (uint32_t)(tile_floats * 4), &abar);
+      }
       int it = 0;
       for (int j = 0; j < n_tiles; ++j) {
         const float* Bt = P + (int64_t)j * tile_floats;
         for (int c = 0; c < nchunks; ++c, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          const int s = it % NST;
+          if (it >= NST) mbar_wait_sleep(&empty[s], ((it / NST) - 1) & 1);
           const uint32_t bytes = (uint32_t)TQ * min(KC, kp - c * KC) * 4;
-          uint8_t* st = ring + s * STAGE_BYTES;
-          mbar_expect_tx(&full[s], 2 * bytes);
-          bulk_g2s(st, Aq + (int64_t)c * TQ * KC, bytes, &full[s]);
-          bulk_g2s(st + CHUNK_BYTES, Bt + (int64_t)c * TQ * KC, bytes, &full[s]);
+          uint8_t* st = ring + s * SB;
+          if constexpr (RES) {
+            mbar_expect_tx(&full[s], bytes);
+            bulk_g2s(st, Bt + (int64_t)c * TQ * KC, bytes, &full[s]);
+          } else {
+            mbar_expect_tx(&full[s], 2 * bytes);
+            bulk_g2s(st, Aq + (int64_t)c * TQ * KC, bytes, &full[s]);
+            bulk_g2s(st + CHUNK_BYTES, Bt + (int64_t)c * TQ * KC, bytes, &full[s]);
+          }
         }
       }
     }
@@ -237,6 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_tf32(TQ, TCN);
+      if constexpr (RES) mbar_wait(&abar, 0);
       int it = 0;
       for (int j = 0; j < n_tiles; ++j) {
         const int b = j & 1;
@@ -244,12 +290,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const uint32_t dt = tbase + (uint32_t)(b * TCN);
         for (int c = 0; c < nchunks; ++c, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&full[s], (it / STAGES) & 1);
+          const int s = it % NST;
+          mbar_wait(&full[s], (it / NST) & 1);
           tc_fence_after();
           const int kc = min(KC, kp - c * KC);
-          const uint32_t sa = smem_u32(ring + s * STAGE_BYTES), sb = sa + CHUNK_BYTES;
+          const uint32_t sr = smem_u32(ring + s * SB);
+          const uint32_t sa = RES ? smem_u32(aq) + (uint32_t)(c * CHUNK_BYTES) : sr;
+          const uint32_t sb = RES ? sr : sr + CHUNK_BYTES;
+#ifndef KNN_SKIP_MMA
           for (int ks = 0; ks < kc / 8; ++ks) {
+#else
+          for (int ks = 0; ks < 0; ++ks) {
+#endif
             const uint64_t ad = umma_desc(sa + ks * 256, 128, (uint32_t)kc * 32);
             const uint64_t bd = umma_desc(sb + ks * 256, 128, (uint32_t)kc * 32);
             umma_tf32(dt, ad, bd, idesc, (c | ks) != 0);
@@ -261,59 +313,97 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // --------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lane quarter of this warp
+    // 4*EG warps: warp w reads TMEM lane quarter w % 4 (queries 32q..32q+31)
+    // and, in group g, columns [g*CG, (g+1)*CG) of every tile; each (group,
+    // query) keeps an unsorted list of its `keep` smallest approximate squared
+    // distances with the current maximum tracked (insert = overwrite the max,
+    // rescan).  Several warps per SM sub-partition hide the TMEM/branch latency.
+    constexpr int CG = TCN / EG;
+    const int ew = warp - 2, g = ew >> 2, q = warp & 3;
     const int r = q * 32 + lane;
     const int64_t qid = (int64_t)qt * TQ + r;
     const float nq = qid < m ? nrm[qid] : 0.f;
+    float* ld = lst_base + (size_t)g * 2 * keep * TQ;
+    int* li = reinterpret_cast<int*>(ld + keep * TQ);
     for (int i = 0; i < keep; ++i) {
-      lst_d[i * TQ + r] = INFINITY;
-      lst_i[i * TQ + r] = -1;
+      ld[i * TQ + r] = INFINITY;
+      li[i * TQ + r] = 0x7fffffff;
     }
-    float thr = INFINITY;
+    float thr = INFINITY;  // current maximum of the list
+    int pm = 0;            // its slot
+    float thq = INFINITY;  // thr - nq: a candidate passes if nc - 2 dot < thq
+    auto insert = [&](float d2, int cid) {
+      ld[pm * TQ + r] = d2;
+      li[pm * TQ + r] = cid;
+      float mx = -INFINITY;
+      for (int i = 0; i < keep; ++i) {
+        const float x = ld[i * TQ + r];
+        if (x > mx) {
+          mx = x;
+          pm = i;
+        }
+      }
+      thr = mx;
+      thq = thr - nq;
+    };
     for (int j = 0; j < n_tiles; ++j) {
       const int b = j & 1;
       mbar_wait(&accf[b], (j >> 1) & 1);
       tc_fence_after();
-      const float4* nc4 = reinterpret_cast<const float4*>(nrm + (int64_t)j * TCN);
+      const float4* nc4 = reinterpret_cast<const float4*>(nrm + (int64_t)j * TCN + g * CG);
+      const bool diag = j == qt;  // the only tile holding the query itself
 #pragma unroll 1
-      for (int h = 0; h < TCN / 32; ++h) {
+      for (int h = 0; h < CG / 32; ++h) {
         uint32_t v[32];
-        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TCN + h * 32), v);
-        if (h == TCN / 32 - 1) {
+        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TCN + g * CG + h * 32), v);
+        if (h == CG / 32 - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acce[b]);
         }
-        const int64_t c0 = (int64_t)j * TCN + h * 32;
+        const int c0 = j * TCN + g * CG + h * 32;
+#ifdef KNN_SKIP_EPI
+        if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) ld[r] = 0.f;
+        continue;
+#endif
+        float4 ncs[8];
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) ncs[i4] = __ldg(nc4 + h * 8 + i4);
 #pragma unroll
         for (int i4 = 0; i4 < 8; ++i4) {
-          const float4 nc = __ldg(nc4 + h * 8 + i4);
-          const float ncv[4] = {nc.x, nc.y, nc.z, nc.w};
+          const float ncv[4] = {ncs[i4].x, ncs[i4].y, ncs[i4].z, ncs[i4].w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int i = i4 * 4 + u;
-            const float d2 = fmaf(-2.f, __uint_as_float(v[i]), nq + ncv[u]);
-            const int64_t cid = c0 + i;
-            if (d2 < thr && cid != qid) {  // sorted insert; equal distances keep the smaller id first
-              int p = keep - 1;
-              while (p > 0 && lst_d[(p - 1) * TQ + r] > d2) {
-                lst_d[p * TQ + r] = lst_d[(p - 1) * TQ + r];
-                lst_i[p * TQ + r] = lst_i[(p - 1) * TQ + r];
-                --p;
-              }
-              lst_d[p * TQ + r] = d2;
-              lst_i[p * TQ + r] = (int)cid;
-              thr = lst_d[(keep - 1) * TQ + r];
+            const float t = fmaf(-2.f, __uint_as_float(v[i]), ncv[u]);  // d2 - nq
+            if (t < thq) {
+              if (!(diag && c0 + i == (int)qid)) insert(t + nq, c0 + i);
             }
           }
         }
       }
     }
-    if (qid < m) {
-      for (int i = 0; i < keep; ++i) {
-        cand_id[qid * KMAX + i] = lst_i[i * TQ + r];
-        cand_d2[qid * KMAX + i] = lst_d[i * TQ + r];
+    // hand-off: group 0 writes the union of the EG lists (EG * keep <= UMAX
+    // entries) and the certificate threshold T = min over groups of the
+    // group's final maximum: every rejected row had d2 >= its group's maximum.
+    asm volatile("barrier.sync 1, %0;" ::"r"(128 * EG) : "memory");
+    if (g == 0 && qid < m) {
+      float T = INFINITY;
+      int o = 0;
+      for (int gg = 0; gg < EG; ++gg) {
+        const float* gd = lst_base + (size_t)gg * 2 * keep * TQ;
+        const int* gi = reinterpret_cast<const int*>(gd + keep * TQ);
+        float mx = -INFINITY;
+        for (int i = 0; i < keep; ++i, ++o) {
+          const float x = gd[i * TQ + r];
+          const int xi = gi[i * TQ + r];
+          mx = fmaxf(mx, x);
+          cand_id[qid * UMAX + o] = xi == 0x7fffffff ? -1 : xi;
+        }
+        T = fminf(T, mx);
       }
+      for (; o < UMAX; ++o) cand_id[qid * UMAX + o] = -1;
+      cand_d2[qid] = T;
     }
   }
   // non-aligned barrier: the producer and MMA warps arrive diverged (lane 0 ran the loop)
@@ -349,39 +439,58 @@ __device__ __forceinline__ bool before(double da, int ia, double db, int ib) {
 
 // One warp per query: lane i re-scores candidate i in fp64, ranks by
 // (distance, index), writes the first k, and certifies the result.
-__global__ void k_rerank(const double* __restrict__ X, int64_t m, int n, int metric, int k, int keep,
+__global__ void k_rerank(const double* __restrict__ X, int64_t m, int n, int metric, int k, int n_union,
                          const int32_t* __restrict__ cand_id, const float* __restrict__ cand_d2,
                          const float* __restrict__ nrm, float rmax, float gamma, float eps_in,
                          int32_t* __restrict__ out_id, double* __restrict__ out_d, int* __restrict__ flag) {
+  constexpr int CPL = UMAX / 32;  // candidates per lane
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t qy = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; qy < m; qy += nw) {
-    int id = lane < keep ? cand_id[qy * KMAX + lane] : -1;
-    double d = INFINITY;
-    if (id >= 0) d = exact_dist(X, n, qy, id, metric);
-    else id = 0x7fffffff;
-    int rank = 0;
-    for (int o = 0; o < 32; ++o) {
-      const double od = __shfl_sync(0xffffffffu, d, o);
-      const int oi = __shfl_sync(0xffffffffu, id, o);
-      rank += (o != lane && before(od, oi, d, id)) ? 1 : 0;
+    int id[CPL];
+    double d[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      id[c] = cand_id[qy * UMAX + c * 32 + lane];
+      d[c] = INFINITY;
+      if (id[c] >= 0) d[c] = exact_dist(X, n, qy, id[c], metric);
+      else id[c] = 0x7fffffff;
     }
-    if (rank < k) {
-      out_id[qy * k + rank] = id;
-      out_d[qy * k + rank] = d;
+    int rank[CPL] = {};
+    for (int c2 = 0; c2 < CPL; ++c2) {
+      if (c2 * 32 >= n_union) break;
+      for (int o = 0; o < 32; ++o) {
+        const double od = __shfl_sync(0xffffffffu, d[c2], o);
+        const int oi = __shfl_sync(0xffffffffu, id[c2], o);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) rank[c] += before(od, oi, d[c], id[c]) ? 1 : 0;
+      }
     }
-    // certificate: every row outside the kept list had approximate squared
-    // distance >= T (the last kept value); its true distance is at least
+    double dk = 0.0;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      if (rank[c] < k) {
+        out_id[qy * k + rank[c]] = id[c];
+        out_d[qy * k + rank[c]] = d[c];
+      }
+      if (rank[c] == k - 1) dk = d[c];
+    }
+    // certificate: every row outside the union had approximate squared
+    // distance >= T; its true distance is at least
     //   sqrt(max(T - gamma (|q~| + R)^2, 0)) - eps_in (|q| + R)
     // (gamma: fp32 Gram-expansion error, eps_in: tf32 input rounding).
-    const double dk = __shfl_sync(0xffffffffu, d, __ffs(__ballot_sync(0xffffffffu, rank == k - 1)) - 1);
+    bool have = false;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) have |= rank[c] == k - 1;
+    const unsigned who = __ballot_sync(0xffffffffu, have);
+    dk = __shfl_sync(0xffffffffu, dk, __ffs(who) - 1);
     if (lane == 0) {
       bool ok = true;
-      if (m - 1 > keep) {
-        const double T = (double)cand_d2[qy * KMAX + keep - 1];
+      if (m - 1 > (int64_t)n_union) {
+        const double T = (double)cand_d2[qy];
         const double qn = sqrt((double)nrm[qy]) * (1.0 + 1e-6);
         const double s = qn + (double)rmax;
-        double lb = sqrt(fmax(T - (double)gamma * s * s, 0.0)) - (double)eps_in * s;
+        const double lb = sqrt(fmax(T - (double)gamma * s * s, 0.0)) - (double)eps_in * s;
         double dke = dk;
         if (metric == 1) dke = sqrt(2.0 * dk);  // cosine distance -> unit-row euclidean
         ok = isfinite(T) && lb > dke;
@@ -514,8 +623,11 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   const int64_t n_tiles = (m + TQ - 1) / TQ, m_pad = n_tiles * TQ;
   // candidates kept per query by the tensor-core pass; beyond KMAX-8 (or for
   // tiny inputs) every query goes to the exact scan
-  const bool tc = k <= KMAX - 8 && m > 2 * (int64_t)KMAX;
-  const int keep = tc ? KMAX : 0;
+  const bool tc = k + 4 <= std::min(KMAX, UMAX / EG) && m > 2 * (int64_t)UMAX;
+  // candidates kept per query and epilogue group (each group sees 1/EG of the
+  // rows): the union of the EG lists is re-ranked, so a group needs only a
+  // share of k plus slack; the insert cost grows ~keep^2
+  const int keep = tc ? std::min(std::min(KMAX, UMAX / EG), k + 4) : 0;
 
   double *dX = nullptr, *dD = nullptr;
   float *dP = nullptr, *dN = nullptr, *cd2 = nullptr;
@@ -555,18 +667,29 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
     if (tc) {
       KTRY(cudaMallocAsync(&dP, sizeof(float) * m_pad * kp, st));
       KTRY(cudaMallocAsync(&dN, sizeof(float) * m_pad, st));
-      KTRY(cudaMallocAsync(&cid, sizeof(int32_t) * m * KMAX, st));
-      KTRY(cudaMallocAsync(&cd2, sizeof(float) * m * KMAX, st));
+      KTRY(cudaMallocAsync(&cid, sizeof(int32_t) * m * UMAX, st));
+      KTRY(cudaMallocAsync(&cd2, sizeof(float) * m, st));
       KTRY(cudaMallocAsync(&rmax_bits, sizeof(unsigned int), st));
       KTRY(cudaMemsetAsync(rmax_bits, 0, sizeof(unsigned int), st));
       k_pack<<<sms * 16, 256, 0, st>>>(dX, m, n, kp, m_pad, dP, dN);
       k_max_norm<<<sms, 256, 0, st>>>(dN, m, rmax_bits);
       unsigned int hr = 0;
       KTRY(cudaMemcpyAsync(&hr, rmax_bits, sizeof hr, cudaMemcpyDeviceToHost, st));
-      KTRY(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+      int smem_max = 0;
+      cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+      smem_max -= 2048;  // static shared memory of the kernel
+      const bool res = tc_smem_bytes(true, kp, keep) <= smem_max;
+      const int shb = tc_smem_bytes(res, kp, keep);
+      if (shb > smem_max) {
+        rc = fail(IVHD_ERR_INVALID_ARG, "kNN: shared memory plan %d > %d bytes", shb, smem_max);
+        break;
+      }
+      KTRY(cudaFuncSetAttribute(k_knn_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+      KTRY(cudaFuncSetAttribute(k_knn_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
       KTRY(cudaStreamSynchronize(st));
       const auto a = clk::now();
-      k_knn_tc<<<(unsigned)n_tiles, THREADS, SMEM_BYTES, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
+      if (res) k_knn_tc<true><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
+      else k_knn_tc<false><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
       KTRY(cudaGetLastError());
       KTRY(cudaStreamSynchronize(st));
       const auto b = clk::now();
@@ -578,7 +701,7 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
       // error model (see k_rerank): fp32 sums of kp terms, generous factor 8
       const float gamma = 8.f * (float)(kp + 8) * 5.96e-8f;
       const float eps_in = 4.9e-4f;  // 2^-11 relative tf32 rounding, per coordinate
-      k_rerank<<<sms * 8, 256, 0, st>>>(dX, m, n, metric, k, keep, cid, cd2, dN, rmax, gamma, eps_in, dI, dD, flag);
+      k_rerank<<<sms * 8, 256, 0, st>>>(dX, m, n, metric, k, keep * EG, cid, cd2, dN, rmax, gamma, eps_in, dI, dD, flag);
       KTRY(cudaGetLastError());
       KTRY(cudaStreamSynchronize(st));
       t_rr = std::chrono::duration<double>(clk::now() - b).count();
