@@ -48,6 +48,10 @@ constexpr int TCN = 128;      // candidates per tile (UMMA N)
 constexpr int KC = 32;        // floats per K chunk (128 bytes per row)
 constexpr int KMAX = 32;      // list slots per (epilogue group, query)
 constexpr int UMAX = 128;     // union of the group lists handed to the re-rank
+#ifndef KNN_ACC_BUFS
+#define KNN_ACC_BUFS 4
+#endif
+constexpr int NACC = KNN_ACC_BUFS;  // TMEM accumulator buffers (128 columns each, <= 4)
 constexpr int STAGES = 4;     // smem ring depth (A chunk + B chunk per stage)
 #ifndef KNN_EPI_GROUPS
 #define KNN_EPI_GROUPS 4
@@ -209,6 +213,26 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
   }
 }
 
+// Rare path of the epilogue, kept out of line so the unrolled filter stays
+// small enough for the instruction cache: overwrite the list maximum with
+// (d2, cid), rescan for the new maximum; returns the new threshold - nq.
+__device__ __noinline__ float knn_insert(float* ld, int* li, int* pm_s, int r, int keep, float d2, int cid, float nq) {
+  const int pm = pm_s[r];
+  ld[pm * TQ + r] = d2;
+  li[pm * TQ + r] = cid;
+  float mx = -INFINITY;
+  int p = 0;
+  for (int i = 0; i < keep; ++i) {
+    const float x = ld[i * TQ + r];
+    if (x > mx) {
+      mx = x;
+      p = i;
+    }
+  }
+  pm_s[r] = p;
+  return mx - nq;
+}
+
 template <bool RES>
 __global__ void __launch_bounds__(THREADS, 1)
     k_knn_tc(const float* __restrict__ P, const float* __restrict__ nrm, int64_t m, int kp, int n_tiles, int keep,
@@ -220,8 +244,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* aq = smem;                                   // RES: resident query tile
   uint8_t* ring = smem + (RES ? (TQ * kp * 4 + 1023) / 1024 * 1024 : 0);
   float* lst_base = reinterpret_cast<float*>(ring + NST * SB);  // [EG][2][keep][TQ]
-  __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[2], acce[2], abar;
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[NACC], acce[NACC], abar;
   __shared__ uint32_t tmem_sh;
+  __shared__ int pm_sh[EG][TQ];  // slot of each list's current maximum
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x;
@@ -233,16 +258,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], 4 * EG);
     }
     mbar_init(&abar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // 2 x 128 fp32 accumulator columns
+  if (warp == 1) {  // NACC x 128 fp32 accumulator columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_sh)),
-                 "r"(256)
+                 "r"(NACC * TCN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     tc_fence_before();
@@ -285,8 +310,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       if constexpr (RES) mbar_wait(&abar, 0);
       int it = 0;
       for (int j = 0; j < n_tiles; ++j) {
-        const int b = j & 1;
-        if (j >= 2) mbar_wait(&acce[b], ((j >> 1) - 1) & 1);  // epilogue drained buffer b
+        const int b = j % NACC;
+        if (j >= NACC) mbar_wait(&acce[b], ((j / NACC) - 1) & 1);  // epilogue drained buffer b
         tc_fence_after();
         const uint32_t dt = tbase + (uint32_t)(b * TCN);
         for (int c = 0; c < nchunks; ++c, ++it) {
@@ -329,26 +354,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       ld[i * TQ + r] = INFINITY;
       li[i * TQ + r] = 0x7fffffff;
     }
-    float thr = INFINITY;  // current maximum of the list
-    int pm = 0;            // its slot
-    float thq = INFINITY;  // thr - nq: a candidate passes if nc - 2 dot < thq
-    auto insert = [&](float d2, int cid) {
-      ld[pm * TQ + r] = d2;
-      li[pm * TQ + r] = cid;
-      float mx = -INFINITY;
-      for (int i = 0; i < keep; ++i) {
-        const float x = ld[i * TQ + r];
-        if (x > mx) {
-          mx = x;
-          pm = i;
-        }
-      }
-      thr = mx;
-      thq = thr - nq;
-    };
+    int* pm_s = pm_sh[g];
+    pm_s[r] = 0;
+    float thq = INFINITY;  // list maximum - nq: a candidate passes if nc - 2 dot < thq
     for (int j = 0; j < n_tiles; ++j) {
-      const int b = j & 1;
-      mbar_wait(&accf[b], (j >> 1) & 1);
+      const int b = j % NACC;
+      mbar_wait(&accf[b], (j / NACC) & 1);
       tc_fence_after();
       const float4* nc4 = reinterpret_cast<const float4*>(nrm + (int64_t)j * TCN + g * CG);
       const bool diag = j == qt;  // the only tile holding the query itself
@@ -377,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int i = i4 * 4 + u;
             const float t = fmaf(-2.f, __uint_as_float(v[i]), ncv[u]);  // d2 - nq
             if (t < thq) {
-              if (!(diag && c0 + i == (int)qid)) insert(t + nq, c0 + i);
+              if (!(diag && c0 + i == (int)qid)) thq = knn_insert(ld, li, pm_s, r, keep, t + nq, c0 + i, nq);
             }
           }
         }
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(NACC * TCN) : "memory");
   }
 }
 
@@ -677,7 +688,9 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
       KTRY(cudaMemcpyAsync(&hr, rmax_bits, sizeof hr, cudaMemcpyDeviceToHost, st));
       int smem_max = 0;
       cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-      smem_max -= 2048;  // static shared memory of the kernel
+      cudaFuncAttributes fa{};
+      KTRY(cudaFuncGetAttributes(&fa, k_knn_tc<true>));
+      smem_max -= (int)fa.sharedSizeBytes;  // static shared memory of the kernel
       const bool res = tc_smem_bytes(true, kp, keep) <= smem_max;
       const int shb = tc_smem_bytes(res, kp, keep);
       if (shb > smem_max) {
