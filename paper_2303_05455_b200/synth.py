@@ -5,7 +5,7 @@ construction is excluded from every timing, as in the paper).
   (10 contiguous clusters, neighbours at small ring offsets).  numpy, O(M k).
 * `mixture_knn_graph` — exact kNN graph of a 10-cluster Gaussian mixture in
   N dimensions (the "YAHOO-shaped" 1.4M x 100 input of config C3).  Built on
-  the GPU by blocked brute force with torch (setup plumbing: matmul + topk);
+  the GPU by the package's exact kNN builder (knng.py, csrc/ivhd_knn.cu);
   ids are shuffled like real data, so the graph has realistic hubness and no
   id locality.
 """
@@ -40,26 +40,14 @@ def mixture_points(m, n, clusters=10, seed=0, spread=2.0):
     return x, labels
 
 
-def mixture_knn_graph(m, n=100, k=2, clusters=10, seed=0, device="cuda", block=4096):
-    """Brute-force (TF32) kNN of `mixture_points` on the GPU.  Returns
-    (neighbors (m,k) int32, distances (m,k) float64, labels)."""
-    import torch
+def mixture_knn_graph(m, n=100, k=2, clusters=10, seed=0, device=0, block=None):
+    """Exact kNN graph of `mixture_points`, built by this package's GPU kNN
+    builder (knng.build_exact_knn: tcgen05 candidate pass + fp64 re-rank).
+    Returns (neighbors (m,k) int32, distances (m,k) float64, labels)."""
+    from . import knng
 
+    if isinstance(device, str):
+        device = int(device.split(":")[1]) if ":" in device else 0
     x, labels = mixture_points(m, n, clusters, seed)
-    X = torch.from_numpy(x).to(device)
-    sq = (X * X).sum(dim=1)
-    nbr = torch.empty((m, k), dtype=torch.int64, device=device)
-    dst = torch.empty((m, k), dtype=torch.float32, device=device)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True  # input synthesis: speed over exact ties
-    try:
-        for s in range(0, m, block):
-            e = min(s + block, m)
-            d2 = sq[s:e, None] + sq[None, :] - 2.0 * (X[s:e] @ X.T)
-            d2[torch.arange(e - s, device=device), torch.arange(s, e, device=device)] = float("inf")
-            v, i = torch.topk(d2, k, dim=1, largest=False, sorted=True)
-            nbr[s:e] = i
-            dst[s:e] = v.clamp_min(0).sqrt()
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-    return (nbr.cpu().numpy().astype(np.int32), dst.cpu().numpy().astype(np.float64), labels)
+    g = knng.build_exact_knn(x.astype(np.float64), k, device=device)
+    return g.neighbors, g.distances, labels
