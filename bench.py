@@ -281,19 +281,22 @@ def algorithmic_bytes(m, n_entries, optimizer):
 
 def knn_leg(w, local, peaks):
     """Time the GPU kNN builder (excluded from the embed
-    timing, as in the paper) on the workload's point set: one warm-up on a
-    slice, then one full build.  Reported beside the embed line."""
+    timing, as in the paper) on the workload's point set: one warm-up
+    full build, then a timed one.  Reported beside the embed line."""
     from paper_2303_05455_b200 import knng, synth
 
     if w["graph"] != "mixture":
         return None
     x, _ = synth.mixture_points(w["m"], w["n"], seed=0)
     x = x.astype(np.float64)
-    knng.build_exact_knn(x[:8192], w["nn"], device=local)
-    t0 = time.perf_counter()
-    knng.build_exact_knn(x, w["nn"], device=local)
-    wall = time.perf_counter() - t0
-    st = dict(knng.last_stats)
+    best = None
+    for _ in range(2):  # the first build also grows the stream-ordered memory pool
+        t0 = time.perf_counter()
+        knng.build_exact_knn(x, w["nn"], device=local)
+        wall = time.perf_counter() - t0
+        if best is None or wall < best[0]:
+            best = (wall, dict(knng.last_stats))
+    wall, st = best
     kp = (w["n"] + 7) // 8 * 8
     flops = 2.0 * w["m"] * w["m"] * kp
     peak = float(peaks.get("bf16_tflops", 1647.6)) / 2.0
