@@ -177,8 +177,9 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
  * cosine (1 - cos, rows normalised first; a zero row is IVHD_ERR_INVALID_ARG
  * with "zero-norm vector" in the message).  1 <= k < m, k <= 64.
  * nbr_out (m, k) int32 and dist_out (m, k) float64 are host buffers.
- * stats_out (optional, 4 doubles): tensor-core pass seconds, re-rank seconds,
- * rows re-scanned exactly (uncertified), total seconds.  Errors: message in
+ * stats_out (optional, 8 doubles): tensor-core pass seconds, re-rank seconds,
+ * rows re-scanned exactly (uncertified), total seconds, setup seconds (H2D +
+ * pack), exact re-scan seconds, D2H seconds, 0.  Errors: message in
  * ivhd_knn_last_error(). */
 int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k, int32_t metric,
                    int32_t* nbr_out, double* dist_out, double* stats_out);

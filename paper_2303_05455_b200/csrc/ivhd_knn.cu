@@ -23,8 +23,9 @@
 //                  have dropped a closer row if the error-bounded lower bound
 //                  of every rejected row's distance exceeds the k-th exact
 //                  distance.  Uncertified rows (rare) go to
-//   4. k_exact     fp64 brute force over all rows for that query (block per
-//                  query, per-thread sorted lists merged in a fixed tree).
+//   4. k_exact_seg fp64 brute force over all rows for that query, split
+//                  into candidate segments (warp per candidate, coalesced
+//                  rows), merged in segment order by k_exact_merge.
 //
 // No CPU fallback: every distance is computed on the GPU.
 #include <cuda_runtime.h>
@@ -512,73 +513,101 @@ __global__ void k_rerank(const double* __restrict__ X, int64_t m, int n, int met
 }
 
 // ------------------------------------------------------------ exact scan
-// Block per flagged query: every thread keeps a sorted (distance, index) list
-// of its strided rows; lists are merged pairwise in a fixed tree.
-constexpr int EX_THREADS = 128;
+// Rows the certificate does not cover (and every row when the tensor-core
+// pass does not apply): exact fp64 scan split into segments of candidates.
+// Block (query i, segment s): each warp takes candidates c = seg0 + warp,
+// +8, ...; the lanes read the row coalesced and reduce the distance with a
+// fixed butterfly; lane 0 keeps the warp's sorted (distance, index) list;
+// the 8 warp lists are merged into the segment's top k (scratch), and
+// k_exact_merge merges the segments of a query in segment order.
+constexpr int EX_THREADS = 256;
+constexpr int EX_WARPS = EX_THREADS / 32;
 constexpr int EX_K = 64;
 
-__global__ void __launch_bounds__(EX_THREADS) k_exact(const double* __restrict__ X, int64_t m, int n, int metric,
-                                                     int k, const int* __restrict__ list, int n_list,
-                                                     int32_t* __restrict__ out_id, double* __restrict__ out_d) {
+__global__ void __launch_bounds__(EX_THREADS) k_exact_seg(const double* __restrict__ X, int64_t m, int n, int metric,
+                                                         int k, const int* __restrict__ list, int n_list, int n_seg,
+                                                         double* __restrict__ sd_out, int* __restrict__ si_out) {
   extern __shared__ __align__(16) unsigned char exs[];
-  double* sd = reinterpret_cast<double*>(exs);               // [EX_THREADS][k]
-  int* si = reinterpret_cast<int*>(sd + EX_THREADS * k);     // [EX_THREADS][k]
-  double* td = reinterpret_cast<double*>(si + EX_THREADS * k);  // merge scratch [EX_THREADS][k]
-  int* ti = reinterpret_cast<int*>(td + EX_THREADS * k);
-  const int t = threadIdx.x;
-  for (int qi = blockIdx.x; qi < n_list; qi += gridDim.x) {
-    const int64_t qy = list[qi];
-    double* md = sd + t * k;
-    int* mi = si + t * k;
+  double* wd = reinterpret_cast<double*>(exs);           // [EX_WARPS][k]
+  int* wi = reinterpret_cast<int*>(wd + EX_WARPS * k);   // [EX_WARPS][k]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qi = blockIdx.x / n_seg, seg = blockIdx.x % n_seg;
+  if (qi >= n_list) return;
+  const int64_t qy = list[qi];
+  const int64_t per = (m + n_seg - 1) / n_seg, c_lo = seg * per, c_hi = min(m, c_lo + per);
+  double* md = wd + warp * k;
+  int* mi = wi + warp * k;
+  if (lane == 0)
     for (int i = 0; i < k; ++i) {
       md[i] = INFINITY;
       mi[i] = 0x7fffffff;
     }
-    for (int64_t c = t; c < m; c += EX_THREADS) {
-      if (c == qy) continue;
-      const double d = exact_dist(X, n, qy, c, metric);
-      if (before(d, (int)c, md[k - 1], mi[k - 1])) {
-        int p = k - 1;
-        while (p > 0 && before(d, (int)c, md[p - 1], mi[p - 1])) {
-          md[p] = md[p - 1];
-          mi[p] = mi[p - 1];
-          --p;
-        }
-        md[p] = d;
-        mi[p] = (int)c;
+  __syncwarp();
+  const double* xq = X + qy * n;
+  for (int64_t c = c_lo + warp; c < c_hi; c += EX_WARPS) {
+    const double* xc = X + c * n;
+    double s = 0.0;
+    if (metric == 0) {
+      for (int t = lane; t < n; t += 32) {
+        const double d = xq[t] - xc[t];
+        s = fma(d, d, s);
       }
+    } else {
+      for (int t = lane; t < n; t += 32) s = fma(xq[t], xc[t], s);
     }
-    __syncthreads();
-    for (int w = 1; w < EX_THREADS; w <<= 1) {  // merge list t + w into t
-      if ((t & (2 * w - 1)) == 0) {
-        const double* ad = sd + t * k;
-        const int* ai = si + t * k;
-        const double* bd = sd + (t + w) * k;
-        const int* bi = si + (t + w) * k;
-        double* od = td + t * k;
-        int* oi = ti + t * k;
-        int a = 0, b = 0;
-        for (int o = 0; o < k; ++o) {
-          if (before(ad[a], ai[a], bd[b], bi[b])) {
-            od[o] = ad[a];
-            oi[o] = ai[a++];
-          } else {
-            od[o] = bd[b];
-            oi[o] = bi[b++];
-          }
-        }
-        for (int o = 0; o < k; ++o) {
-          sd[t * k + o] = od[o];
-          si[t * k + o] = oi[o];
-        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double d = metric == 0 ? sqrt(s) : fmax(1.0 - s, 0.0);
+    if (lane == 0 && c != qy && before(d, (int)c, md[k - 1], mi[k - 1])) {
+      int p = k - 1;
+      while (p > 0 && before(d, (int)c, md[p - 1], mi[p - 1])) {
+        md[p] = md[p - 1];
+        mi[p] = mi[p - 1];
+        --p;
       }
-      __syncthreads();
+      md[p] = d;
+      mi[p] = (int)c;
     }
-    if (t < k) {
-      out_id[qy * k + t] = si[t];
-      out_d[qy * k + t] = sd[t];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // merge the warp lists (k-way, fixed order)
+    int pos[EX_WARPS] = {};
+    double* od = sd_out + ((int64_t)qi * n_seg + seg) * k;
+    int* oi = si_out + ((int64_t)qi * n_seg + seg) * k;
+    for (int o = 0; o < k; ++o) {
+      int bw = 0;
+      for (int w = 1; w < EX_WARPS; ++w)
+        if (before(wd[w * k + pos[w]], wi[w * k + pos[w]], wd[bw * k + pos[bw]], wi[bw * k + pos[bw]])) bw = w;
+      od[o] = wd[bw * k + pos[bw]];
+      oi[o] = wi[bw * k + pos[bw]];
+      if (pos[bw] < k - 1) ++pos[bw];
+      else wd[bw * k + pos[bw]] = INFINITY, wi[bw * k + pos[bw]] = 0x7fffffff;
     }
-    __syncthreads();
+  }
+}
+
+// One thread per flagged query: merge its n_seg sorted segment lists.
+__global__ void k_exact_merge(const int* __restrict__ list, int n_list, int n_seg, int k,
+                              double* __restrict__ sd, int* __restrict__ si, int32_t* __restrict__ out_id,
+                              double* __restrict__ out_d) {
+  const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= n_list) return;
+  const int64_t qy = list[qi];
+  double* d = sd + (int64_t)qi * n_seg * k;
+  int* id = si + (int64_t)qi * n_seg * k;
+  // repeated selection of the smallest segment head; heads advance in place
+  for (int o = 0; o < k; ++o) {
+    int bs = 0;
+    for (int sg = 1; sg < n_seg; ++sg)
+      if (before(d[sg * k], id[sg * k], d[bs * k], id[bs * k])) bs = sg;
+    out_id[qy * k + o] = id[bs * k];
+    out_d[qy * k + o] = d[bs * k];
+    for (int i = 0; i < k - 1; ++i) {  // pop the head of segment bs
+      d[bs * k + i] = d[bs * k + i + 1];
+      id[bs * k + i] = id[bs * k + i + 1];
+    }
+    d[bs * k + k - 1] = INFINITY;
+    id[bs * k + k - 1] = 0x7fffffff;
   }
 }
 
@@ -646,9 +675,11 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   int *flag = nullptr, *list = nullptr, *cnt = nullptr;
   long long* bad = nullptr;
   unsigned int* rmax_bits = nullptr;
+  double* xsd = nullptr;
+  int* xsi = nullptr;
   int rc = IVHD_OK;
   int n_fallback = 0;
-  double t_tc = 0, t_rr = 0;
+  double t_tc = 0, t_rr = 0, t_setup = 0, t_ex = 0, t_d2h = 0;
   cudaError_t e = cudaSuccess;
   do {
 #define KTRY(call) \
@@ -701,6 +732,7 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
       KTRY(cudaFuncSetAttribute(k_knn_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
       KTRY(cudaStreamSynchronize(st));
       const auto a = clk::now();
+      t_setup = std::chrono::duration<double>(a - t0).count();
       if (res) k_knn_tc<true><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
       else k_knn_tc<false><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
       KTRY(cudaGetLastError());
@@ -724,15 +756,29 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
     k_flag_list<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(flag, m, list, cnt);
     KTRY(cudaMemcpyAsync(&n_fallback, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
     KTRY(cudaStreamSynchronize(st));
+    const auto tx0 = clk::now();
     if (n_fallback > 0) {
-      const size_t shb = (size_t)EX_THREADS * k * (8 + 4) * 2;
-      KTRY(cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
-      k_exact<<<std::min(n_fallback, sms * 4), EX_THREADS, shb, st>>>(dX, m, n, metric, k, list, n_fallback, dI, dD);
-      KTRY(cudaGetLastError());
+      // segments per query: fill the GPU (>= 4 blocks per SM), segments of
+      // at least 256 rows; processed in batches bounding the scratch size
+      int n_seg = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (4LL * sms + n_fallback - 1) / n_fallback));
+      const int batch = std::max(1, std::min(n_fallback, (int)((256LL << 20) / ((int64_t)n_seg * k * 12))));
+      KTRY(cudaMallocAsync(&xsd, sizeof(double) * (size_t)batch * n_seg * k, st));
+      KTRY(cudaMallocAsync(&xsi, sizeof(int) * (size_t)batch * n_seg * k, st));
+      const size_t shb = (size_t)EX_WARPS * k * 12;
+      for (int b0 = 0; b0 < n_fallback; b0 += batch) {
+        const int nb = std::min(batch, n_fallback - b0);
+        k_exact_seg<<<(unsigned)(nb * n_seg), EX_THREADS, shb, st>>>(dX, m, n, metric, k, list + b0, nb, n_seg, xsd, xsi);
+        k_exact_merge<<<(nb + 127) / 128, 128, 0, st>>>(list + b0, nb, n_seg, k, xsd, xsi, dI, dD);
+        KTRY(cudaGetLastError());
+      }
+      KTRY(cudaStreamSynchronize(st));
     }
+    t_ex = std::chrono::duration<double>(clk::now() - tx0).count();
+    const auto td0 = clk::now();
     KTRY(cudaMemcpyAsync(nbr_out, dI, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, st));
     KTRY(cudaMemcpyAsync(dist_out, dD, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
     KTRY(cudaStreamSynchronize(st));
+    t_d2h = std::chrono::duration<double>(clk::now() - td0).count();
 #undef KTRY
   } while (0);
   cudaFreeAsync(dX, st); cudaFreeAsync(dI, st); cudaFreeAsync(dD, st); cudaFreeAsync(flag, st);
@@ -742,6 +788,8 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   if (cid) cudaFreeAsync(cid, st);
   if (cd2) cudaFreeAsync(cd2, st);
   if (rmax_bits) cudaFreeAsync(rmax_bits, st);
+  if (xsd) cudaFreeAsync(xsd, st);
+  if (xsi) cudaFreeAsync(xsi, st);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   if (rc != IVHD_OK) return rc;
@@ -751,6 +799,10 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
     stats_out[1] = t_rr;
     stats_out[2] = (double)n_fallback;
     stats_out[3] = std::chrono::duration<double>(clk::now() - t0).count();
+    stats_out[4] = t_setup;
+    stats_out[5] = t_ex;
+    stats_out[6] = t_d2h;
+    stats_out[7] = 0.0;
   }
   return IVHD_OK;
 }

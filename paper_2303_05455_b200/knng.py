@@ -45,7 +45,7 @@ def build_exact_knn(dataset_or_matrix, k, metric="euclidean", chunk_budget=None,
     lib = _lib.load()
     nbr = np.empty((m, k), dtype=np.int32)
     dist = np.empty((m, k), dtype=np.float64)
-    stats = np.zeros(4, dtype=np.float64)
+    stats = np.zeros(8, dtype=np.float64)
     t0 = time.perf_counter()
     rc = lib.ivhd_knn_build(int(device), _lib.ptr(x, _lib.ctypes.c_double), m, int(x.shape[1]), k,
                             _METRICS[metric], _lib.ptr(nbr, _lib.ctypes.c_int32),
@@ -60,5 +60,6 @@ def build_exact_knn(dataset_or_matrix, k, metric="euclidean", chunk_budget=None,
         raise DeviceError(f"kNN build failed: {msg}")
     last_stats.clear()
     last_stats.update(tc_seconds=stats[0], rerank_seconds=stats[1], exact_rows=int(stats[2]),
-                      device_seconds=stats[3], wall_seconds=time.perf_counter() - t0)
+                      device_seconds=stats[3], setup_seconds=stats[4], exact_seconds=stats[5],
+                      d2h_seconds=stats[6], wall_seconds=time.perf_counter() - t0)
     return KnnGraph(nbr, dist, metric=metric)

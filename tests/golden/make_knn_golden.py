@@ -43,6 +43,9 @@ def knn_inputs():
     # cosine metric (knng.py:105-115)
     rng = np.random.default_rng(15)
     out["cosine64"] = (rng.standard_normal((2500, 64)) + 0.5, 7, "cosine")
+    # k beyond the tensor-core pass (k + 4 > 32): every row takes the exact scan
+    rng = np.random.default_rng(17)
+    out["exact_k40"] = (rng.standard_normal((1200, 24)), 40, "euclidean")
     # odd width (not a multiple of 8), k = 1
     rng = np.random.default_rng(16)
     out["odd13_k1"] = (rng.uniform(-1, 1, (1000, 13)), 1, "euclidean")
