@@ -13,6 +13,7 @@ Metrics: "euclidean" and "cosine" (knng.py:105-115, 185-189).  "precomputed"
 InvalidArgumentError.
 """
 
+import os
 import time
 
 import numpy as np
@@ -62,4 +63,67 @@ def build_exact_knn(dataset_or_matrix, k, metric="euclidean", chunk_budget=None,
     last_stats.update(tc_seconds=stats[0], rerank_seconds=stats[1], exact_rows=int(stats[2]),
                       device_seconds=stats[3], setup_seconds=stats[4], exact_seconds=stats[5],
                       d2h_seconds=stats[6], wall_seconds=time.perf_counter() - t0)
+    return KnnGraph(nbr, dist, metric=metric)
+
+
+# ------------------------------------------------------------- graph cache
+# The reference's binary cache (knng.py:286-332): b"IVHG", then <u4
+# [version=1, M, k, metric id, has_dist], the (M, k) <u4 neighbour block and,
+# if flagged, the (M, k) <f4 distance block.
+
+_CACHE_MAGIC = b"IVHG"
+_METRIC_IDS = {"euclidean": 0, "cosine": 1, "precomputed": 2}
+
+
+def cache_write(graph, path):
+    """Write `graph` in the reference's IVHG format (knng.py:286-300):
+    byte-identical to the reference writer."""
+    from .errors import MalformedInputError
+
+    has_dist = graph.distances is not None
+    metric = getattr(graph, "metric", "euclidean")
+    header = np.asarray([1, graph.neighbors.shape[0], graph.neighbors.shape[1], _METRIC_IDS[metric],
+                         int(has_dist)], dtype="<u4")
+    try:
+        with open(path, "wb") as fh:
+            fh.write(_CACHE_MAGIC)
+            fh.write(header.tobytes())
+            fh.write(np.ascontiguousarray(graph.neighbors, dtype="<u4").tobytes())
+            if has_dist:
+                fh.write(np.ascontiguousarray(graph.distances, dtype="<f4").tobytes())
+    except OSError as exc:
+        raise MalformedInputError(f"{path}: cannot write graph cache: {exc}")
+
+
+def cache_read(path, distances=True):
+    """Read an IVHG cache (knng.py:303-332).  The neighbour block is
+    memory-mapped, not copied: `run_embedding` hands the mapping straight to
+    the device CSR builder (ivhd_set_graph reads it once, H2D), so a 10^8-row
+    graph is never duplicated in host memory.  Same errors as the reference
+    (MalformedInputError on a bad magic, version or a truncated file)."""
+    from .errors import MalformedInputError
+
+    try:
+        with open(path, "rb") as fh:
+            head = fh.read(24)
+        size = os.path.getsize(path)
+    except OSError as exc:
+        raise MalformedInputError(f"{path}: cannot read graph cache: {exc}")
+    if head[:4] != _CACHE_MAGIC:
+        raise MalformedInputError(f"{path}: not a graph cache file")
+    if len(head) < 24:
+        raise MalformedInputError(f"{path}: truncated graph cache")
+    version, m, k, metric_id, has_dist = np.frombuffer(head[4:24], dtype="<u4")
+    if version != 1:
+        raise MalformedInputError(f"{path}: unsupported cache version {version}")
+    nbytes = int(m) * int(k) * 4
+    if size < 24 + nbytes * (1 + int(has_dist)):
+        raise MalformedInputError(f"{path}: truncated graph cache")
+    # ids < 2^31, so the <u4 block reads as int32 without conversion
+    nbr = np.memmap(path, dtype="<i4", mode="r", offset=24, shape=(int(m), int(k))) if nbytes else \
+        np.empty((int(m), int(k)), dtype=np.int32)
+    dist = None
+    if has_dist and distances and nbytes:
+        dist = np.memmap(path, dtype="<f4", mode="r", offset=24 + nbytes, shape=(int(m), int(k))).astype(np.float64)
+    metric = {v: key for key, v in _METRIC_IDS.items()}[int(metric_id)]
     return KnnGraph(nbr, dist, metric=metric)

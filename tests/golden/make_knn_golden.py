@@ -64,6 +64,11 @@ def main():
         arrays[f"{name}_dist"] = g.distances
         print(name, x.shape, k, metric)
     np.savez_compressed(os.path.join(HERE, "knn_graphs.npz"), **arrays)
+    # the reference's IVHG cache writer (knng.py:286-300) on one of the graphs
+    x, k, metric = knn_inputs()["cosine64"]
+    g = knng.build_exact_knn(x[:300], 4, metric="cosine")
+    knng.cache_write(g, os.path.join(HERE, "ref_cache_cosine.ivhg"))
+    knng.cache_write(knng.KnnGraph(g.neighbors, None), os.path.join(HERE, "ref_cache_nodist.ivhg"))
 
 
 if __name__ == "__main__":
