@@ -27,6 +27,8 @@
  *   ivhd_shard_* / ivhd_step_*      (new) vertex-range sharding
  *   ivhd_knn_build                  knng.build_exact_knn             knng.py:158-194
  *                                   (euclidean / cosine)
+ *   ivhd_neighbor_hit               metrics.neighbor_hit (points)    metrics.py:254-294
+ *
  */
 #ifndef IVHD_B200_H
 #define IVHD_B200_H
@@ -184,6 +186,16 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
 int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k, int32_t metric,
                    int32_t* nbr_out, double* dist_out, double* stats_out);
 const char* ivhd_knn_last_error(void);
+
+/* Label neighbour hit of an embedding (metrics.neighbor_hit, metrics.py:254-294)
+ * computed on `device`: y (m, dim) float64 host points (1 <= dim <= 3), labels
+ * (m) int32; cf_nn_out[j] (nn_max doubles) = fraction of same-label points
+ * among the j+1 nearest other points, averaged over all points.  Exact grid
+ * kNN, (distance, index) order.  1 <= nn_max < m, nn_max <= 128.  nbr_out:
+ * optional (m, nn_max) int32 neighbour ids.  Errors: ivhd_metrics_last_error(). */
+int ivhd_neighbor_hit(int device, const double* y, int64_t m, int32_t dim, const int32_t* labels,
+                      int32_t nn_max, double* cf_nn_out, int32_t* nbr_out);
+const char* ivhd_metrics_last_error(void);
 
 #ifdef __cplusplus
 }

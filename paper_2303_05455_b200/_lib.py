@@ -82,6 +82,9 @@ SIGNATURES = {
     "ivhd_step_finalize": (ctypes.c_int, [ctypes.c_void_p, c_f64p, c_f64p,
                                           ctypes.POINTER(ctypes.c_int)]),
     "ivhd_knn_last_error": (ctypes.c_char_p, []),
+    "ivhd_metrics_last_error": (ctypes.c_char_p, []),
+    "ivhd_neighbor_hit": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, c_i32p,
+                                         ctypes.c_int32, c_f64p, c_i32p]),
     "ivhd_knn_build": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_int32, c_i32p, c_f64p, c_f64p]),
 }

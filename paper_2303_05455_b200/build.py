@@ -13,7 +13,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", "ivhd_capi.cu"), os.path.join(HERE, "csrc", "ivhd_knn.cu")]
+SRC = [os.path.join(HERE, "csrc", "ivhd_capi.cu"), os.path.join(HERE, "csrc", "ivhd_knn.cu"),
+       os.path.join(HERE, "csrc", "ivhd_metrics.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "ivhd_step.cuh"), os.path.join(HERE, "csrc", "ivhd_rng.cuh"), os.path.join(ROOT, "include", "ivhd_b200.h")]
 OUT = os.path.join(HERE, "libivhd_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
