@@ -394,6 +394,7 @@ def gpu_arm(args, w):
 
     # ---------------- e2e: public API from host arrays (rank 0, N == 1)
     e2e = None
+    final_points = None
     if world == 1 and not args.no_e2e:
         # the step's input, the kNN graph, lives in pinned host memory
         nb_pinned = torch.empty(nb.shape, dtype=torch.int32, pin_memory=True).numpy()
@@ -410,6 +411,7 @@ def gpu_arm(args, w):
             if i:  # first call is warm-up
                 walls.append(time.perf_counter() - t0)
         final_stress = res.state.stress
+        final_points = res.embedding.points
         # H2D: the nn-id block (the layout and random partners are drawn on
         # the device); D2H: positions + deltas, the partners, the trace
         h2d = m * nb.shape[1] * 4
@@ -430,6 +432,18 @@ def gpu_arm(args, w):
     knn = None
     if world == 1 and rank == 0 and not args.no_knn:
         knn = knn_leg(w, local, peaks)
+    quality = None
+    if final_points is not None and w["graph"] == "mixture":
+        # label neighbour hit of the embedding (metrics.neighbor_hit, GPU grid kNN)
+        from paper_2303_05455_b200 import metrics, synth
+
+        labels = synth.mixture_labels(m, w["n"], seed=0)
+        metrics.neighbor_hit(final_points[:4096], labels[:4096], nn_max=100, device=local)  # warm-up
+        t0 = time.perf_counter()
+        cf_nn, cf = metrics.neighbor_hit(final_points, labels, nn_max=100, device=local)
+        quality = {"neighbor_hit_cf": cf, "cf_2": float(cf_nn[1]), "cf_10": float(cf_nn[9]),
+                   "seconds": time.perf_counter() - t0,
+                   "note": "metrics.neighbor_hit(nn_max=100) of the e2e embedding on the GPU (exact grid kNN)"}
 
     if rank == 0:
         peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -458,7 +472,7 @@ def gpu_arm(args, w):
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps * iters * (2 if sharded else 1), "clocks": clk.summary(),
             "final_stress_e2e": final_stress,
-            "knn": knn,
+            "knn": knn, "quality": quality,
         }
         print(json.dumps(line), flush=True)
     if sharded:

@@ -40,6 +40,13 @@ def mixture_points(m, n, clusters=10, seed=0, spread=2.0):
     return x, labels
 
 
+def mixture_labels(m, n, clusters=10, seed=0, spread=2.0):
+    """The labels of `mixture_points` without drawing the points (same stream)."""
+    rng = np.random.default_rng(seed)
+    rng.standard_normal((clusters, n)).astype(np.float32)
+    return rng.integers(0, clusters, size=m)
+
+
 def mixture_knn_graph(m, n=100, k=2, clusters=10, seed=0, device=0, block=None):
     """Exact kNN graph of `mixture_points`, built by this package's GPU kNN
     builder (knng.build_exact_knn: tcgen05 candidate pass + fp64 re-rank).
