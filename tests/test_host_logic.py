@@ -179,20 +179,23 @@ def test_errors_hierarchy():
     err = P.NumericalDivergenceError(7, state="s")
     assert isinstance(err, P.IvhdError) and err.iteration == 7 and err.state == "s"
     assert issubclass(P.InvalidArgumentError, P.IvhdError)
-    try:
-        import sys
+    import os
+    import subprocess
+    import sys
 
-        sys.path.insert(0, "/root/reference/pkg/src")
-        import ivhd.errors as ref  # available in the build container only
-    except Exception:
+    if not os.path.isdir("/root/reference/pkg/src"):  # build container only
         return
     # with the reference importable, callers catching its classes keep working
-    import importlib
-
-    from paper_2303_05455_b200 import errors as E
-
-    importlib.reload(E)
-    assert issubclass(E.InvalidArgumentError, ref.InvalidArgumentError)
+    # (fresh interpreter: reloading the module here would swap the classes
+    # under the other tests' feet)
+    code = ("import sys; sys.path.insert(0, '/root/reference/pkg/src'); import ivhd.errors as ref; "
+            "from paper_2303_05455_b200 import errors as E; "
+            "assert issubclass(E.InvalidArgumentError, ref.InvalidArgumentError); "
+            "assert issubclass(E.MalformedInputError, ref.MalformedInputError); "
+            "assert issubclass(E.DegenerateMetricError, ref.DegenerateMetricError)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
 
 
 def test_embedding_and_graph_types():
