@@ -52,6 +52,9 @@ WORKLOADS = {
                         iterations=2500, graph="mixture"),
     "c4": dict(m=10_000_000, n=0, nn=3, rn=1, c=0.1, optimizer="force-directed",
                iterations=200, graph="planted"),
+    # the paper's 10^8+ scale on ONE B200 (BASELINE configs[4] names 8 GPUs)
+    "c5": dict(m=100_000_000, n=0, nn=2, rn=1, c=0.1, optimizer="force-directed",
+               iterations=100, graph="planted"),
 }
 
 
@@ -455,7 +458,8 @@ def gpu_arm(args, w):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: 10-cluster Gaussian mixture, exact kNN graph from the package's GPU "
                     "builder (untimed here; timed separately under 'knn')",
-            "config": {"workload": f"{args.workload}: YAHOO-shaped M={m} N={w['n']} kNN graph, "
+            "config": {"workload": f"{args.workload}: " + (f"YAHOO-shaped M={m} N={w['n']} kNN graph, "
+                                   if w["graph"] == "mixture" else f"planted-cluster graph M={m}, ") +
                                    f"nn={w['nn']} rn={w['rn']} c={w['c']} {w['optimizer']}, "
                                    f"{iters} iterations per step",
                        "m": m, "connections": L, "iterations_per_step": iters,
