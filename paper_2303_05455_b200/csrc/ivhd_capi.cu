@@ -375,6 +375,16 @@ __global__ void k_degrees(const uint32_t* __restrict__ row_ptr, int64_t m, uint3
     deg[i] = row_ptr[i + 1] - row_ptr[i];
 }
 
+// Windowed relabelling key: windows of W consecutive ids stay in order, ids
+// inside a window are sorted by descending degree (descending sort on
+// (reversed window << 32 | degree)).
+__global__ void k_window_keys(const uint32_t* __restrict__ row_ptr, int64_t m, int64_t W,
+                              uint64_t* __restrict__ key) {
+  const int64_t nwin = (m + W - 1) / W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    key[i] = ((uint64_t)(nwin - 1 - i / W) << 32) | (uint64_t)(row_ptr[i + 1] - row_ptr[i]);
+}
+
 __global__ void k_inverse(const int32_t* __restrict__ perm, int64_t m, int32_t* __restrict__ inv) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -519,13 +529,35 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
     if ((e = dalloc(ctx, &deg2, 4 * m)) != cudaSuccess) break;
     if ((e = dalloc(ctx, &ids, 4 * m)) != cudaSuccess) break;
     if ((e = dalloc(ctx, &perm, 4 * m)) != cudaSuccess) break;
-    k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, deg);
     k_iota<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ids, m);
-    if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
-        cudaSuccess) break;
-    if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
-    if ((e = cub::DeviceRadixSort::SortPairsDescending(tmp, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
-        cudaSuccess) break;
+    static const int64_t window = [] {
+      const char* w = getenv("IVHD_ORDER_WINDOW");  // experiments: degree sort inside id windows
+      return w ? std::max<int64_t>(0, atoll(w)) : (int64_t)0;
+    }();
+    if (window > 0 && window < m) {
+      uint64_t *k1 = nullptr, *k2 = nullptr;
+      int eb = 33;
+      while (eb < 64 && ((int64_t)1 << (eb - 32)) < (m + window - 1) / window) ++eb;
+      do {
+        if ((e = dalloc(ctx, &k1, 8 * m)) != cudaSuccess) break;
+        if ((e = dalloc(ctx, &k2, 8 * m)) != cudaSuccess) break;
+        k_window_keys<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, window, k1);
+        if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, k1, k2, ids, perm, (int)m, 0, eb, st)) !=
+            cudaSuccess) break;
+        if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
+        e = cub::DeviceRadixSort::SortPairsDescending(tmp, tb, k1, k2, ids, perm, (int)m, 0, eb, st);
+      } while (0);
+      dfree(ctx, k1);
+      dfree(ctx, k2);
+      if (e != cudaSuccess) break;
+    } else {
+      k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, deg);
+      if ((e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
+          cudaSuccess) break;
+      if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
+      if ((e = cub::DeviceRadixSort::SortPairsDescending(tmp, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
+          cudaSuccess) break;
+    }
     if (ctx->pos_set) {
       // data is currently in the old order (ctx->perm / ctx->inv): re-order
       float* scratch = reinterpret_cast<float*>(ctx->stage);  // 32 bytes/vertex
