@@ -381,15 +381,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         float4 ncs[8];
 #pragma unroll
         for (int i4 = 0; i4 < 8; ++i4) ncs[i4] = __ldg(nc4 + h * 8 + i4);
+        // fast pass, branch-free: bit i = candidate i beats the threshold
+        unsigned msk = 0;
 #pragma unroll
         for (int i4 = 0; i4 < 8; ++i4) {
           const float ncv[4] = {ncs[i4].x, ncs[i4].y, ncs[i4].z, ncs[i4].w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int i = i4 * 4 + u;
-            const float t = fmaf(-2.f, __uint_as_float(v[i]), ncv[u]);  // d2 - nq
-            if (t < thq) {
-              if (!(diag && c0 + i == (int)qid)) thq = knn_insert(ld, li, pm_s, r, keep, t + nq, c0 + i, nq);
+            const float t = fmaf(-2.f, __uint_as_float(v[i4 * 4 + u]), ncv[u]);  // d2 - nq
+            msk |= t < thq ? (1u << (i4 * 4 + u)) : 0u;
+          }
+        }
+        if (msk) {  // rare: re-test in order against the moving threshold, insert
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float ncv[4] = {ncs[i4].x, ncs[i4].y, ncs[i4].z, ncs[i4].w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i4 * 4 + u;
+              if ((msk >> i) & 1u) {
+                const float t = fmaf(-2.f, __uint_as_float(v[i]), ncv[u]);
+                if (t < thq && !(diag && c0 + i == (int)qid))
+                  thq = knn_insert(ld, li, pm_s, r, keep, t + nq, c0 + i, nq);
+              }
             }
           }
         }
@@ -654,6 +668,14 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   if (m >= 0x7fffffffLL) return fail(IVHD_ERR_INVALID_ARG, "M too large for 31-bit ids");
   if (k > EX_K) return fail(IVHD_ERR_INVALID_ARG, "k=%d above the supported %d", k, EX_K);
   if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+  {  // keep freed stream-ordered memory pooled: returning GBs to the driver
+     // at every synchronisation costs seconds (as in ivhd_create)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   cudaStream_t st;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail(IVHD_ERR_CUDA, "stream");
   int sms = 148;

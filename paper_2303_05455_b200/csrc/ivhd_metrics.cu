@@ -265,6 +265,14 @@ int ivhd_neighbor_hit(int device, const double* y, int64_t m, int32_t dim, const
   if (nn_max > NH_MAX) return fail(IVHD_ERR_INVALID_ARG, "nn_max=%d above the supported %d", nn_max, NH_MAX);
   if (m >= 0x7fffffffLL) return fail(IVHD_ERR_INVALID_ARG, "M too large");
   if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+  {  // keep freed stream-ordered memory pooled: returning GBs to the driver
+     // at every synchronisation costs seconds (as in ivhd_create)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   cudaStream_t st;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail(IVHD_ERR_CUDA, "stream");
   int sms = 148;
