@@ -12,6 +12,7 @@ run into segments at phase boundaries / resampling points, and (c) talks to
 an observer between iterations when one is attached.
 """
 
+import sys
 import warnings
 from dataclasses import dataclass, field
 
@@ -368,6 +369,53 @@ def _apply_mutation(sess, key, value):
 # --------------------------------------------------------------- the loop
 
 
+class LazyPositions:
+    """Positions handed to an observer (steering fast
+    path): the device → host copy happens only when the observer reads them
+    (np.asarray, indexing, len, .copy(), any ndarray attribute), so an
+    observer that publishes a frame every N iterations (server.py:103-116)
+    pays the (M, dim) transfer once per frame, not once per iteration.  If the
+    observer keeps a reference past its return, the loop materialises the
+    object before the next iteration, so it always holds that iteration's
+    positions."""
+
+    __slots__ = ("_dev", "_arr", "shape")
+
+    def __init__(self, dev, m, dim):
+        self._dev = dev
+        self._arr = None
+        self.shape = (m, dim)
+
+    def _get(self):
+        if self._arr is None:
+            self._arr = self._dev.positions()
+            self._dev = None
+        return self._arr
+
+    materialize = _get
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._get()
+        if dtype is not None and a.dtype != dtype:
+            return a.astype(dtype)
+        return a.copy() if copy else a
+
+    def __len__(self):
+        return self.shape[0]
+
+    def __getitem__(self, key):
+        return self._get()[key]
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def __getattr__(self, name):  # ndarray API (copy, mean, min, tolist, ...)
+        return getattr(self._get(), name)
+
+    def __repr__(self):
+        return repr(self._get())
+
+
 def run_embedding(graph=None, config=None, dataset=None, helper_graph=None, observer=None,
                   threads=1, device=0):
     """Execute a full embedding run on the GPU (engine.py:312-414).
@@ -430,7 +478,7 @@ def run_embedding(graph=None, config=None, dataset=None, helper_graph=None, obse
             diverged(it, stress, done)
         ran += done
         if observer is not None:
-            positions = dev.positions()
+            positions = LazyPositions(dev, sess.m, sess.dim)
             energy = float(stress[0])
             state.positions = positions
             state.iteration = it + 1
@@ -438,6 +486,8 @@ def run_embedding(graph=None, config=None, dataset=None, helper_graph=None, obse
             snapshot = {"c": sess.c, "b": float(step[0]), "optimizer": config.optimizer,
                         "phase": _phase_name(rnn_on, l1_on)}
             requested = observer(it, positions, energy, snapshot)
+            if sys.getrefcount(positions) > 3:  # kept by the observer (or state): pin this iteration's values
+                positions.materialize()
             for key, value in (requested or {}).items():
                 applied = _apply_mutation(sess, key, value)
                 if applied is not None:
