@@ -221,7 +221,11 @@ def test_observer_positions_are_lazy_and_pinned_when_kept():
         np.testing.assert_array_equal(np.asarray(kept[it]), eager[it])
     # frame every 50 iterations: the per-iteration device round trip without a
     # full position copy (recorded, not asserted: timing is informative only)
+    def framer(it, p, e, prm):
+        if it % 50 == 0:
+            np.asarray(p).sum()
+
     t0 = time.perf_counter()
     run_embedding(graph=KnnGraph(nb), config=EmbeddingConfig(nn=2, rn=1, c=0.1, iterations=300, seed=3),
-                  observer=lambda it, p, e, prm: np.asarray(p).sum() if it % 50 == 0 else None)
+                  observer=framer)
     print(f"observer fast path: {(time.perf_counter() - t0) / 300 * 1e6:.0f} us/iteration")
