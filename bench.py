@@ -48,8 +48,10 @@ WORKLOADS = {
                iterations=2000, graph="mixture"),
     "c2-adadelta": dict(m=70_000, n=784, nn=5, rn=1, c=0.01, optimizer="adadelta",
                         iterations=2500, graph="mixture"),
+    # the default alpha (0.02) diverges on this hub-heavy synthetic graph in the
+    # reference algorithm too (oracle, fp64: iteration 74; tools/nesterov_check.py)
     "c2-nesterov": dict(m=70_000, n=784, nn=5, rn=1, c=0.01, optimizer="nesterov",
-                        iterations=2500, graph="mixture"),
+                        iterations=2500, graph="mixture", alpha=2e-4),
     "c4": dict(m=10_000_000, n=0, nn=3, rn=1, c=0.1, optimizer="force-directed",
                iterations=200, graph="planted"),
     # the paper's 10^8+ scale on ONE B200 (BASELINE configs[4] names 8 GPUs)
@@ -205,7 +207,7 @@ def cpu_sample(nb, w, budget_s=15.0, threads=None):
 
     threads = threads or os.cpu_count() or 1
     run = OracleRun(nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=10**9, seed=0,
-                    optimizer=w["optimizer"], threads=threads)
+                    optimizer=w["optimizer"], threads=threads, opt=_opt(w))
     t0 = time.perf_counter()
     run.step()
     t1 = time.perf_counter() - t0
@@ -221,6 +223,12 @@ def cpu_sample(nb, w, budget_s=15.0, threads=None):
             "s_per_iteration": dt / n}
 
 
+def _opt(w):
+    from paper_2303_05455_b200 import OptimizerParams
+
+    return OptimizerParams(alpha=w["alpha"]) if "alpha" in w else None
+
+
 def reference_arm(args, w):
     """--impl reference: CPU implementation of the path on all host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -232,7 +240,7 @@ def reference_arm(args, w):
 
     threads = os.cpu_count() or 1
     run = OracleRun(nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=10**9, seed=0,
-                    optimizer=w["optimizer"], threads=threads)
+                    optimizer=w["optimizer"], threads=threads, opt=_opt(w))
     L = (w["nn"] + w["rn"]) * w["m"]
     per_step = max(1, args.ref_iters)
     for _ in range(args.warmup):
@@ -355,7 +363,7 @@ def gpu_arm(args, w):
         dev = ShardedEmbedding(m, 2, rank, world, device=local, stream=stream.cuda_stream)
     else:
         dev = DeviceEmbedding(m, 2, device=local, stream=stream.cuda_stream)
-    dev.set_optimizer(resolve_optimizer(w["optimizer"], m))
+    dev.set_optimizer(resolve_optimizer(w["optimizer"], m, opt=_opt(w)))
     dev.set_positions(y0)
     dev.set_graph(0, nn_sets, rn)
     dev.snapshot()
@@ -404,7 +412,7 @@ def gpu_arm(args, w):
         nb_pinned[...] = nb
         graph = KnnGraph(nb_pinned)
         cfg = EmbeddingConfig(nn=w["nn"], rn=w["rn"], c=w["c"], iterations=iters, seed=0,
-                              optimizer=w["optimizer"])
+                              optimizer=w["optimizer"], opt=_opt(w))
         walls = []
         for i in range(1 + args.e2e_steps):
             torch.cuda.synchronize()
