@@ -207,7 +207,8 @@ def cpu_sample(nb, w, budget_s=15.0, threads=None):
 
     threads = threads or os.cpu_count() or 1
     run = OracleRun(nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=10**9, seed=0,
-                    optimizer=w["optimizer"], threads=threads, opt=_opt(w))
+                    optimizer=w["optimizer"], threads=threads,
+                    opt={"alpha": w["alpha"]} if "alpha" in w else None)
     t0 = time.perf_counter()
     run.step()
     t1 = time.perf_counter() - t0
@@ -240,7 +241,8 @@ def reference_arm(args, w):
 
     threads = os.cpu_count() or 1
     run = OracleRun(nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=10**9, seed=0,
-                    optimizer=w["optimizer"], threads=threads, opt=_opt(w))
+                    optimizer=w["optimizer"], threads=threads,
+                    opt={"alpha": w["alpha"]} if "alpha" in w else None)
     L = (w["nn"] + w["rn"]) * w["m"]
     per_step = max(1, args.ref_iters)
     for _ in range(args.warmup):
