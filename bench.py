@@ -483,6 +483,14 @@ def gpu_arm(args, w):
                          "algorithmic_bytes_per_launch": nbytes,
                          "note": f"algorithmic bytes {nbytes} per iteration (8L+36M) / device time "
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
+            "roofline_gather": {
+                "bound": "l1tex->xbar requests", "achieved": n_entries / s_iter / 1e9,
+                "peak": 148 * float(peaks.get("sm_max_mhz", 1965.0)) / 1e3, "unit": "G requests/s",
+                "frac": (n_entries / s_iter) / (148 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6),
+                "note": "the binding unit per ncu (profiles/r01_step_kernel_ncu.txt): every symmetrised "
+                        "entry's 8-byte neighbour gather misses L1 and is one L1->crossbar request; the "
+                        "interface issues ~1 request/cycle/SM (l1tex__m_l1tex2xbar_req_cycles_active); "
+                        "achieved = 2L requests per iteration / device time per iteration"},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps * iters * (2 if sharded else 1), "clocks": clk.summary(),
             "final_stress_e2e": final_stress,
