@@ -400,7 +400,7 @@ __device__ void finalize_warp(const StepArgs& A, const double4* src, int n) {
   const int lane = threadIdx.x & 31;
   const double2* p2 = reinterpret_cast<const double2*>(src);
   double4 s = make_double4(0, 0, 0, 0);
-  constexpr int kBatch = 8;  // loads in flight per lane (L2, bypassing L1)
+  constexpr int kBatch = 16;  // loads in flight per lane (L2, bypassing L1): 444 block partials in one round trip
   for (int t0 = lane; t0 < n; t0 += 32 * kBatch) {
     double2 a[kBatch], b[kBatch];
 #pragma unroll
@@ -641,11 +641,10 @@ constexpr int kUnitCache = IVHD_UNIT_CACHE;  // unit words cached per block
 // the slot count D <= 8 is a template constant, all D column reads and gathers
 // are issued first, then ~20 instructions per entry.  Slots past the lane's
 // last entry are self pairs (zero contribution).
-template <int D, bool GCOL, bool SPOS = false>
+template <int D, bool GCOL>
 __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G, int deg,
                                          const float* __restrict__ Yin, uint32_t v, float y0, float y1, float c,
-                                         long long gstep, float (&f)[2], float& e,
-                                         const float2* __restrict__ gp = nullptr) {
+                                         long long gstep, float (&f)[2], float& e) {
   uint32_t cw[D];
   float2 p[D];
 #pragma unroll
@@ -653,15 +652,11 @@ __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G,
 #pragma unroll
   for (int q = 0; q < D; ++q) {
     p[q] = make_float2(y0, y1);
-    if constexpr (SPOS) {  // neighbour positions already staged in shared memory
-      if (q < deg) p[q] = gp[q * G];
-    } else {
 #ifdef IVHD_ABLATE_GATHER  // timing experiment only: no random traffic (wrong results)
-      if (q < deg) p[q] = __ldg(reinterpret_cast<const float2*>(Yin) + (v ^ 1u));
+    if (q < deg) p[q] = __ldg(reinterpret_cast<const float2*>(Yin) + (v ^ 1u));
 #else
-      if (q < deg) p[q] = ld_pos(reinterpret_cast<const float2*>(Yin) + (cw[q] & kIdMask));
+    if (q < deg) p[q] = ld_pos(reinterpret_cast<const float2*>(Yin) + (cw[q] & kIdMask));
 #endif
-    }
   }
   float fx = f[0], fy = f[1], ee = e;
   unsigned dmask = 0;
@@ -696,55 +691,29 @@ __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G,
   e = ee;
 }
 
-#ifndef IVHD_GATHER_STAGING
-#define IVHD_GATHER_STAGING 0
-#endif
-#ifndef IVHD_GS_STAGES
-#define IVHD_GS_STAGES 3
-#endif
-// Gather staging (2-D, binary, L2, no look-ahead — every BASELINE config):
-// each consumer thread copies the neighbour positions of ITS entries of unit
-// k+1 into that unit's stage with 8-byte cp.async before computing unit k, so
-// the random loads are in flight during a whole unit of compute (software
-// pipelining; a thread later reads back only what it gathered itself).
-template <int DIM, int OPT, bool WEIGHTED, int NORM>
-__host__ __device__ constexpr bool gather_staged() {
-  return IVHD_GATHER_STAGING && DIM == 2 && !WEIGHTED && NORM == 0 && OPT != OPT_NEST;
-}
-
 // Shared-memory layout of one ring stage.
-template <int DIM, int OPT, bool GS>
+template <int DIM, int OPT>
 struct StageLayout {
-  static constexpr int STAGES = GS ? IVHD_GS_STAGES : kStages;
+  static constexpr int STAGES = kStages;
   static constexpr int YS = Layout<DIM, OPT>::YS, SS = Layout<DIM, OPT>::SS;
   static constexpr int RP_BYTES = ((kBlock + 1) * 4 + 15) / 16 * 16 + 16;
   static constexpr int COL_BYTES = kColCap * 4 + 32;
-  static constexpr int GP_BYTES = GS ? kColCap * 8 + 16 : 0;
   static constexpr int Y_BYTES = kBlock * YS * 4;
   static constexpr int S_BYTES = kBlock * (SS > 0 ? SS : 1) * 4;
-  static constexpr int RP_OFF = 0, COL_OFF = RP_BYTES, GP_OFF = COL_OFF + COL_BYTES, Y_OFF = GP_OFF + GP_BYTES,
-                       S_OFF = Y_OFF + Y_BYTES;
+  static constexpr int RP_OFF = 0, COL_OFF = RP_BYTES, Y_OFF = COL_OFF + COL_BYTES, S_OFF = Y_OFF + Y_BYTES;
   static constexpr int BYTES = S_OFF + S_BYTES;
 };
 
 template <int DIM, int OPT, bool WEIGHTED, int NORM>
 __host__ __device__ constexpr int step_smem_bytes() {
-  using SL = StageLayout<DIM, OPT, gather_staged<DIM, OPT, WEIGHTED, NORM>()>;
+  using SL = StageLayout<DIM, OPT>;
   return SL::STAGES * SL::BYTES;
 }
 
 template <int DIM, int OPT, bool WEIGHTED, int NORM>
 __host__ __device__ constexpr int step_min_blocks() {
-  return gather_staged<DIM, OPT, WEIGHTED, NORM>() && IVHD_GS_STAGES >= 3 ? 2 : IVHD_MINBLOCKS;
+  return IVHD_MINBLOCKS;
 }
-
-// 8-byte cp.async gather into shared memory, per-thread commit groups
-__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst_smem)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Per-stage metadata written by the producer before it arrives on the
 // stage's barriers (release) and read by consumers after the wait (acquire).
@@ -771,9 +740,8 @@ constexpr int kConsumerWarps = kBlock / 32;
 
 template <int DIM, int OPT, bool WEIGHTED, int NORM>
 __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, NORM>()) step_kernel(StepArgs A) {
-  constexpr bool GS = gather_staged<DIM, OPT, WEIGHTED, NORM>();
   using L = Layout<DIM, OPT>;
-  using SL = StageLayout<DIM, OPT, GS>;
+  using SL = StageLayout<DIM, OPT>;
   constexpr int kStages = SL::STAGES;
   constexpr bool NEST = (OPT == OPT_NEST);
   constexpr int SSX = L::SS > 0 ? L::SS : 1;
@@ -944,42 +912,11 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       bc1 = (float)(1.0 / (1.0 - pow((double)A.h.gv, tt)));
       bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
     }
-    // gather staging: this thread's neighbour positions of unit k -> stage
-    auto own_gathers = [&](int k) {
-      const int s = k % kStages;
-      const uint32_t par = (uint32_t)(k / kStages) & 1;
-      mbar_wait(&bar_r[s], par);
-      mbar_wait(&bar_b[s], par);
-      if (meta[s].staged) {
-        unsigned char* st = smem_raw + s * SL::BYTES;
-        const int pk = meta[s].packed, lgG = pk & 7, G = 1 << lgG, lg = tid & (G - 1), grp = tid >> lgG;
-        if (grp < meta[s].nv) {
-          const uint32_t* rp = reinterpret_cast<const uint32_t*>(st + SL::RP_OFF);
-          const uint32_t* cols = reinterpret_cast<const uint32_t*>(st + SL::COL_OFF) + meta[s].col_off;
-          float2* gp = reinterpret_cast<float2*>(st + SL::GP_OFF);
-          const float2* Y2 = reinterpret_cast<const float2*>(Yin);
-          const int e0 = (int)rp[0], b = (int)rp[grp] - e0, deg = (int)rp[grp + 1] - e0 - b;
-          for (int e = b + lg; e < b + deg; e += G) cp_async8(gp + e, Y2 + (cols[e] & kIdMask));
-        }
-      }
-      cp_async_commit();
-    };
-    if constexpr (GS) {
-      if (my_units > 0) own_gathers(0);
-    }
     for (int k = 0; k < my_units; ++k) {
       const int u = blockIdx.x + k * grid;
       const int s = k % kStages;
       unsigned char* st = smem_raw + s * SL::BYTES;
       const uint32_t par = (uint32_t)(k / kStages) & 1;
-      if constexpr (GS) {
-        if (k + 1 < my_units) {
-          own_gathers(k + 1);
-          cp_async_wait<1>();  // unit k's positions have landed (in flight during unit k-1)
-        } else {
-          cp_async_wait<0>();
-        }
-      }
       mbar_wait(&bar_r[s], par);
       mbar_wait(&bar_a[s], par);
       mbar_wait(&bar_b[s], par);
@@ -1035,31 +972,8 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
                   fast_row<8, GC>(cb + c0 * G, G, nl - c0, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e);
               }
             };
-            if constexpr (GS) {
-              if (staged) {  // columns and neighbour positions both in shared memory
-                const uint32_t* cb = colst + (beg - e0 + coff) + lg;
-                const float2* gpb = reinterpret_cast<const float2*>(st + SL::GP_OFF) + (beg - e0) + lg;
-                if (slots <= 8) {
-                  switch (slots) {
-#define IVHD_FAST_CASE(D) \
-  case D: fast_row<D, false, true>(cb, G, nl, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e, gpb); break;
-                    IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
-                    IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
-#undef IVHD_FAST_CASE
-                    default: break;
-                  }
-                } else {
-                  for (int c0 = 0; c0 < nl; c0 += 8)
-                    fast_row<8, false, true>(cb + c0 * G, G, nl - c0, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e,
-                                             gpb + c0 * G);
-                }
-              } else {
-                run(std::true_type{}, A.col + beg + lg);
-              }
-            } else {
-              if (staged) run(std::false_type{}, colst + (beg - e0 + coff) + lg);
-              else run(std::true_type{}, A.col + beg + lg);
-            }
+            if (staged) run(std::false_type{}, colst + (beg - e0 + coff) + lg);
+            else run(std::true_type{}, A.col + beg + lg);
             f[0] = ff[0];
             f[1] = ff[1];
           }
