@@ -45,22 +45,24 @@
 namespace knn {
 
 constexpr int TQ = 128;       // queries per CTA (UMMA M)
-constexpr int TCN = 128;      // candidates per tile (UMMA N)
+#ifndef KNN_TCN
+#define KNN_TCN 256
+#endif
+constexpr int TCN = KNN_TCN;  // candidates per tile (UMMA N): TCN/TQ consecutive 128-row images
 constexpr int KC = 32;        // floats per K chunk (128 bytes per row)
 constexpr int KMAX = 32;      // list slots per (epilogue group, query)
 constexpr int UMAX = 128;     // union of the group lists handed to the re-rank
-#ifndef KNN_ACC_BUFS
-#define KNN_ACC_BUFS 4
-#endif
-constexpr int NACC = KNN_ACC_BUFS;  // TMEM accumulator buffers (128 columns each, <= 4)
+constexpr int NACC = 512 / TCN;  // TMEM accumulator buffers (TCN columns each; 512 columns in all)
+constexpr int HALVES = TCN / TQ;
 constexpr int STAGES = 4;     // smem ring depth (A chunk + B chunk per stage)
 #ifndef KNN_EPI_GROUPS
 #define KNN_EPI_GROUPS 4
 #endif
 constexpr int EG = KNN_EPI_GROUPS;       // epilogue groups: group g owns columns [g*TCN/EG, (g+1)*TCN/EG)
 constexpr int THREADS = 64 + 128 * EG;   // producer warp, MMA warp, 4*EG epilogue warps
-constexpr int CHUNK_BYTES = TQ * KC * 4;                // 16 KB
-constexpr int STAGE_BYTES = 2 * CHUNK_BYTES;            // A + B chunk
+constexpr int CHUNK_BYTES = TQ * KC * 4;                // 16 KB: one 128-row image chunk
+constexpr int BCHUNK_BYTES = HALVES * CHUNK_BYTES;      // candidate chunk (TCN rows)
+constexpr int STAGE_BYTES = CHUNK_BYTES + BCHUNK_BYTES; // A + B chunk (query tile not resident)
 constexpr int LIST_BYTES = EG * 2 * KMAX * TQ * 4;      // per-group (d2, id) lists (host sizes them by keep)
 
 // byte offset of element (r, k) inside a chunk image with kc floats per row:
@@ -192,9 +194,9 @@ __global__ void k_normalize(double* __restrict__ X, int64_t m, int n, long long*
 constexpr int KP_RES = 256;
 constexpr int STAGES_RES = 4;
 // dynamic shared memory: [query tile (RES)] [ring] [EG x 2 x keep x TQ lists]
-inline int tc_smem_bytes(bool res, int kp, int keep) {
+inline int tc_smem_bytes(bool res, int kp, int keep, int nst) {
   const int a = res ? (TQ * kp * 4 + 1023) / 1024 * 1024 : 0;
-  return a + (res ? STAGES_RES * CHUNK_BYTES : STAGES * STAGE_BYTES) + EG * 2 * keep * TQ * 4 + 1024;
+  return a + nst * (res ? BCHUNK_BYTES : STAGE_BYTES) + EG * 2 * keep * TQ * 4 + 1024;
 }
 
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
@@ -237,15 +239,16 @@ __device__ __noinline__ float knn_insert(float* ld, int* li, int* pm_s, int r, i
 template <bool RES>
 __global__ void __launch_bounds__(THREADS, 1)
     k_knn_tc(const float* __restrict__ P, const float* __restrict__ nrm, int64_t m, int kp, int n_tiles, int keep,
-             int32_t* __restrict__ cand_id, float* __restrict__ cand_d2) {
+             int nst, int32_t* __restrict__ cand_id, float* __restrict__ cand_d2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  constexpr int NST = RES ? STAGES_RES : STAGES;
-  constexpr int SB = RES ? CHUNK_BYTES : STAGE_BYTES;  // bytes per ring stage
+  constexpr int NSTMAX = RES ? STAGES_RES : STAGES;
+  const int NST = nst;                                  // ring depth (<= NSTMAX, sized by the host)
+  constexpr int SB = RES ? BCHUNK_BYTES : STAGE_BYTES;  // bytes per ring stage
   uint8_t* aq = smem;                                   // RES: resident query tile
   uint8_t* ring = smem + (RES ? (TQ * kp * 4 + 1023) / 1024 * 1024 : 0);
   float* lst_base = reinterpret_cast<float*>(ring + NST * SB);  // [EG][2][keep][TQ]
-  __shared__ __align__(8) uint64_t full[NST], empty[NST], accf[NACC], acce[NACC], abar;
+  __shared__ __align__(8) uint64_t full[NSTMAX], empty[NSTMAX], accf[NACC], acce[NACC], abar;
   __shared__ uint32_t tmem_sh;
   __shared__ int pm_sh[EG][TQ];  // slot of each list's current maximum
 
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(&abar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // NACC x 128 fp32 accumulator columns
+  if (warp == 1) {  // NACC x TCN fp32 accumulator columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_sh)),
                  "r"(NACC * TCN)
                  : "memory");
@@ -286,21 +289,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         bulk_g2s(aq, Aq, (uint32_t)(tile_floats * 4), &abar);
       }
       int it = 0;
+      // candidate tile j = 128-row images HALVES*j .. HALVES*j+HALVES-1; their
+      // chunk-c images land back to back, which is exactly the canonical
+      // layout of a TCN-row operand (row group 16 starts one image later)
       for (int j = 0; j < n_tiles; ++j) {
-        const float* Bt = P + (int64_t)j * tile_floats;
         for (int c = 0; c < nchunks; ++c, ++it) {
           const int s = it % NST;
           if (it >= NST) mbar_wait_sleep(&empty[s], ((it / NST) - 1) & 1);
           const uint32_t bytes = (uint32_t)TQ * min(KC, kp - c * KC) * 4;
           uint8_t* st = ring + s * SB;
-          if constexpr (RES) {
-            mbar_expect_tx(&full[s], bytes);
-            bulk_g2s(st, Bt + (int64_t)c * TQ * KC, bytes, &full[s]);
-          } else {
-            mbar_expect_tx(&full[s], 2 * bytes);
-            bulk_g2s(st, Aq + (int64_t)c * TQ * KC, bytes, &full[s]);
-            bulk_g2s(st + CHUNK_BYTES, Bt + (int64_t)c * TQ * KC, bytes, &full[s]);
-          }
+          uint8_t* sbp = st + (RES ? 0 : CHUNK_BYTES);
+          mbar_expect_tx(&full[s], (RES ? 0u : bytes) + HALVES * bytes);
+          if constexpr (!RES) bulk_g2s(st, Aq + (int64_t)c * TQ * KC, bytes, &full[s]);
+          for (int h = 0; h < HALVES; ++h)
+            bulk_g2s(sbp + h * bytes, P + (int64_t)(HALVES * j + h) * tile_floats + (int64_t)c * TQ * KC, bytes,
+                     &full[s]);
         }
       }
     }
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&accf[b], (j / NACC) & 1);
       tc_fence_after();
       const float4* nc4 = reinterpret_cast<const float4*>(nrm + (int64_t)j * TCN + g * CG);
-      const bool diag = j == qt;  // the only tile holding the query itself
+      const bool diag = j == qt / HALVES;  // the only tile holding the query itself
 #pragma unroll 1
       for (int h = 0; h < CG / 32; ++h) {
         uint32_t v[32];
@@ -682,7 +685,9 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
 
   const int kp = (n + 7) / 8 * 8;
-  const int64_t n_tiles = (m + TQ - 1) / TQ, m_pad = n_tiles * TQ;
+  // query tiles of TQ rows; candidate tiles of TCN rows (padding rows have
+  // norm +inf and are never candidates)
+  const int64_t n_tiles = (m + TQ - 1) / TQ, m_pad = (m + TCN - 1) / TCN * TCN, n_ctiles = m_pad / TCN;
   // candidates kept per query by the tensor-core pass; beyond KMAX-8 (or for
   // tiny inputs) every query goes to the exact scan
   const bool tc = k + 4 <= std::min(KMAX, UMAX / EG) && m > 2 * (int64_t)UMAX;
@@ -744,8 +749,16 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
       cudaFuncAttributes fa{};
       KTRY(cudaFuncGetAttributes(&fa, k_knn_tc<true>));
       smem_max -= (int)fa.sharedSizeBytes;  // static shared memory of the kernel
-      const bool res = tc_smem_bytes(true, kp, keep) <= smem_max;
-      const int shb = tc_smem_bytes(res, kp, keep);
+      // query tile resident if the deepest ring still fits; otherwise streamed
+      int nst = STAGES_RES;
+      bool res = true;
+      while (nst > 2 && tc_smem_bytes(true, kp, keep, nst) > smem_max) --nst;
+      if (tc_smem_bytes(true, kp, keep, nst) > smem_max) {
+        res = false;
+        nst = STAGES;
+        while (nst > 2 && tc_smem_bytes(false, kp, keep, nst) > smem_max) --nst;
+      }
+      const int shb = tc_smem_bytes(res, kp, keep, nst);
       if (shb > smem_max) {
         rc = fail(IVHD_ERR_INVALID_ARG, "kNN: shared memory plan %d > %d bytes", shb, smem_max);
         break;
@@ -755,8 +768,10 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
       KTRY(cudaStreamSynchronize(st));
       const auto a = clk::now();
       t_setup = std::chrono::duration<double>(a - t0).count();
-      if (res) k_knn_tc<true><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
-      else k_knn_tc<false><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_tiles, keep, cid, cd2);
+      if (res)
+        k_knn_tc<true><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_ctiles, keep, nst, cid, cd2);
+      else
+        k_knn_tc<false><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_ctiles, keep, nst, cid, cd2);
       KTRY(cudaGetLastError());
       KTRY(cudaStreamSynchronize(st));
       const auto b = clk::now();
