@@ -196,9 +196,12 @@ class _Session:
         if graph is None:
             if dataset is None:
                 raise InvalidArgumentError("need a graph or a dataset to embed")
-            raise InvalidArgumentError(
-                "kNN graph construction is outside this package's hot path; "
-                "build the graph first (e.g. ivhd.knng.build_exact_knn) and pass graph=")
+            # engine.py:170-176: the exact kNN graph of the dataset (GPU builder)
+            from .knng import build_exact_knn
+
+            k = config.nn * 4 if config.rnn_final_steps > 0 else config.nn
+            graph = build_exact_knn(dataset, min(k, self.data.shape[0] - 1), config.graph_metric,
+                                    device=device)
         self.graph = graph
         neighbors = np.asarray(graph.neighbors)
         m, k = neighbors.shape
@@ -215,6 +218,11 @@ class _Session:
                 self.helper = helper_graph
             elif k >= min(4 * config.nn, m - 1):
                 self.helper = graph
+            elif self.data is not None:  # engine.py:194-199
+                from .knng import build_exact_knn
+
+                self.helper = build_exact_knn(dataset, min(4 * config.nn, m - 1), config.graph_metric,
+                                              device=device)
             else:
                 raise InvalidArgumentError(
                     "reverse-neighbor phase needs a helper graph or the dataset")

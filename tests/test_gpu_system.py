@@ -229,3 +229,26 @@ def test_observer_positions_are_lazy_and_pinned_when_kept():
     run_embedding(graph=KnnGraph(nb), config=EmbeddingConfig(nn=2, rn=1, c=0.1, iterations=300, seed=3),
                   observer=framer)
     print(f"observer fast path: {(time.perf_counter() - t0) / 300 * 1e6:.0f} us/iteration")
+
+
+@pytest.mark.gpu
+def test_run_embedding_builds_graph_from_dataset():
+    """engine.py:170-176 / 194-199: without a graph, run_embedding builds the
+    exact kNN graph (and the 4*nn helper for the RNN phase) from the dataset —
+    here on the GPU — and the run equals one given that graph explicitly."""
+    from types import SimpleNamespace
+
+    from paper_2303_05455_b200 import EmbeddingConfig, run_embedding
+    from paper_2303_05455_b200.knng import build_exact_knn
+
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((3000, 20)) + 3.0 * rng.standard_normal((6, 20))[rng.integers(0, 6, 3000)]
+    ds = SimpleNamespace(data=x, labels=None)
+    cfg = EmbeddingConfig(nn=3, rn=1, c=0.1, iterations=40, seed=5)
+    a = run_embedding(dataset=ds, config=cfg)
+    b = run_embedding(graph=build_exact_knn(x, 3), config=cfg)
+    np.testing.assert_array_equal(a.embedding.points, b.embedding.points)
+    cfg2 = EmbeddingConfig(nn=3, rn=1, c=0.1, iterations=40, seed=5, rnn_final_steps=10)
+    c = run_embedding(dataset=ds, config=cfg2)
+    d = run_embedding(graph=build_exact_knn(x, 3), helper_graph=build_exact_knn(x, 12), dataset=ds, config=cfg2)
+    np.testing.assert_array_equal(c.embedding.points, d.embedding.points)
