@@ -177,7 +177,8 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
  * `device` (knng.build_exact_knn, knng.py:158-194): row i lists its k nearest
  * other rows by (distance, index); metric 0 = euclidean (distance), 1 =
  * cosine (1 - cos, rows normalised first; a zero row is IVHD_ERR_INVALID_ARG
- * with "zero-norm vector" in the message).  1 <= k < m, k <= 64.
+ * with "zero-norm vector" in the message), 2 = precomputed (x is an (m, m)
+ * distance matrix, n == m; k <= 128).  1 <= k < m, k <= 64 otherwise.
  * nbr_out (m, k) int32 and dist_out (m, k) float64 are host buffers.
  * stats_out (optional, 8 doubles): tensor-core pass seconds, re-rank seconds,
  * rows re-scanned exactly (uncertified), total seconds, setup seconds (H2D +

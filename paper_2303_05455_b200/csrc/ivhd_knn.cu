@@ -628,6 +628,93 @@ __global__ void k_exact_merge(const int* __restrict__ list, int n_list, int n_se
   }
 }
 
+// metric "precomputed" (knng.py:175-181, _row_topk knng.py:122-155): the k
+// smallest entries of every row of a dense (m, m) distance matrix, self
+// excluded, by (value, index).  One warp per row streams it coalesced; the
+// row's current k best live in registers across the lanes (slot s = lane +
+// 32 j, sorted), candidates that beat the k-th enter one at a time (warp
+// ballot), so each row costs one pass over its m values.
+constexpr int PK_MAX = 128;
+__global__ void __launch_bounds__(256) k_topk_rows(const double* __restrict__ D, int64_t m, int k,
+                                                  int32_t* __restrict__ out_id, double* __restrict__ out_d) {
+  constexpr int SPL = PK_MAX / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < m; r += nw) {
+    double ld[SPL];
+    int li[SPL];
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      ld[j] = INFINITY;
+      li[j] = 0x7fffffff;
+    }
+    double thr = INFINITY;
+    int thr_i = 0x7fffffff;
+    int cnt = 0;
+    const double* row = D + r * m;
+    for (int64_t c0 = 0; c0 < m; c0 += 32) {
+      const int64_t c = c0 + lane;
+      double d = INFINITY;
+      int id = 0x7fffffff;
+      if (c < m && c != r) {
+        d = row[c];
+        id = (int)c;
+      }
+      unsigned pass = __ballot_sync(0xffffffffu, id != 0x7fffffff && (cnt < k || before(d, id, thr, thr_i)));
+      while (pass) {
+        const int src = __ffs(pass) - 1;
+        pass &= pass - 1;
+        const double nd = __shfl_sync(0xffffffffu, d, src);
+        const int ni = __shfl_sync(0xffffffffu, id, src);
+        if (!(cnt < k || before(nd, ni, thr, thr_i))) continue;
+        int bef = 0;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) bef += before(ld[j], li[j], nd, ni) ? 1 : 0;
+        const int pos = __reduce_add_sync(0xffffffffu, bef);
+#pragma unroll
+        for (int j = SPL - 1; j >= 0; --j) {
+          double pd = __shfl_up_sync(0xffffffffu, ld[j], 1);
+          int pi = __shfl_up_sync(0xffffffffu, li[j], 1);
+          const double cd = j > 0 ? __shfl_sync(0xffffffffu, ld[j > 0 ? j - 1 : 0], 31) : INFINITY;
+          const int ci = j > 0 ? __shfl_sync(0xffffffffu, li[j > 0 ? j - 1 : 0], 31) : 0x7fffffff;
+          if (lane == 0) {
+            pd = cd;
+            pi = ci;
+          }
+          const int sl = lane + 32 * j;
+          if (sl > pos) {
+            ld[j] = pd;
+            li[j] = pi;
+          } else if (sl == pos) {
+            ld[j] = nd;
+            li[j] = ni;
+          }
+        }
+        cnt = min(cnt + 1, k);
+        const int ts = k - 1;
+        double tv = ld[0];
+        int ti = li[0];
+#pragma unroll
+        for (int j = 1; j < SPL; ++j)
+          if ((ts >> 5) == j) {
+            tv = ld[j];
+            ti = li[j];
+          }
+        thr = __shfl_sync(0xffffffffu, tv, ts & 31);
+        thr_i = __shfl_sync(0xffffffffu, ti, ts & 31);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int sl = lane + 32 * j;
+      if (sl < k) {
+        out_id[r * k + sl] = li[j];
+        out_d[r * k + sl] = ld[j];
+      }
+    }
+  }
+}
+
 __global__ void k_flag_list(const int* __restrict__ flag, int64_t m, int* __restrict__ list, int* __restrict__ cnt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < m && flag[i]) list[atomicAdd(cnt, 1)] = (int)i;
@@ -667,7 +754,40 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   if (!x || !nbr_out || !dist_out) return fail(IVHD_ERR_INVALID_ARG, "null pointer");
   if (!(1 <= k && k < m)) return fail(IVHD_ERR_INVALID_ARG, "k must satisfy 1 <= k < M, got k=%d, M=%lld", k, (long long)m);
   if (n < 1) return fail(IVHD_ERR_INVALID_ARG, "need at least one feature column");
-  if (metric != 0 && metric != 1) return fail(IVHD_ERR_INVALID_ARG, "metric must be euclidean (0) or cosine (1)");
+  if (metric < 0 || metric > 2)
+    return fail(IVHD_ERR_INVALID_ARG, "metric must be euclidean (0), cosine (1) or precomputed (2)");
+  if (metric == 2) {  // x is an (m, m) distance matrix (n must equal m)
+    if (n != m) return fail(IVHD_ERR_INVALID_ARG, "precomputed metric needs a square matrix");
+    if (k > PK_MAX) return fail(IVHD_ERR_INVALID_ARG, "k=%d above the supported %d", k, PK_MAX);
+    if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail(IVHD_ERR_CUDA, "stream");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    double *dD = nullptr, *dd = nullptr;
+    int32_t* di = nullptr;
+    cudaError_t e = cudaSuccess;
+    do {
+      if ((e = cudaMallocAsync(&dD, sizeof(double) * m * m, st)) != cudaSuccess) break;
+      if ((e = cudaMallocAsync(&dd, sizeof(double) * m * k, st)) != cudaSuccess) break;
+      if ((e = cudaMallocAsync(&di, sizeof(int32_t) * m * k, st)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(dD, x, sizeof(double) * m * m, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+      k_topk_rows<<<(unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)sms * 16), 256, 0, st>>>(dD, m, k, di, dd);
+      if ((e = cudaGetLastError()) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(nbr_out, di, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(dist_out, dd, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+      e = cudaStreamSynchronize(st);
+    } while (0);
+    if (dD) cudaFreeAsync(dD, st);
+    if (dd) cudaFreeAsync(dd, st);
+    if (di) cudaFreeAsync(di, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "kNN (precomputed): %s", cudaGetErrorString(e));
+    if (stats_out)
+      for (int i = 0; i < 8; ++i) stats_out[i] = 0.0;
+    return IVHD_OK;
+  }
   if (m >= 0x7fffffffLL) return fail(IVHD_ERR_INVALID_ARG, "M too large for 31-bit ids");
   if (k > EX_K) return fail(IVHD_ERR_INVALID_ARG, "k=%d above the supported %d", k, EX_K);
   if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);

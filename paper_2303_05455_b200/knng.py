@@ -8,9 +8,9 @@ candidate pass, an exact fp64 re-rank with an error-bounded certificate, and
 an exact fp64 scan for any row the certificate does not cover.  There is no
 CPU path.
 
-Metrics: "euclidean" and "cosine" (knng.py:105-115, 185-189).  "precomputed"
-(a square distance matrix) is not a GPU path here and raises
-InvalidArgumentError.
+Metrics: "euclidean" and "cosine" (knng.py:105-115, 185-189) through the
+tensor-core pass; "precomputed" (a square distance matrix, knng.py:175-181)
+through a warp-per-row streaming top-k (k <= 128).
 """
 
 import os
@@ -22,7 +22,7 @@ from . import _lib
 from .embed import KnnGraph
 from .errors import DegenerateMetricError, DeviceError, DimensionMismatchError, InvalidArgumentError
 
-_METRICS = {"euclidean": 0, "cosine": 1}
+_METRICS = {"euclidean": 0, "cosine": 1, "precomputed": 2}
 
 last_stats = {}
 
@@ -38,8 +38,8 @@ def build_exact_knn(dataset_or_matrix, k, metric="euclidean", chunk_budget=None,
     k = int(k)
     if not (1 <= k < m):
         raise InvalidArgumentError(f"k must satisfy 1 <= k < M, got k={k}, M={m}")
-    if metric == "precomputed":
-        raise InvalidArgumentError("precomputed metric is not supported by the GPU kNN builder")
+    if metric == "precomputed" and (data.ndim != 2 or data.shape[0] != data.shape[1]):
+        raise DimensionMismatchError("precomputed metric needs a square matrix")
     if metric not in _METRICS:
         raise InvalidArgumentError(f"unknown metric {metric!r}")
     x = _lib.f64(data)

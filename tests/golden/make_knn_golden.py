@@ -46,6 +46,11 @@ def knn_inputs():
     # k beyond the tensor-core pass (k + 4 > 32): every row takes the exact scan
     rng = np.random.default_rng(17)
     out["exact_k40"] = (rng.standard_normal((1200, 24)), 40, "euclidean")
+    # precomputed square distance matrix (knng.py:175-181) with exact ties
+    rng = np.random.default_rng(18)
+    pts = rng.integers(0, 6, (700, 3)).astype(np.float64)
+    dmat = np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1))
+    out["precomputed_ties"] = (dmat, 9, "precomputed")
     # odd width (not a multiple of 8), k = 1
     rng = np.random.default_rng(16)
     out["odd13_k1"] = (rng.uniform(-1, 1, (1000, 13)), 1, "euclidean")
