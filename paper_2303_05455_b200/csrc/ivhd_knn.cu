@@ -146,26 +146,44 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 
 // ------------------------------------------------------------------ pack
-// One warp per row: tf32-rounded values into the tile images, fp32 norm of
-// the rounded row.  Padding rows get norm +inf (never a candidate).
+// One warp per row: tf32-rounded values into the tile images of the query
+// operand PA and the candidate operand PB, fp32 norm s of the rounded row.
+// Two augmented columns fold the candidate norm into the MMA:
+//     PA[.., n:n+2] = (1, 1),   PB[.., n:n+2] = -(h_hi, h_lo),  h = s / 2
+// so each accumulator holds q.c - |c|^2 / 2 = -(d^2 - |q|^2) / 2 and the
+// epilogue filter is one compare per candidate.  Padding candidate rows get
+// h = +inf (never a candidate) and norm +inf.
 __global__ void k_pack(const double* __restrict__ X, int64_t m, int n, int kp, int64_t m_pad,
-                       float* __restrict__ P, float* __restrict__ nrm) {
+                       float* __restrict__ PA, float* __restrict__ PB, float* __restrict__ nrm) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < m_pad; r += nw) {
     const int64_t t = r / TQ;
     const int rr = (int)(r % TQ);
+    auto off = [&](int k) {
+      const int c = k / KC, kk = k % KC, kc = min(KC, kp - c * KC);
+      return (t * (int64_t)TQ * kp * 4 + (int64_t)c * CHUNK_BYTES + img_off(rr, kk, kc)) >> 2;
+    };
     float s = 0.f;
     for (int k = lane; k < kp; k += 32) {
       const float v = (r < m && k < n) ? tf32_round((float)X[r * n + k]) : 0.f;
       s = fmaf(v, v, s);
-      const int c = k / KC, kk = k % KC, kc = min(KC, kp - c * KC);
-      const int64_t off = t * (int64_t)TQ * kp * 4 + (int64_t)c * CHUNK_BYTES + img_off(rr, kk, kc);
-      P[off >> 2] = v;
+      if (k < n || k >= n + 2) {
+        PA[off(k)] = v;
+        PB[off(k)] = v;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) nrm[r] = r < m ? s : INFINITY;
+    if (lane == 0) {
+      nrm[r] = r < m ? s : INFINITY;
+      const float h = r < m ? 0.5f * s : INFINITY;
+      const float hi = tf32_round(h), lo = r < m ? tf32_round(h - hi) : 0.f;
+      PA[off(n)] = 1.f;
+      PA[off(n + 1)] = 1.f;
+      PB[off(n)] = -hi;
+      PB[off(n + 1)] = -lo;
+    }
   }
 }
 
@@ -238,7 +256,8 @@ __device__ __noinline__ float knn_insert(float* ld, int* li, int* pm_s, int r, i
 
 template <bool RES>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_knn_tc(const float* __restrict__ P, const float* __restrict__ nrm, int64_t m, int kp, int n_tiles, int keep,
+    k_knn_tc(const float* __restrict__ PA, const float* __restrict__ P, const float* __restrict__ nrm, int64_t m,
+             int kp, int n_tiles, int keep,
              int nst, int32_t* __restrict__ cand_id, float* __restrict__ cand_d2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -283,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
-      const float* Aq = P + (int64_t)qt * tile_floats;
+      const float* Aq = PA + (int64_t)qt * tile_floats;
       if constexpr (RES) {  // the whole query tile: one contiguous copy
         mbar_expect_tx(&abar, (uint32_t)(tile_floats * 4));
         bulk_g2s(aq, Aq, (uint32_t)(tile_floats * 4), &abar);
@@ -365,7 +384,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = j % NACC;
       mbar_wait(&accf[b], (j / NACC) & 1);
       tc_fence_after();
-      const float4* nc4 = reinterpret_cast<const float4*>(nrm + (int64_t)j * TCN + g * CG);
       const bool diag = j == qt / HALVES;  // the only tile holding the query itself
 #pragma unroll 1
       for (int h = 0; h < CG / 32; ++h) {
@@ -381,32 +399,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) ld[r] = 0.f;
         continue;
 #endif
-        float4 ncs[8];
-#pragma unroll
-        for (int i4 = 0; i4 < 8; ++i4) ncs[i4] = __ldg(nc4 + h * 8 + i4);
-        // fast pass, branch-free: bit i = candidate i beats the threshold
+        // fast pass, one compare per candidate: acc = q.c - |c|^2/2 and
+        // d^2 - nq = -2 acc < thq  <=>  acc > -thq/2
+        const float thh = -0.5f * thq;
         unsigned msk = 0;
 #pragma unroll
-        for (int i4 = 0; i4 < 8; ++i4) {
-          const float ncv[4] = {ncs[i4].x, ncs[i4].y, ncs[i4].z, ncs[i4].w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float t = fmaf(-2.f, __uint_as_float(v[i4 * 4 + u]), ncv[u]);  // d2 - nq
-            msk |= t < thq ? (1u << (i4 * 4 + u)) : 0u;
-          }
-        }
+        for (int i = 0; i < 32; ++i) msk |= __uint_as_float(v[i]) > thh ? (1u << i) : 0u;
         if (msk) {  // rare: re-test in order against the moving threshold, insert
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
-            const float ncv[4] = {ncs[i4].x, ncs[i4].y, ncs[i4].z, ncs[i4].w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int i = i4 * 4 + u;
-              if ((msk >> i) & 1u) {
-                const float t = fmaf(-2.f, __uint_as_float(v[i]), ncv[u]);
-                if (t < thq && !(diag && c0 + i == (int)qid))
-                  thq = knn_insert(ld, li, pm_s, r, keep, t + nq, c0 + i, nq);
-              }
+          for (int i = 0; i < 32; ++i) {
+            if ((msk >> i) & 1u) {
+              const float t = -2.f * __uint_as_float(v[i]);  // d2 - nq
+              if (t < thq && !(diag && c0 + i == (int)qid))
+                thq = knn_insert(ld, li, pm_s, r, keep, t + nq, c0 + i, nq);
             }
           }
         }
@@ -804,7 +809,7 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
 
-  const int kp = (n + 7) / 8 * 8;
+  const int kp = (n + 2 + 7) / 8 * 8;  // features + 2 augmented norm columns, K steps of 8
   // query tiles of TQ rows; candidate tiles of TCN rows (padding rows have
   // norm +inf and are never candidates)
   const int64_t n_tiles = (m + TQ - 1) / TQ, m_pad = (m + TCN - 1) / TCN * TCN, n_ctiles = m_pad / TCN;
@@ -817,7 +822,7 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   const int keep = tc ? std::min(std::min(KMAX, UMAX / EG), k + 4) : 0;
 
   double *dX = nullptr, *dD = nullptr;
-  float *dP = nullptr, *dN = nullptr, *cd2 = nullptr;
+  float *dP = nullptr, *dPA = nullptr, *dN = nullptr, *cd2 = nullptr;
   int32_t *dI = nullptr, *cid = nullptr;
   int *flag = nullptr, *list = nullptr, *cnt = nullptr;
   long long* bad = nullptr;
@@ -855,12 +860,13 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
     }
     if (tc) {
       KTRY(cudaMallocAsync(&dP, sizeof(float) * m_pad * kp, st));
+      KTRY(cudaMallocAsync(&dPA, sizeof(float) * m_pad * kp, st));
       KTRY(cudaMallocAsync(&dN, sizeof(float) * m_pad, st));
       KTRY(cudaMallocAsync(&cid, sizeof(int32_t) * m * UMAX, st));
       KTRY(cudaMallocAsync(&cd2, sizeof(float) * m, st));
       KTRY(cudaMallocAsync(&rmax_bits, sizeof(unsigned int), st));
       KTRY(cudaMemsetAsync(rmax_bits, 0, sizeof(unsigned int), st));
-      k_pack<<<sms * 16, 256, 0, st>>>(dX, m, n, kp, m_pad, dP, dN);
+      k_pack<<<sms * 16, 256, 0, st>>>(dX, m, n, kp, m_pad, dPA, dP, dN);
       k_max_norm<<<sms, 256, 0, st>>>(dN, m, rmax_bits);
       unsigned int hr = 0;
       KTRY(cudaMemcpyAsync(&hr, rmax_bits, sizeof hr, cudaMemcpyDeviceToHost, st));
@@ -889,9 +895,11 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
       const auto a = clk::now();
       t_setup = std::chrono::duration<double>(a - t0).count();
       if (res)
-        k_knn_tc<true><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_ctiles, keep, nst, cid, cd2);
+        k_knn_tc<true><<<(unsigned)n_tiles, THREADS, shb, st>>>(dPA, dP, dN, m, kp, (int)n_ctiles, keep, nst, cid,
+                                                                cd2);
       else
-        k_knn_tc<false><<<(unsigned)n_tiles, THREADS, shb, st>>>(dP, dN, m, kp, (int)n_ctiles, keep, nst, cid, cd2);
+        k_knn_tc<false><<<(unsigned)n_tiles, THREADS, shb, st>>>(dPA, dP, dN, m, kp, (int)n_ctiles, keep, nst, cid,
+                                                                 cd2);
       KTRY(cudaGetLastError());
       KTRY(cudaStreamSynchronize(st));
       const auto b = clk::now();
@@ -941,6 +949,7 @@ int ivhd_knn_build(int device, const double* x, int64_t m, int32_t n, int32_t k,
   cudaFreeAsync(dX, st); cudaFreeAsync(dI, st); cudaFreeAsync(dD, st); cudaFreeAsync(flag, st);
   cudaFreeAsync(list, st); cudaFreeAsync(cnt, st); cudaFreeAsync(bad, st);
   if (dP) cudaFreeAsync(dP, st);
+  if (dPA) cudaFreeAsync(dPA, st);
   if (dN) cudaFreeAsync(dN, st);
   if (cid) cudaFreeAsync(cid, st);
   if (cd2) cudaFreeAsync(cd2, st);
