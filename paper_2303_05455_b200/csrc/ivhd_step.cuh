@@ -19,13 +19,16 @@
 //              sum|dold|^2, #non-finite}: fixed tile size => the reduction
 //              order is independent of grid size and of the rank count.
 //
-// Work mapping: a block of 256 threads takes fixed-size vertex tiles from a
-// dynamic tile counter; inside a tile G lanes cooperate on one vertex (its
-// symmetrised CSR row), reduce with a fixed xor-butterfly (all lanes get the
-// bit-identical sum), and lane 0 of the group applies the optimizer.  No
-// atomics touch the data; the last block to finish reduces the tile partials
-// in fixed order and writes the decision (cur buffer, b, trace, status) that
-// the next launch reads.
+// Work mapping: persistent blocks of 8 consumer warps + 1 TMA producer warp
+// run a static list of work units (one pass of a 256-vertex tile with G lanes
+// per vertex; cost-balanced per block in the fused loop, round robin in the
+// sharded one).  The producer stages each unit's row pointers, columns,
+// positions and optimizer state with cp.async.bulk into a 3-stage ring; the G
+// lanes of a row gather neighbour positions, reduce with a fixed xor
+// butterfly (all lanes get the bit-identical sum) and lane 0 of the group
+// applies the optimizer.  No atomics touch the data; the last block to finish
+// reduces the partials in fixed order and writes the decision (cur buffer, b,
+// trace, status) that the next launch reads.
 #pragma once
 #include <cstdint>
 #include <type_traits>
