@@ -31,7 +31,7 @@ struct CsrSlot {
   uint32_t* col = nullptr;      // [n]
   float2* ew = nullptr;         // [n] or nullptr (binary)
   uint8_t* tile_g = nullptr;    // [n_tiles_cap] lanes per vertex of each tile
-  uint8_t* tile_dm = nullptr;   // [n_tiles_cap] max row length of each tile (clamped to 255)
+  uint32_t* tile_dm = nullptr;  // [n_tiles_cap] max row length of each tile
   int* units = nullptr;         // work units (tile << 12 | pass << 7 | min(slots per lane,15) << 3 | log2 G)
   int n_units = 0;
   std::vector<int> unit_base;   // host: first unit of each tile (n_tiles_cap + 1)
@@ -439,7 +439,7 @@ __global__ void k_fill_perm_cols(const uint32_t* __restrict__ rp_old, const uint
 // Lanes per vertex of each tile: smallest power of two G with
 // G * kUnroll >= the tile's max degree (capped at a warp); pad tiles get 1.
 __global__ void k_tile_g(const uint32_t* __restrict__ rp, int64_t m, int n_tiles_cap,
-                         uint8_t* __restrict__ tile_g, uint8_t* __restrict__ tile_dm) {
+                         uint8_t* __restrict__ tile_g, uint32_t* __restrict__ tile_dm) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_tiles_cap; t += nwarps) {
@@ -451,7 +451,7 @@ __global__ void k_tile_g(const uint32_t* __restrict__ rp, int64_t m, int n_tiles
     while (G < 32 && (uint32_t)(G * kUnroll) < mx) G <<= 1;
     if (lane == 0) {
       tile_g[t] = (uint8_t)G;
-      tile_dm[t] = (uint8_t)min(mx, 255u);
+      tile_dm[t] = mx;  // unclamped: the slots-per-lane bound must cover hub rows
     }
   }
 }
@@ -480,7 +480,7 @@ int ensure_slot(ivhd_ctx* ctx, CsrSlot& s, int64_t n, bool weighted) {
   // +16 entries: TMA copies round sizes up to 16 bytes
   if (s.row_ptr == nullptr) CU(ctx, dalloc(ctx, &s.row_ptr, sizeof(uint32_t) * (ctx->m + 1 + 16)));
   if (s.tile_g == nullptr) CU(ctx, dalloc(ctx, &s.tile_g, (size_t)ctx->n_tiles_cap));
-  if (s.tile_dm == nullptr) CU(ctx, dalloc(ctx, &s.tile_dm, (size_t)ctx->n_tiles_cap));
+  if (s.tile_dm == nullptr) CU(ctx, dalloc(ctx, &s.tile_dm, sizeof(uint32_t) * ctx->n_tiles_cap));
   if (n > s.cap) {
     if (s.col) dfree(ctx, s.col);
     if (s.ew) dfree(ctx, s.ew);
@@ -654,9 +654,11 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
                                                                                      ctx->n_tiles_cap, S.tile_g, S.tile_dm);
     if ((e = cudaGetLastError()) != cudaSuccess) break;
     // work units: one per (tile, pass), in tile order
-    std::vector<uint8_t> g(ctx->n_tiles_cap), dm(ctx->n_tiles_cap);
+    std::vector<uint8_t> g(ctx->n_tiles_cap);
+    std::vector<uint32_t> dm(ctx->n_tiles_cap);
     if ((e = cudaMemcpyAsync(g.data(), S.tile_g, g.size(), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
-    if ((e = cudaMemcpyAsync(dm.data(), S.tile_dm, dm.size(), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(dm.data(), S.tile_dm, sizeof(uint32_t) * dm.size(), cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess) break;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
     S.unit_base.assign(ctx->n_tiles_cap + 1, 0);
     std::vector<int> units;
@@ -670,7 +672,7 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
     S.unit_cost.resize(units.size());
     for (size_t u = 0; u < units.size(); ++u) {
       const int t = units[u] >> 12, G = 1 << (units[u] & 7);
-      S.unit_cost[u] = (dm[t] + G - 1) / G;  // slots per lane (clamped degree for hubs)
+      S.unit_cost[u] = (dm[t] + G - 1) / G;  // slots per lane
     }
     S.sched_grid = 0;
     S.n_units = (int)units.size();
@@ -1400,8 +1402,8 @@ int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p) {
   ctx->opt_set = true;
   Hyper h{};
   h.a = (float)p->a;
-  h.g1 = (float)p->gamma1;
-  h.g2 = (float)p->gamma2;
+  h.g1 = p->gamma1;
+  h.g2 = p->gamma2;
   h.tau = p->tau;
   h.adapt = p->auto_adapt;
   h.beta = (float)p->beta;

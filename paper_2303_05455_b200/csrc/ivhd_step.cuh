@@ -96,8 +96,9 @@ struct Ctrl {
 };
 
 struct Hyper {
-  float a, g1, g2;       // force-directed
+  float a;               // force-directed friction (per-vertex fp32 update)
   float beta, gv, gs, rho, eps;
+  double g1, g2;         // step-size factors: b is kept in fp64 like the reference
   double tau;
   int adapt;
 };
@@ -337,10 +338,10 @@ __device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
   if (OPT == OPT_FD && A.h.adapt) {
     const double dT = s.y - s.z;
     if (dT > A.h.tau) {
-      step *= (double)A.h.g2;
+      step *= A.h.g2;
       commit = false;
     } else if (dT < -A.h.tau) {
-      step *= (double)A.h.g1;
+      step *= A.h.g1;
       commit = false;
     }
   }
