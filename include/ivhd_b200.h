@@ -28,6 +28,8 @@
  *   ivhd_knn_build                  knng.build_exact_knn             knng.py:158-194
  *                                   (euclidean / cosine)
  *   ivhd_neighbor_hit               metrics.neighbor_hit (points)    metrics.py:254-294
+ *   ivhd_curve_pass                 metrics._curve_pass (rnx/gnn/    metrics.py:149-182
+ *                                   trust/continuity/evaluate)
  *
  */
 #ifndef IVHD_B200_H
@@ -196,6 +198,21 @@ const char* ivhd_knn_last_error(void);
  * optional (m, nn_max) int32 neighbour ids.  Errors: ivhd_metrics_last_error(). */
 int ivhd_neighbor_hit(int device, const double* y, int64_t m, int32_t dim, const int32_t* labels,
                       int32_t nn_max, double* cf_nn_out, int32_t* nbr_out);
+/* One rank-curve pass (metrics._curve_pass, metrics.py:149-182) on `device`:
+ * x (m, n) float64 source points, or with x_precomputed an (m, m) distance
+ * matrix; y (m, dim) float64 embedding (1 <= dim <= 3); labels (m) int32 or
+ * NULL.  Ranks use squared distances (|a|^2 + |b|^2) - 2 a.b clamped at 0 and
+ * the (distance, index) tie rule.  Outputs (integer counts, host buffers):
+ * agree_out[p], p = 0..k_max: #pairs with max(rho, r) == p; same_ld_out /
+ * same_hd_out[p], p < k_max: #rows whose (p+1)-th LD / HD neighbour shares the
+ * label (only with labels); trust_out / cont_out[a]: summed entrant / leaver
+ * rank penalties at report_ks[a] (n_report <= 8, 1 <= k < m/2).
+ * 1 <= k_max <= m-2 and max(k_max, report ks) <= 1024.
+ * Errors: ivhd_metrics_last_error(). */
+int ivhd_curve_pass(int device, const double* x, int64_t m, int32_t n, int32_t x_precomputed, const double* y,
+                    int32_t dim, const int32_t* labels, int32_t k_max, const int32_t* report_ks, int32_t n_report,
+                    int64_t* agree_out, int64_t* same_ld_out, int64_t* same_hd_out, int64_t* trust_out,
+                    int64_t* cont_out);
 const char* ivhd_metrics_last_error(void);
 
 #ifdef __cplusplus

@@ -22,6 +22,7 @@ from .ivhd_oracle import (  # noqa: F401
     build_connections,
     components,
     csr_forces,
+    curve_pass,
     forces,
     init_layout,
     make_state,

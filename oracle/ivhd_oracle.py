@@ -444,3 +444,50 @@ class OracleRun:
         for _ in range(n):
             self.step()
         return self.Y
+
+
+# ------------------------------------------------------------- rank curves
+# Restatement of metrics.py:57-110 (distance blocks, rank rule) and
+# metrics.py:149-182 (`_curve_pass`), for small M (the full M x M rank
+# matrices are materialised).  Checker for ivhd_curve_pass.
+
+
+def _sq_dist_matrix(Z):
+    """metrics.py:76-84: max((|a|^2 + |b|^2) - 2 a.b, 0)."""
+    sq = np.einsum("ij,ij->i", Z, Z)
+    D = sq[:, None] + sq[None, :] - 2.0 * (Z @ Z.T)
+    np.maximum(D, 0.0, out=D)
+    return D
+
+
+def _ranks(D):
+    """metrics.py:103-113: rank 1..M-1 by (distance, index), self = 0."""
+    m = D.shape[0]
+    D = np.array(D, dtype=np.float64)
+    D[np.arange(m), np.arange(m)] = np.inf
+    idx = np.broadcast_to(np.arange(m), (m, m))
+    order = np.lexsort((idx, D), axis=1)
+    ranks = np.empty((m, m), dtype=np.int64)
+    np.put_along_axis(ranks, order, np.broadcast_to(np.arange(1, m + 1), (m, m)), axis=1)
+    ranks[np.arange(m), np.arange(m)] = 0
+    return ranks, order
+
+
+def curve_pass(X, Y, labels, k_max, report_ks, x_precomputed=False):
+    """metrics.py:149-182 -> (agree[0..k_max], same_ld, same_hd, trust_pen, cont_pen)."""
+    m = X.shape[0]
+    hd, hd_order = _ranks(X if x_precomputed else _sq_dist_matrix(X))
+    ld, ld_order = _ranks(_sq_dist_matrix(Y))
+    peak = np.maximum(hd, ld)
+    peak[np.arange(m), np.arange(m)] = m
+    agree = np.bincount(peak.ravel(), minlength=m + 1)[: k_max + 1].astype(np.int64)
+    same_ld = same_hd = None
+    if labels is not None:
+        own = labels[:, None]
+        same_ld = (labels[ld_order[:, :k_max]] == own).sum(axis=0)
+        same_hd = (labels[hd_order[:, :k_max]] == own).sum(axis=0)
+    trust, cont = {}, {}
+    for k in report_ks:
+        trust[k] = int((hd[(ld <= k) & (hd > k)] - k).sum())
+        cont[k] = int((ld[(hd <= k) & (hd > 0) & (ld > k)] - k).sum())
+    return agree, same_ld, same_hd, trust, cont

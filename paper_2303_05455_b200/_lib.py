@@ -85,6 +85,9 @@ SIGNATURES = {
     "ivhd_metrics_last_error": (ctypes.c_char_p, []),
     "ivhd_neighbor_hit": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, c_i32p,
                                          ctypes.c_int32, c_f64p, c_i32p]),
+    "ivhd_curve_pass": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                       c_f64p, ctypes.c_int32, c_i32p, ctypes.c_int32, c_i32p, ctypes.c_int32,
+                                       c_i64p, c_i64p, c_i64p, c_i64p, c_i64p]),
     "ivhd_knn_build": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_int32, c_i32p, c_f64p, c_f64p]),
 }

@@ -249,6 +249,327 @@ __global__ void __launch_bounds__(QWARPS * 32) k_grid_knn(const double* __restri
   for (int i = threadIdx.x; i < kk; i += blockDim.x) atomicAdd(&hits[i], (unsigned long long)sh_hits[i]);
 }
 
+
+// ---------------------------------------------------------------------------
+// Rank-curve pass (reference metrics.py:149-182 `_curve_pass`, used by
+// rnx_curve 185-202, gnn_curve 217-228, trust_continuity 240-251 and
+// evaluate_embedding 351-380).  For every point i the reference ranks all
+// other points by (squared distance, index) in the source space X (rho) and
+// in the embedding Y (r) and accumulates
+//     agree[max(rho, r)] += 1                         (Q_NX counts)
+//     same_hd[p] / same_ld[p] += label match of the p-th neighbour
+//     trust[k] += rho - k   for j with r <= k < rho   (entrants)
+//     cont[k]  += r - k     for j with rho <= k < r   (leavers)
+// Only ranks <= k_max reach the curves (cumsum(agree)[1..k_max]), so the
+// pass needs each row's K = max(k_max, report ks) nearest in both spaces,
+// plus the exact far rank of the few entrants / leavers outside that list.
+//
+// Distances follow the reference formula (metrics.py:76-84):
+//     d2(i, j) = max((|x_i|^2 + |x_j|^2) - 2 x_i.x_j, 0),  d2(i, i) = +inf.
+// X rows come in blocks of B rows: a fp64 SIMT tile kernel writes the (B, M)
+// distance block (the 126 MB L2 holds a block's working set for small M);
+// Y distances (dim <= 3) are recomputed on the fly.  Per row one CTA keeps
+// the best 1024 (d2, j) pairs sorted in shared memory and merges a pending
+// buffer of threshold-passing candidates by bitonic sort (~k ln(M/k)
+// insertions per row).  All counts are integers: deterministic.
+namespace curves {
+
+constexpr int KMAX = 1024;  // longest ranked list per row
+constexpr int NT = 512;     // threads per row CTA
+constexpr int NB = 2 * KMAX;
+constexpr int MAX_REPORT = 8;
+constexpr int DT = 64, DK = 16;  // distance tile
+
+struct Report {
+  int n;
+  int k[MAX_REPORT];
+  int kmax;  // max of k (0 when n == 0)
+};
+
+__global__ void k_sqnorm(const double* __restrict__ x, int64_t m, int n, double* __restrict__ sq) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (int c = 0; c < n; ++c) s = fma(x[i * n + c], x[i * n + c], s);
+  sq[i] = s;
+}
+
+// out[r][j] = max((sq[r0+r] + sq[j]) - 2 x_{r0+r}.x_j, 0) for r < nb, j < m
+__global__ void __launch_bounds__(256) k_dist_block(const double* __restrict__ x, const double* __restrict__ sq,
+                                                    int64_t m, int n, int64_t r0, int nb, double* __restrict__ out) {
+  __shared__ double As[DK][DT + 1], Bs[DK][DT + 1];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int64_t rb = (int64_t)blockIdx.y * DT, cb = (int64_t)blockIdx.x * DT;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < n; k0 += DK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = t + 256 * q, row = e >> 4, kk = e & 15;
+      const int64_t ra = rb + row, cbb = cb + row;
+      As[kk][row] = (ra < nb && k0 + kk < n) ? x[(r0 + ra) * n + k0 + kk] : 0.0;
+      Bs[kk][row] = (cbb < m && k0 + kk < n) ? x[cbb * n + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < DK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = As[kk][ty + 16 * u];
+        b[u] = Bs[kk][tx + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t r = rb + ty + 16 * u;
+    if (r >= nb) continue;
+    const double si = sq[r0 + r];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t c = cb + tx + 16 * v;
+      if (c < m) out[r * m + c] = fmax((si + sq[c]) - 2.0 * acc[u][v], 0.0);
+    }
+  }
+}
+
+struct HdRow {
+  const double* p;
+  __device__ __forceinline__ double operator()(int64_t j) const { return p[j]; }
+};
+
+struct LdRow {
+  const double* y;
+  const double* sq;
+  int dim;
+  double yi[3];
+  double si;
+  __device__ __forceinline__ double operator()(int64_t j) const {
+    double dot = 0.0;
+    for (int d = 0; d < dim; ++d) dot = fma(yi[d], y[j * dim + d], dot);
+    return fmax((si + sq[j]) - 2.0 * dot, 0.0);
+  }
+};
+
+// Bitonic sort of consecutive segments of length S (power of two) within the
+// first N entries, ascending by (d, j).
+__device__ void bitonic(double* d, int* jj, int N, int S) {
+  for (int k = 2; k <= S; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < N / 2; t += NT) {
+        const int i = 2 * t - (t & (j - 1));
+        const int p = i + j;
+        const bool asc = (k == S) || !(i & k);
+        const bool gt = lt(d[p], jj[p], d[i], jj[i]);
+        if (gt == asc) {
+          const double td = d[i];
+          d[i] = d[p];
+          d[p] = td;
+          const int tj = jj[i];
+          jj[i] = jj[p];
+          jj[p] = tj;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// Merge the pending half into the sorted best half.
+__device__ void merge_pending(double* sd, int* sj, int* s_cnt) {
+  const int cnt = *s_cnt;
+  for (int t = KMAX + cnt + threadIdx.x; t < NB; t += NT) {
+    sd[t] = INFINITY;
+    sj[t] = 0x7fffffff;
+  }
+  __syncthreads();
+  bitonic(sd, sj, NB, NB);
+  if (threadIdx.x == 0) *s_cnt = 0;
+  __syncthreads();
+}
+
+// sd[0..K) / sj[0..K) <- the K smallest (d2, j), j != self, in order.
+template <class Dist>
+__device__ void select_row(const Dist& dist, int64_t m, int self, int K, double* sd, int* sj, int* s_cnt) {
+  for (int t = threadIdx.x; t < NB; t += NT) {
+    sd[t] = INFINITY;
+    sj[t] = 0x7fffffff;
+  }
+  if (threadIdx.x == 0) *s_cnt = 0;
+  __syncthreads();
+  double thr_d = INFINITY;
+  int thr_j = 0x7fffffff;
+  for (int64_t c = 0; c < m; c += NT) {
+    if (*s_cnt > KMAX - NT) {
+      merge_pending(sd, sj, s_cnt);
+      thr_d = sd[K - 1];
+      thr_j = sj[K - 1];
+    }
+    const int64_t j = c + threadIdx.x;
+    if (j < m && j != self) {
+      const double d = dist(j);
+      if (lt(d, (int)j, thr_d, thr_j)) {
+        const int p = atomicAdd(s_cnt, 1);
+        sd[KMAX + p] = d;
+        sj[KMAX + p] = (int)j;
+      }
+    }
+    __syncthreads();
+  }
+  merge_pending(sd, sj, s_cnt);
+}
+
+// 1-based rank of id j in a by-id sorted list (keys in kd as doubles), 0 if absent
+__device__ __forceinline__ int find_rank(const double* kd, const int* kr, int K, int j) {
+  int lo = 0, hi = K;
+  const double key = (double)j;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (kd[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < K && kd[lo] == key) ? kr[lo] : 0;
+}
+
+// 1-based full rank of (dq, jq) among all j != self of a row
+template <class Dist>
+__device__ int full_rank(const Dist& dist, int64_t m, int self, double dq, int jq, int* s_tmp) {
+  int c = 0;
+  for (int64_t j = threadIdx.x; j < m; j += NT)
+    if (j != self && lt(dist(j), (int)j, dq, jq)) ++c;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) atomicAdd(s_tmp, c);
+  __syncthreads();
+  const int r = *s_tmp + 1;
+  __syncthreads();
+  if (threadIdx.x == 0) *s_tmp = 0;
+  __syncthreads();
+  return r;
+}
+
+struct Shared {
+  double sd[NB];
+  int sj[NB];
+  int hd_ids[KMAX], ld_ids[KMAX];
+  unsigned agree[KMAX + 1], same_ld[KMAX], same_hd[KMAX];
+  int need_hd_j[KMAX], need_hd_r[KMAX], need_ld_j[KMAX], need_ld_r[KMAX];
+  unsigned long long trust[MAX_REPORT], cont[MAX_REPORT];
+  int cnt, n_need_hd, n_need_ld, tmp;
+};
+
+__global__ void __launch_bounds__(NT) k_curve_rows(const double* __restrict__ hd_block, int64_t r0, int nb, int64_t m,
+                                                   const double* __restrict__ y, const double* __restrict__ sqy,
+                                                   int dim, const int32_t* __restrict__ labels, int k_max, int K,
+                                                   Report rep, unsigned long long* __restrict__ g_agree,
+                                                   unsigned long long* __restrict__ g_same_ld,
+                                                   unsigned long long* __restrict__ g_same_hd,
+                                                   unsigned long long* __restrict__ g_trust,
+                                                   unsigned long long* __restrict__ g_cont) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Shared& S = *reinterpret_cast<Shared*>(smem_raw);
+  const int tid = threadIdx.x;
+  for (int t = tid; t <= KMAX; t += NT) S.agree[t] = 0;
+  for (int t = tid; t < KMAX; t += NT) S.same_ld[t] = S.same_hd[t] = 0;
+  if (tid < MAX_REPORT) S.trust[tid] = S.cont[tid] = 0;
+  if (tid == 0) S.n_need_hd = S.n_need_ld = S.tmp = 0;
+  __syncthreads();
+  for (int row = blockIdx.x; row < nb; row += gridDim.x) {
+    const int i = (int)(r0 + row);
+    const HdRow hd{hd_block + (int64_t)row * m};
+    LdRow ld{y, sqy, dim, {0, 0, 0}, sqy[i]};
+    for (int d = 0; d < dim; ++d) ld.yi[d] = y[(int64_t)i * dim + d];
+    const int own = labels ? labels[i] : 0;
+
+    select_row(hd, m, i, K, S.sd, S.sj, &S.cnt);
+    for (int t = tid; t < K; t += NT) {
+      S.hd_ids[t] = S.sj[t];
+      if (labels && t < k_max && labels[S.sj[t]] == own) ++S.same_hd[t];  // one writer per slot
+    }
+    __syncthreads();
+    select_row(ld, m, i, K, S.sd, S.sj, &S.cnt);
+    for (int t = tid; t < K; t += NT) {
+      S.ld_ids[t] = S.sj[t];
+      if (labels && t < k_max && labels[S.sj[t]] == own) ++S.same_ld[t];
+    }
+    __syncthreads();
+    // by-id lists: [0, KMAX) = HD (id, rank), [KMAX, NB) = LD (id, rank)
+    for (int t = tid; t < KMAX; t += NT) {
+      S.sd[t] = t < K ? (double)S.hd_ids[t] : INFINITY;
+      S.sj[t] = t + 1;
+      S.sd[KMAX + t] = t < K ? (double)S.ld_ids[t] : INFINITY;
+      S.sj[KMAX + t] = t + 1;
+    }
+    __syncthreads();
+    bitonic(S.sd, S.sj, NB, KMAX);
+    for (int t = tid; t < K; t += NT) {
+      {  // LD neighbour of rank rl: agreement and trustworthiness entrants
+        const int rl = t + 1, rh = find_rank(S.sd, S.sj, K, S.ld_ids[t]);
+        if (rh) {
+          const int p = max(rh, rl);
+          if (p <= k_max) atomicAdd(&S.agree[p], 1u);
+        }
+        if (rl <= rep.kmax) {
+          if (!rh) {
+            const int q = atomicAdd(&S.n_need_hd, 1);
+            S.need_hd_j[q] = S.ld_ids[t];
+            S.need_hd_r[q] = rl;
+          } else {
+            for (int a = 0; a < rep.n; ++a)
+              if (rl <= rep.k[a] && rh > rep.k[a]) atomicAdd(&S.trust[a], (unsigned long long)(rh - rep.k[a]));
+          }
+        }
+      }
+      {  // HD neighbour of rank rh: continuity leavers
+        const int rh = t + 1;
+        if (rh <= rep.kmax) {
+          const int rl = find_rank(S.sd + KMAX, S.sj + KMAX, K, S.hd_ids[t]);
+          if (!rl) {
+            const int q = atomicAdd(&S.n_need_ld, 1);
+            S.need_ld_j[q] = S.hd_ids[t];
+            S.need_ld_r[q] = rh;
+          } else {
+            for (int a = 0; a < rep.n; ++a)
+              if (rh <= rep.k[a] && rl > rep.k[a]) atomicAdd(&S.cont[a], (unsigned long long)(rl - rep.k[a]));
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ranks beyond the lists: one counting pass over the row per neighbour
+    const int nh = S.n_need_hd, nl = S.n_need_ld;
+    for (int q = 0; q < nh; ++q) {
+      const int jq = S.need_hd_j[q];
+      const int rank = full_rank(hd, m, i, hd(jq), jq, &S.tmp);
+      if (tid < rep.n && S.need_hd_r[q] <= rep.k[tid]) S.trust[tid] += (unsigned long long)(rank - rep.k[tid]);
+    }
+    for (int q = 0; q < nl; ++q) {
+      const int jq = S.need_ld_j[q];
+      const int rank = full_rank(ld, m, i, ld(jq), jq, &S.tmp);
+      if (tid < rep.n && S.need_ld_r[q] <= rep.k[tid]) S.cont[tid] += (unsigned long long)(rank - rep.k[tid]);
+    }
+    __syncthreads();
+    if (tid == 0) S.n_need_hd = S.n_need_ld = 0;
+    __syncthreads();
+  }
+  for (int t = tid; t <= k_max; t += NT)
+    if (S.agree[t]) atomicAdd(&g_agree[t], (unsigned long long)S.agree[t]);
+  if (labels)
+    for (int t = tid; t < k_max; t += NT) {
+      if (S.same_ld[t]) atomicAdd(&g_same_ld[t], (unsigned long long)S.same_ld[t]);
+      if (S.same_hd[t]) atomicAdd(&g_same_hd[t], (unsigned long long)S.same_hd[t]);
+    }
+  if (tid < rep.n) {
+    atomicAdd(&g_trust[tid], S.trust[tid]);
+    atomicAdd(&g_cont[tid], S.cont[tid]);
+  }
+}
+
+}  // namespace curves
+
 }  // namespace metrics
 
 using namespace metrics;
@@ -374,6 +695,111 @@ int ivhd_neighbor_hit(int device, const double* y, int64_t m, int32_t dim, const
   cudaStreamDestroy(st);
   if (rc != IVHD_OK) return rc;
   if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "neighbor_hit: %s", cudaGetErrorString(e));
+  return IVHD_OK;
+}
+
+
+int ivhd_curve_pass(int device, const double* x, int64_t m, int32_t n, int32_t x_precomputed, const double* y,
+                    int32_t dim, const int32_t* labels, int32_t k_max, const int32_t* report_ks, int32_t n_report,
+                    int64_t* agree_out, int64_t* same_ld_out, int64_t* same_hd_out, int64_t* trust_out,
+                    int64_t* cont_out) {
+  using namespace curves;
+  if (!x || !y || !agree_out) return fail(IVHD_ERR_INVALID_ARG, "null pointer");
+  if (m < 3) return fail(IVHD_ERR_INVALID_ARG, "need at least 3 points");
+  if (m >= 0x7fffffffLL) return fail(IVHD_ERR_INVALID_ARG, "M too large");
+  if (dim < 1 || dim > 3) return fail(IVHD_ERR_INVALID_ARG, "embedding dimension must be 1..3, got %d", dim);
+  if (x_precomputed ? n != m : n < 1) return fail(IVHD_ERR_INVALID_ARG, "bad source shape (m=%lld, n=%d)", (long long)m, n);
+  if (!(1 <= k_max && k_max <= m - 2)) return fail(IVHD_ERR_INVALID_ARG, "k_max must be in [1, %lld]", (long long)(m - 2));
+  if (n_report < 0 || n_report > MAX_REPORT || (n_report && !report_ks))
+    return fail(IVHD_ERR_INVALID_ARG, "at most %d report ks", MAX_REPORT);
+  if (labels && (!same_ld_out || !same_hd_out)) return fail(IVHD_ERR_INVALID_ARG, "null label-count output");
+  if (n_report && (!trust_out || !cont_out)) return fail(IVHD_ERR_INVALID_ARG, "null trust/continuity output");
+  Report rep{};
+  rep.n = n_report;
+  for (int a = 0; a < n_report; ++a) {
+    if (!(1 <= report_ks[a] && 2LL * report_ks[a] < m))
+      return fail(IVHD_ERR_INVALID_ARG, "k must satisfy 1 <= k < M/2, got %d", report_ks[a]);
+    rep.k[a] = report_ks[a];
+    rep.kmax = std::max(rep.kmax, rep.k[a]);
+  }
+  const int K = (int)std::min<int64_t>(std::max(k_max, rep.kmax), m - 1);
+  if (K > KMAX) return fail(IVHD_ERR_INVALID_ARG, "k_max=%d above the supported %d", K, KMAX);
+  if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail(IVHD_ERR_CUDA, "stream");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  // distance block: <= 1 GiB, at least one row
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(m, ((int64_t)1 << 27) / m));
+  double *dx = nullptr, *sqx = nullptr, *dy = nullptr, *sqy = nullptr, *blk = nullptr;
+  int32_t* dl = nullptr;
+  unsigned long long* acc = nullptr;  // agree[KMAX+1] | same_ld[KMAX] | same_hd[KMAX] | trust[8] | cont[8]
+  const size_t n_acc = (KMAX + 1) + 2 * KMAX + 2 * MAX_REPORT;
+  cudaError_t e = cudaSuccess;
+  do {
+#define MTRY(call) \
+  if ((e = (call)) != cudaSuccess) break
+    MTRY(cudaMallocAsync(&dy, sizeof(double) * m * dim, st));
+    MTRY(cudaMallocAsync(&sqy, sizeof(double) * m, st));
+    MTRY(cudaMallocAsync(&blk, sizeof(double) * nb_max * m, st));
+    MTRY(cudaMallocAsync(&acc, sizeof(unsigned long long) * n_acc, st));
+    MTRY(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * n_acc, st));
+    MTRY(cudaMemcpyAsync(dy, y, sizeof(double) * m * dim, cudaMemcpyHostToDevice, st));
+    if (labels) {
+      MTRY(cudaMallocAsync(&dl, sizeof(int32_t) * m, st));
+      MTRY(cudaMemcpyAsync(dl, labels, sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+    }
+    if (!x_precomputed) {
+      MTRY(cudaMallocAsync(&dx, sizeof(double) * m * n, st));
+      MTRY(cudaMallocAsync(&sqx, sizeof(double) * m, st));
+      MTRY(cudaMemcpyAsync(dx, x, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+      k_sqnorm<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(dx, m, n, sqx);
+    }
+    k_sqnorm<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(dy, m, dim, sqy);
+    MTRY(cudaFuncSetAttribute(k_curve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Shared)));
+    unsigned long long* g = acc;
+    for (int64_t r0 = 0; r0 < m; r0 += nb_max) {
+      const int nb = (int)std::min<int64_t>(nb_max, m - r0);
+      if (x_precomputed) {
+        MTRY(cudaMemcpyAsync(blk, x + r0 * m, sizeof(double) * nb * m, cudaMemcpyHostToDevice, st));
+      } else {
+        dim3 grid((unsigned)((m + DT - 1) / DT), (unsigned)((nb + DT - 1) / DT));
+        k_dist_block<<<grid, 256, 0, st>>>(dx, sqx, m, n, r0, nb, blk);
+      }
+      const int ctas = std::min(nb, sms * 3);
+      k_curve_rows<<<ctas, NT, sizeof(Shared), st>>>(blk, r0, nb, m, dy, sqy, dim, dl, k_max, K, rep, g,
+                                                     g + KMAX + 1, g + 2 * KMAX + 1, g + 3 * KMAX + 1,
+                                                     g + 3 * KMAX + 1 + MAX_REPORT);
+      MTRY(cudaGetLastError());
+    }
+    if (e != cudaSuccess) break;
+    std::vector<unsigned long long> h(n_acc);
+    MTRY(cudaMemcpyAsync(h.data(), acc, sizeof(unsigned long long) * n_acc, cudaMemcpyDeviceToHost, st));
+    MTRY(cudaStreamSynchronize(st));
+    for (int t = 0; t <= k_max; ++t) agree_out[t] = (int64_t)h[t];
+    if (labels)
+      for (int t = 0; t < k_max; ++t) {
+        same_ld_out[t] = (int64_t)h[KMAX + 1 + t];
+        same_hd_out[t] = (int64_t)h[2 * KMAX + 1 + t];
+      }
+    for (int a = 0; a < n_report; ++a) {
+      trust_out[a] = (int64_t)h[3 * KMAX + 1 + a];
+      cont_out[a] = (int64_t)h[3 * KMAX + 1 + MAX_REPORT + a];
+    }
+#undef MTRY
+  } while (0);
+  for (void* p : {(void*)dx, (void*)sqx, (void*)dy, (void*)sqy, (void*)blk, (void*)dl, (void*)acc})
+    if (p) cudaFreeAsync(p, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "curve_pass: %s", cudaGetErrorString(e));
   return IVHD_OK;
 }
 

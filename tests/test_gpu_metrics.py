@@ -60,3 +60,96 @@ def test_neighbor_ids_equal_kdtree_at_scale():
     rows = rng.choice(len(y), 2000, replace=False)
     _, idx = cKDTree(y).query(y[rows], k=101)
     np.testing.assert_array_equal(nbr[rows], idx[:, 1:])
+
+
+# ------------------------------------------------------------- rank curves
+from tests.golden.make_curves_golden import OUT as CURVES_GOLD, curve_inputs  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(curve_inputs()))
+def test_evaluate_embedding_matches_reference(name):
+    """GPU curve pass (ivhd_curve_pass) against the reference's
+    evaluate_embedding.  Ranks come from fp64 distances summed in a different
+    order than the reference's BLAS, so a near-tie may flip: each curve value
+    is an average of integer counts over k*M pairs; allow a few flips."""
+    from paper_2303_05455_b200 import metrics
+
+    X, Y, lab, k_max, ks, pre = curve_inputs()[name]
+    gold = np.load(CURVES_GOLD)
+    cur = metrics.evaluate_embedding(X, Y, labels=lab, k_max=k_max, nn_max=20, report_ks=ks, x_precomputed=pre)
+    m = len(Y)
+    exact = "lattice" in name or "precomp" in name  # integer arithmetic / given distances
+    tol = 0.0 if exact else 4.0 / m
+    np.testing.assert_allclose(cur.q_nx, gold[f"{name}/q_nx"], rtol=0, atol=tol + 1e-15)
+    np.testing.assert_allclose(cur.r_nx, gold[f"{name}/r_nx"], rtol=0, atol=2 * tol + 1e-15)
+    assert cur.auc_rnx == pytest.approx(float(gold[f"{name}/auc_rnx"]), abs=tol + 1e-15)
+    if lab is not None:
+        np.testing.assert_allclose(cur.g_nn, gold[f"{name}/g_nn"], rtol=0, atol=tol + 1e-15)
+        assert cur.auc_gnn == pytest.approx(float(gold[f"{name}/auc_gnn"]), abs=tol + 1e-15)
+    keep = [k for k in ks if k < m / 2]
+    np.testing.assert_allclose([cur.trust[k] for k in keep], gold[f"{name}/trust"], rtol=0, atol=tol + 1e-15)
+    np.testing.assert_allclose([cur.continuity[k] for k in keep], gold[f"{name}/continuity"], rtol=0,
+                               atol=tol + 1e-15)
+    if not pre:
+        _, _, _, auc = metrics.rnx_curve(X, Y, k_max=k_max)
+        assert auc == pytest.approx(float(gold[f"{name}/rnx_auc_direct"]), abs=tol + 1e-15)
+        t, c = metrics.trust_continuity(X, Y, ks[0])
+        np.testing.assert_allclose([t, c], gold[f"{name}/tc_direct"], rtol=0, atol=tol + 1e-15)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [0, 1])
+def test_curve_counts_equal_oracle(seed):
+    """Integer counts equal the oracle restatement (metrics.py:149-182) on
+    integer-valued inputs (exact distances, heavy ties)."""
+    import oracle as O
+    from paper_2303_05455_b200 import metrics
+
+    rng = np.random.default_rng(100 + seed)
+    m = 700 + 37 * seed
+    X = rng.integers(-4, 5, (m, 6)).astype(np.float64)
+    Y = rng.integers(-6, 7, (m, 2 + seed)).astype(np.float64)
+    lab = rng.integers(0, 5, m)
+    ks = (3, 20, 100)
+    got = metrics._curve_pass(X, Y, lab, 300, ks)
+    want = O.curve_pass(X, Y, lab, 300, ks)
+    for g, w in zip(got[:3], want[:3]):
+        np.testing.assert_array_equal(g, w)
+    assert got[3] == want[3] and got[4] == want[4]
+
+
+@pytest.mark.gpu
+def test_curves_identity_embedding_at_scale():
+    """Size-independent property at C1 scale (M=20000, several distance
+    blocks): an embedding equal to the source ranks every pair identically,
+    so Q_NX = R_NX = 1, trust = continuity = 1 and G_NN = 0."""
+    from paper_2303_05455_b200 import metrics
+
+    rng = np.random.default_rng(7)
+    m = 20000
+    X = rng.standard_normal((m, 2)) * np.array([3.0, 1.0])
+    lab = (X[:, 0] > 0).astype(np.int64)
+    cur = metrics.evaluate_embedding(X, X.copy(), labels=lab, report_ks=(15, 100))
+    np.testing.assert_array_equal(cur.q_nx, np.ones(1000))
+    assert cur.auc_rnx == pytest.approx(1.0, abs=1e-12)
+    np.testing.assert_array_equal(cur.g_nn, np.zeros(1000))
+    assert cur.trust == {15: 1.0, 100: 1.0} and cur.continuity == {15: 1.0, 100: 1.0}
+
+
+@pytest.mark.gpu
+def test_curve_errors():
+    from paper_2303_05455_b200 import metrics
+    from paper_2303_05455_b200.errors import DimensionMismatchError, InvalidArgumentError
+
+    X = np.random.default_rng(0).standard_normal((50, 4))
+    with pytest.raises(InvalidArgumentError):
+        metrics.rnx_curve(X, X[:, :2], k_max=49)
+    with pytest.raises(DimensionMismatchError):
+        metrics.rnx_curve(X, X[:40, :2])
+    with pytest.raises(InvalidArgumentError):
+        metrics.gnn_curve(X, X[:, :2], None)
+    with pytest.raises(InvalidArgumentError):
+        metrics.trust_continuity(X, X[:, :2], 25)
+    with pytest.raises(InvalidArgumentError):
+        metrics.rnx_curve(X[:3], X[:3, :2])
