@@ -435,20 +435,59 @@ __device__ __forceinline__ int find_rank(const double* kd, const int* kr, int K,
   return (lo < K && kd[lo] == key) ? kr[lo] : 0;
 }
 
-// 1-based full rank of (dq, jq) among all j != self of a row
+// Exact 1-based ranks, among all j != self of a row, of Q query ids that lie
+// outside the row's ranked list: one pass over the row.  The queries are
+// sorted by (d2, id) in qd/qj; every row element lands (binary search) on the
+// first query above it, diff[] counts those landings, and a query's rank is
+// one plus the landings at or below its sorted position.
 template <class Dist>
-__device__ int full_rank(const Dist& dist, int64_t m, int self, double dq, int jq, int* s_tmp) {
-  int c = 0;
-  for (int64_t j = threadIdx.x; j < m; j += NT)
-    if (j != self && lt(dist(j), (int)j, dq, jq)) ++c;
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0) atomicAdd(s_tmp, c);
+__device__ void far_ranks(const Dist& dist, int64_t m, int self, int Q, const int* need_j, double* qd, int* qj,
+                          int* diff) {
+  for (int t = threadIdx.x; t < KMAX; t += NT) {
+    qd[t] = t < Q ? dist(need_j[t]) : INFINITY;
+    qj[t] = t < Q ? need_j[t] : 0x7fffffff;
+    diff[t] = 0;
+  }
   __syncthreads();
-  const int r = *s_tmp + 1;
+  bitonic(qd, qj, KMAX, KMAX);
+  for (int64_t j = threadIdx.x; j < m; j += NT) {
+    if (j == self) continue;
+    const double d = dist(j);
+    int lo = 0, hi = Q;  // first query q with (d, j) < (qd[q], qj[q])
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (lt(d, (int)j, qd[mid], qj[mid])) hi = mid;
+      else lo = mid + 1;
+    }
+    if (lo < Q) atomicAdd(&diff[lo], 1);
+  }
   __syncthreads();
-  if (threadIdx.x == 0) *s_tmp = 0;
+  if (threadIdx.x < 32) {  // inclusive scan of diff[0..Q) by one warp
+    int carry = 0;
+    for (int b = 0; b < Q; b += 32) {
+      const int t = b + threadIdx.x;
+      int v = t < Q ? diff[t] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (threadIdx.x >= o) v += u;
+      }
+      if (t < Q) diff[t] = v + carry;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
   __syncthreads();
-  return r;
+}
+
+// rank of query id jq (distance dq) after far_ranks
+__device__ __forceinline__ int far_rank_of(const double* qd, const int* qj, const int* diff, int Q, double dq, int jq) {
+  int lo = 0, hi = Q;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (lt(qd[mid], qj[mid], dq, jq)) lo = mid + 1;
+    else hi = mid;
+  }
+  return diff[lo] + 1;
 }
 
 struct Shared {
@@ -457,8 +496,9 @@ struct Shared {
   int hd_ids[KMAX], ld_ids[KMAX];
   unsigned agree[KMAX + 1], same_ld[KMAX], same_hd[KMAX];
   int need_hd_j[KMAX], need_hd_r[KMAX], need_ld_j[KMAX], need_ld_r[KMAX];
+  int diff[KMAX];
   unsigned long long trust[MAX_REPORT], cont[MAX_REPORT];
-  int cnt, n_need_hd, n_need_ld, tmp;
+  int cnt, n_need_hd, n_need_ld;
 };
 
 __global__ void __launch_bounds__(NT) k_curve_rows(const double* __restrict__ hd_block, int64_t r0, int nb, int64_t m,
@@ -475,7 +515,7 @@ __global__ void __launch_bounds__(NT) k_curve_rows(const double* __restrict__ hd
   for (int t = tid; t <= KMAX; t += NT) S.agree[t] = 0;
   for (int t = tid; t < KMAX; t += NT) S.same_ld[t] = S.same_hd[t] = 0;
   if (tid < MAX_REPORT) S.trust[tid] = S.cont[tid] = 0;
-  if (tid == 0) S.n_need_hd = S.n_need_ld = S.tmp = 0;
+  if (tid == 0) S.n_need_hd = S.n_need_ld = 0;
   __syncthreads();
   for (int row = blockIdx.x; row < nb; row += gridDim.x) {
     const int i = (int)(r0 + row);
@@ -539,17 +579,26 @@ __global__ void __launch_bounds__(NT) k_curve_rows(const double* __restrict__ hd
       }
     }
     __syncthreads();
-    // ranks beyond the lists: one counting pass over the row per neighbour
+    // ranks beyond the lists: one batched counting pass over the row per space
     const int nh = S.n_need_hd, nl = S.n_need_ld;
-    for (int q = 0; q < nh; ++q) {
-      const int jq = S.need_hd_j[q];
-      const int rank = full_rank(hd, m, i, hd(jq), jq, &S.tmp);
-      if (tid < rep.n && S.need_hd_r[q] <= rep.k[tid]) S.trust[tid] += (unsigned long long)(rank - rep.k[tid]);
+    if (nh) {
+      far_ranks(hd, m, i, nh, S.need_hd_j, S.sd, S.sj, S.diff);
+      for (int q = tid; q < nh; q += NT) {
+        const int jq = S.need_hd_j[q];
+        const int rank = far_rank_of(S.sd, S.sj, S.diff, nh, hd(jq), jq);
+        for (int a = 0; a < rep.n; ++a)
+          if (S.need_hd_r[q] <= rep.k[a]) atomicAdd(&S.trust[a], (unsigned long long)(rank - rep.k[a]));
+      }
+      __syncthreads();
     }
-    for (int q = 0; q < nl; ++q) {
-      const int jq = S.need_ld_j[q];
-      const int rank = full_rank(ld, m, i, ld(jq), jq, &S.tmp);
-      if (tid < rep.n && S.need_ld_r[q] <= rep.k[tid]) S.cont[tid] += (unsigned long long)(rank - rep.k[tid]);
+    if (nl) {
+      far_ranks(ld, m, i, nl, S.need_ld_j, S.sd, S.sj, S.diff);
+      for (int q = tid; q < nl; q += NT) {
+        const int jq = S.need_ld_j[q];
+        const int rank = far_rank_of(S.sd, S.sj, S.diff, nl, ld(jq), jq);
+        for (int a = 0; a < rep.n; ++a)
+          if (S.need_ld_r[q] <= rep.k[a]) atomicAdd(&S.cont[a], (unsigned long long)(rank - rep.k[a]));
+      }
     }
     __syncthreads();
     if (tid == 0) S.n_need_hd = S.n_need_ld = 0;
