@@ -457,6 +457,17 @@ def gpu_arm(args, w):
         quality = {"neighbor_hit_cf": cf, "cf_2": float(cf_nn[1]), "cf_10": float(cf_nn[9]),
                    "seconds": time.perf_counter() - t0,
                    "note": "metrics.neighbor_hit(nn_max=100) of the e2e embedding on the GPU (exact grid kNN)"}
+        # rank curves (R_NX / G_NN AUC, trust/continuity) on a fixed seeded
+        # subsample: the O(M^2) metrics, as SURVEY §8(c) prescribes above 20k
+        x_all, _ = synth.mixture_points(m, w["n"], seed=0)
+        sub = np.sort(np.random.default_rng(0).choice(m, size=min(m, 20000), replace=False))
+        xs, ys, ls = x_all[sub].astype(np.float64), final_points[sub], labels[sub]
+        del x_all
+        t0 = time.perf_counter()
+        cur = metrics.evaluate_embedding(xs, ys, labels=ls, nn_max=100, report_ks=(15, 100), device=local)
+        quality["curves"] = {**cur.summary(), "seconds": time.perf_counter() - t0,
+                             "sample": f"{len(sub)} rows, sorted default_rng(0).choice(M)",
+                             "note": "metrics.evaluate_embedding on the GPU (curve pass k_max=1000)"}
 
     if rank == 0:
         peak = float(peaks.get("hbm_gbs", 6650.0))
