@@ -252,3 +252,34 @@ def test_run_embedding_builds_graph_from_dataset():
     c = run_embedding(dataset=ds, config=cfg2)
     d = run_embedding(graph=build_exact_knn(x, 3), helper_graph=build_exact_knn(x, 12), dataset=ds, config=cfg2)
     np.testing.assert_array_equal(c.embedding.points, d.embedding.points)
+
+
+def test_c2_fixture_quality_matches_reference_within_1pct():
+    """North star acceptance on SURVEY §8(d)'s discriminating C2 fixture
+    (mnist_like 70k -> PCA 100 -> exact 2-NN graph, nn=2 rn=1 c=0.01, FD,
+    2500 iterations; tests/golden/make_quality_golden.py): final stress,
+    neighbour hit (cf, cf_2, cf_10 over all 70k points) and the rank-curve
+    metrics on a fixed 2000-row subsample (AUC R_NX, AUC G_NN, trust /
+    continuity at 15 and 100) agree with the reference's run within 1%."""
+    import os
+
+    from paper_2303_05455_b200 import metrics
+    from tests.golden.make_quality_golden import OUT, subsample
+
+    g = np.load(OUT)
+    nb, labels = g["neighbors"], g["labels"].astype(np.int64)
+    cfg = P.EmbeddingConfig(nn=2, rn=1, c=0.01, iterations=2500, seed=0)
+    res = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    y = res.embedding.points
+    assert res.state.stress == pytest.approx(float(g["stress"]), rel=1e-2)
+    cf_nn, cf = metrics.neighbor_hit(y, labels, nn_max=100)
+    ref_nn = g["cf_nn"]
+    for got, want in ((cf, ref_nn.mean()), (cf_nn[1], ref_nn[1]), (cf_nn[9], ref_nn[9])):
+        assert got == pytest.approx(float(want), rel=1e-2)
+    sub = subsample()
+    cur = metrics.evaluate_embedding(g["x_sub"], y[sub], labels=labels[sub], report_ks=(15, 100))
+    print(os.linesep, cur.summary(), float(g["auc_rnx"]), float(g["auc_gnn"]), g["trust"], g["continuity"])
+    assert cur.auc_rnx == pytest.approx(float(g["auc_rnx"]), rel=1e-2)
+    assert cur.auc_gnn == pytest.approx(float(g["auc_gnn"]), rel=1e-2)
+    np.testing.assert_allclose([cur.trust[15], cur.trust[100]], g["trust"], rtol=1e-2)
+    np.testing.assert_allclose([cur.continuity[15], cur.continuity[100]], g["continuity"], rtol=1e-2)
