@@ -115,6 +115,12 @@ int ivhd_set_connections(ivhd_ctx* ctx, int slot, const int32_t* edges,
 int ivhd_set_positions(ivhd_ctx* ctx, const double* y);      /* (m, dim) */
 int ivhd_get_positions(ivhd_ctx* ctx, double* y_out);        /* (m, dim) */
 int ivhd_get_deltas(ivhd_ctx* ctx, double* d_out);           /* (m, dim) */
+/* Page-locked host buffers (cudaHostAlloc, portable) for result arrays: the
+ * positions / deltas copies above run at full PCIe/C2C rate into them and need
+ * no first-touch page faults.  No reference counterpart (host memory of the
+ * arrays engine.py:379-413 returns). */
+int ivhd_host_alloc(int device, uint64_t bytes, void** out);
+int ivhd_host_free(void* p);
 int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p); /* resets state */
 int ivhd_set_step_size(ivhd_ctx* ctx, double step);
 int ivhd_get_step_size(ivhd_ctx* ctx, double* step_out);

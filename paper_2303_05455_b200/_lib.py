@@ -7,6 +7,7 @@ present, the first call raises DeviceError.
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -85,6 +86,8 @@ SIGNATURES = {
     "ivhd_metrics_last_error": (ctypes.c_char_p, []),
     "ivhd_neighbor_hit": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, c_i32p,
                                          ctypes.c_int32, c_f64p, c_i32p]),
+    "ivhd_host_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
+    "ivhd_host_free": (ctypes.c_int, [ctypes.c_void_p]),
     "ivhd_curve_pass": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                        c_f64p, ctypes.c_int32, c_i32p, ctypes.c_int32, c_i32p, ctypes.c_int32,
                                        c_i64p, c_i64p, c_i64p, c_i64p, c_i64p]),
@@ -146,3 +149,49 @@ def check(code, ctx_handle=None):
     if code == ERR_DIVERGED:
         raise StatusError(code, msg)
     raise DeviceError(f"ivhd status {code}: {msg}")
+
+
+class PinnedPool:
+    """Page-locked host buffers for result arrays (positions, deltas), recycled
+    when the arrays that use them are garbage-collected.
+
+    A run's device -> host copies land directly in them at full link rate, and
+    a recycled buffer has no first-touch page faults (fresh 22 MB arrays cost
+    ~5 ms each at C3).  Arrays below 1 MiB, above `max_bytes`, or beyond
+    `cap_bytes` of outstanding pinned memory are plain numpy allocations.
+    """
+
+    def __init__(self, max_bytes=512 << 20, cap_bytes=2 << 30):
+        self.max_bytes = max_bytes
+        self.cap_bytes = cap_bytes
+        self._free = {}  # nbytes -> [address]
+        self._outstanding = 0
+        self._lock = threading.Lock()
+
+    def empty(self, shape, device=0):
+        n = int(np.prod(shape))
+        nbytes = n * 8
+        if nbytes < (1 << 20) or nbytes > self.max_bytes:
+            return np.empty(shape)
+        with self._lock:
+            lst = self._free.get(nbytes)
+            addr = lst.pop() if lst else None
+            if addr is None:
+                if self._outstanding + nbytes > self.cap_bytes:
+                    return np.empty(shape)
+                out = ctypes.c_void_p()
+                if load().ivhd_host_alloc(int(device), nbytes, ctypes.byref(out)) != OK or not out.value:
+                    return np.empty(shape)
+                addr = out.value
+            self._outstanding += nbytes
+        buf = (ctypes.c_char * nbytes).from_address(addr)
+        weakref.finalize(buf, self._release, addr, nbytes)
+        return np.frombuffer(buf, dtype=np.float64, count=n).reshape(shape)
+
+    def _release(self, addr, nbytes):
+        with self._lock:
+            self._outstanding -= nbytes
+            self._free.setdefault(nbytes, []).append(addr)
+
+
+pinned = PinnedPool()

@@ -900,6 +900,19 @@ const char* ivhd_global_error(void) { return g_error.c_str(); }
 
 const char* ivhd_last_error(const ivhd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_error.c_str(); }
 
+int ivhd_host_alloc(int device, uint64_t bytes, void** out) {
+  if (!out || !bytes) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null output or zero size");
+  *out = nullptr;
+  CU(nullptr, cudaSetDevice(device));
+  CU(nullptr, cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+  return IVHD_OK;
+}
+
+int ivhd_host_free(void* p) {
+  if (p) CU(nullptr, cudaFreeHost(p));
+  return IVHD_OK;
+}
+
 int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream) {
   if (!out) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null output pointer");
   *out = nullptr;

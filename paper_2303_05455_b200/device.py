@@ -46,6 +46,7 @@ class DeviceEmbedding:
         self.lib = _lib.load()
         self.m = int(m)
         self.dim = int(dim)
+        self.device = int(device)
         h = ctypes.c_void_p()
         check(self.lib.ivhd_create(ctypes.byref(h), int(device), self.m, self.dim, int(stream)))
         self.h = h
@@ -131,13 +132,15 @@ class DeviceEmbedding:
             raise InvalidArgumentError(f"positions must be ({self.m}, {self.dim})")
         self._check(self.lib.ivhd_set_positions(self.h, y.ctypes.data_as(c_f64p)))
 
-    def positions(self):
-        out = np.empty((self.m, self.dim))
+    def positions(self, out=None):
+        out = np.empty((self.m, self.dim)) if out is None else out
+        assert out.shape == (self.m, self.dim) and out.dtype == np.float64 and out.flags.c_contiguous
         self._check(self.lib.ivhd_get_positions(self.h, out.ctypes.data_as(c_f64p)))
         return out
 
-    def deltas(self):
-        out = np.empty((self.m, self.dim))
+    def deltas(self, out=None):
+        out = np.empty((self.m, self.dim)) if out is None else out
+        assert out.shape == (self.m, self.dim) and out.dtype == np.float64 and out.flags.c_contiguous
         self._check(self.lib.ivhd_get_deltas(self.h, out.ctypes.data_as(c_f64p)))
         return out
 

@@ -18,6 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _lib
 from .config import EmbeddingConfig, coerce_config, resolve_optimizer
 from .config import OPTIMIZER_KINDS
 from .device import DeviceEmbedding, is_pcg64
@@ -513,12 +514,17 @@ def run_embedding(graph=None, config=None, dataset=None, helper_graph=None, obse
             state.stress = float(stress[done - 1])
         it = end
 
-    positions = dev.positions() if ran else sess.y0.copy()
+    # result arrays in recycled page-locked host memory (_lib.PinnedPool): the
+    # copies run at link rate with no first-touch faults; the embedding gets its
+    # own copy of the final positions (engine.py:413), read from the device again
+    shape = (sess.m, sess.dim)
+    positions = dev.positions(out=_lib.pinned.empty(shape, dev.device)) if ran else sess.y0.copy()
     state.positions = positions
     state.rn_assignments = sess.rn
-    state.deltas = dev.deltas() if ran else np.zeros((sess.m, sess.dim))
+    state.deltas = dev.deltas(out=_lib.pinned.empty(shape, dev.device)) if ran else np.zeros(shape)
     if total == 0 or state.stress != state.stress:
         state.stress = dev.stress(0, "l2", sess.c, positions)
+    emb_points = dev.positions(out=_lib.pinned.empty(shape, dev.device)) if ran else positions.copy()
     dev.close()
-    emb = Embedding(positions.copy(), labels=sess.labels)
+    emb = Embedding(emb_points, labels=sess.labels)
     return RunResult(embedding=emb, trace=trace, state=state, mutations=mutations)

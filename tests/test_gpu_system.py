@@ -283,3 +283,29 @@ def test_c2_fixture_quality_matches_reference_within_1pct():
     assert cur.auc_gnn == pytest.approx(float(g["auc_gnn"]), rel=1e-2)
     np.testing.assert_allclose([cur.trust[15], cur.trust[100]], g["trust"], rtol=1e-2)
     np.testing.assert_allclose([cur.continuity[15], cur.continuity[100]], g["continuity"], rtol=1e-2)
+
+
+def test_result_arrays_in_recycled_pinned_buffers():
+    """run_embedding's result arrays come from the pinned pool: independent
+    buffers (the embedding is its own copy, engine.py:413), recycled once the
+    arrays die, values equal across runs."""
+    import gc
+
+    from paper_2303_05455_b200 import _lib, synth
+
+    nb = synth.planted_graph(200_000, 2, seed=1)
+    cfg = P.EmbeddingConfig(nn=2, rn=1, c=0.1, iterations=20, seed=0)
+    r1 = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    pts, pos, dl = r1.embedding.points, r1.state.positions, r1.state.deltas
+    assert pts.ctypes.data != pos.ctypes.data and pos.ctypes.data != dl.ctypes.data
+    np.testing.assert_array_equal(pts, pos)
+    keep = pts.copy()
+    pos[0, 0] += 1.0
+    assert pts[0, 0] == keep[0, 0]
+    addrs = {pts.ctypes.data, pos.ctypes.data, dl.ctypes.data}
+    del r1, pts, pos, dl
+    gc.collect()
+    r2 = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    assert {r2.embedding.points.ctypes.data, r2.state.positions.ctypes.data, r2.state.deltas.ctypes.data} == addrs
+    np.testing.assert_array_equal(r2.embedding.points, keep)
+    assert _lib.pinned._outstanding == 3 * 200_000 * 2 * 8
