@@ -423,6 +423,98 @@ __device__ void select_row(const Dist& dist, int64_t m, int self, int K, double*
   merge_pending(sd, sj, s_cnt);
 }
 
+// Radix select of the same K smallest (d2, j): up to three 12-bit histogram
+// passes over the row's distance bits (non-negative fp64 bit patterns order
+// like the values) narrow down the bucket that holds the K-th key; every key
+// below that bucket and the whole bucket are then collected and sorted once.
+// Returns false (nothing written) when the bucket is too crowded to collect —
+// exact ties of many points — and the caller falls back to select_row.
+// The histogram aliases sd, the per-thread bin sums alias sj.
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  return (unsigned long long)__double_as_longlong(d + 0.0);  // -0 -> +0
+}
+
+template <class Dist>
+__device__ bool select_radix(const Dist& dist, int64_t m, int self, int K, double* sd, int* sj, int* s_misc) {
+  unsigned* hist = reinterpret_cast<unsigned*>(sd);  // 4096 bins
+  int* tsum = sj;                                    // 512 per-thread sums
+  unsigned long long prefix = 0;
+  int sh = 64, need = K, below = 0, bucket = 0;
+  for (int level = 0; level < 3; ++level) {
+    const int nsh = sh - 12;
+    for (int t = threadIdx.x; t < 4096; t += NT) hist[t] = 0;
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < m; j += NT) {
+      if (j == self) continue;
+      const unsigned long long k = dkey(dist(j));
+      if (level == 0 || (k >> sh) == prefix) atomicAdd(&hist[(k >> nsh) & 4095], 1u);
+    }
+    __syncthreads();
+    {
+      int a = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) a += hist[threadIdx.x * 8 + b];
+      tsum[threadIdx.x] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // find the bin where the running count reaches `need`
+      const int lane = threadIdx.x;
+      int a = 0;
+      for (int t = 0; t < 16; ++t) a += tsum[lane * 16 + t];
+      int incl = a;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
+      const int L = __ffs(hit) - 1;  // hit != 0: the row has >= need keys in this group
+      if (lane == L) {
+        int run = incl - a;
+        int t = lane * 16;
+        while (run + tsum[t] < need) run += tsum[t++];
+        int b = t * 8;
+        while (run + (int)hist[b] < need) run += hist[b++];
+        s_misc[0] = b;
+        s_misc[1] = run;
+        s_misc[2] = (int)hist[b];
+      }
+    }
+    __syncthreads();
+    const int b = s_misc[0];
+    need -= s_misc[1];
+    below += s_misc[1];
+    bucket = s_misc[2];
+    prefix = (prefix << 12) | (unsigned long long)b;
+    sh = nsh;
+    __syncthreads();
+    if (below + bucket <= NB) break;
+  }
+  if (below + bucket > NB) return false;
+  // collect every key below the bucket and the bucket itself, then sort once
+  if (threadIdx.x == 0) s_misc[3] = 0;
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < m; j += NT) {
+    if (j == self) continue;
+    const double d = dist(j);
+    if ((dkey(d) >> sh) <= prefix) {
+      const int p = atomicAdd(&s_misc[3], 1);
+      sd[p] = d;
+      sj[p] = (int)j;
+    }
+  }
+  __syncthreads();
+  const int n = s_misc[3];
+  const int N = n <= KMAX ? KMAX : NB;
+  for (int t = n + threadIdx.x; t < N; t += NT) {
+    sd[t] = INFINITY;
+    sj[t] = 0x7fffffff;
+  }
+  __syncthreads();
+  bitonic(sd, sj, N, N);
+  return true;
+}
+
 // 1-based rank of id j in a by-id sorted list (keys in kd as doubles), 0 if absent
 __device__ __forceinline__ int find_rank(const double* kd, const int* kr, int K, int j) {
   int lo = 0, hi = K;
@@ -499,6 +591,7 @@ struct Shared {
   int diff[KMAX];
   unsigned long long trust[MAX_REPORT], cont[MAX_REPORT];
   int cnt, n_need_hd, n_need_ld;
+  int misc[4];
 };
 
 __global__ void __launch_bounds__(NT) k_curve_rows(const double* __restrict__ hd_block, int64_t r0, int nb, int64_t m,
@@ -524,13 +617,13 @@ __global__ void __launch_bounds__(NT) k_curve_rows(const double* __restrict__ hd
     for (int d = 0; d < dim; ++d) ld.yi[d] = y[(int64_t)i * dim + d];
     const int own = labels ? labels[i] : 0;
 
-    select_row(hd, m, i, K, S.sd, S.sj, &S.cnt);
+    if (!select_radix(hd, m, i, K, S.sd, S.sj, S.misc)) select_row(hd, m, i, K, S.sd, S.sj, &S.cnt);
     for (int t = tid; t < K; t += NT) {
       S.hd_ids[t] = S.sj[t];
       if (labels && t < k_max && labels[S.sj[t]] == own) ++S.same_hd[t];  // one writer per slot
     }
     __syncthreads();
-    select_row(ld, m, i, K, S.sd, S.sj, &S.cnt);
+    if (!select_radix(ld, m, i, K, S.sd, S.sj, S.misc)) select_row(ld, m, i, K, S.sd, S.sj, &S.cnt);
     for (int t = tid; t < K; t += NT) {
       S.ld_ids[t] = S.sj[t];
       if (labels && t < k_max && labels[S.sj[t]] == own) ++S.same_ld[t];
