@@ -153,3 +153,23 @@ def test_curve_errors():
         metrics.trust_continuity(X, X[:, :2], 25)
     with pytest.raises(InvalidArgumentError):
         metrics.rnx_curve(X[:3], X[:3, :2])
+
+
+@pytest.mark.gpu
+def test_curve_counts_tie_crowded_rows_equal_oracle():
+    """Rows whose K-th distance is shared by > 1000 points (3000 points on 4
+    embedded locations) take the merge fallback of the radix select; counts
+    still equal the oracle's (index tie rule)."""
+    import oracle as O
+    from paper_2303_05455_b200 import metrics
+
+    rng = np.random.default_rng(9)
+    m = 3000
+    X = rng.integers(0, 3, (m, 4)).astype(np.float64)
+    Y = rng.integers(0, 2, (m, 2)).astype(np.float64)
+    lab = rng.integers(0, 3, m)
+    got = metrics._curve_pass(X, Y, lab, 1000, (10, 100))
+    want = O.curve_pass(X, Y, lab, 1000, (10, 100))
+    for g, w in zip(got[:3], want[:3]):
+        np.testing.assert_array_equal(g, w)
+    assert got[3] == want[3] and got[4] == want[4]
