@@ -268,22 +268,6 @@ __global__ void k_row_ptr(const uint32_t* __restrict__ keys, int64_t n, int64_t 
   }
 }
 
-__global__ void k_fill_cols(const uint32_t* __restrict__ vals, int64_t n, int64_t L,
-                            const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
-                            const uint8_t* __restrict__ rand, int64_t n_nn,
-                            const float* __restrict__ tgt, const float* __restrict__ scl,
-                            uint32_t* __restrict__ col, float2* __restrict__ ew) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t h = vals[k];
-    const int64_t e = h < L ? h : h - L;
-    const uint32_t other = (uint32_t)(h < L ? dst[e] : src[e]);
-    const bool rn = rand ? (rand[e] != 0) : (e >= n_nn);
-    col[k] = other | (rn ? kRandBit : 0u);
-    if (ew) ew[k] = make_float2(tgt ? tgt[e] : (rn ? 1.f : 0.f), scl ? scl[e] : 1.f);
-  }
-}
-
 __global__ void k_binary_edges(const int32_t* __restrict__ nn, int64_t stride, int ncols,
                                const int32_t* __restrict__ rn, int nrn, int64_t m,
                                int32_t* __restrict__ src, int32_t* __restrict__ dst) {

@@ -63,7 +63,6 @@ constexpr int THREADS = 64 + 128 * EG;   // producer warp, MMA warp, 4*EG epilog
 constexpr int CHUNK_BYTES = TQ * KC * 4;                // 16 KB: one 128-row image chunk
 constexpr int BCHUNK_BYTES = HALVES * CHUNK_BYTES;      // candidate chunk (TCN rows)
 constexpr int STAGE_BYTES = CHUNK_BYTES + BCHUNK_BYTES; // A + B chunk (query tile not resident)
-constexpr int LIST_BYTES = EG * 2 * KMAX * TQ * 4;      // per-group (d2, id) lists (host sizes them by keep)
 
 // byte offset of element (r, k) inside a chunk image with kc floats per row:
 // core matrices of 8 rows x 16 bytes; K-chunk stride (LBO) 128 bytes, 8-row
@@ -207,9 +206,9 @@ __global__ void k_normalize(double* __restrict__ X, int64_t m, int n, long long*
 
 // ---------------------------------------------------------- candidate pass
 // RES: the query tile (all K chunks) is loaded once and stays in shared
-// memory (kp <= KP_RES); otherwise each ring stage carries the query chunk
-// next to the candidate chunk.
-constexpr int KP_RES = 256;
+// memory when the deepest ring still fits beside it (decided at launch from the
+// shared-memory plan); otherwise each ring stage carries the query chunk next to
+// the candidate chunk.
 constexpr int STAGES_RES = 4;
 // dynamic shared memory: [query tile (RES)] [ring] [EG x 2 x keep x TQ lists]
 inline int tc_smem_bytes(bool res, int kp, int keep, int nst) {

@@ -372,7 +372,6 @@ __device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
 // count.
 template <int OPT>
 __device__ void finalize_block(const StepArgs& A, double4* sm, const double4* src, int n) {
-  Ctrl* ctrl = A.ctrl;
   const double2* p2 = reinterpret_cast<const double2*>(src);
   double4 s = make_double4(0, 0, 0, 0);
   for (int t0 = threadIdx.x; t0 < n; t0 += 8 * kBlock) {
