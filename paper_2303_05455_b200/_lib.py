@@ -157,15 +157,24 @@ class PinnedPool:
 
     A run's device -> host copies land directly in them at full link rate, and
     a recycled buffer has no first-touch page faults (fresh 22 MB arrays cost
-    ~5 ms each at C3).  Arrays below 1 MiB, above `max_bytes`, or beyond
-    `cap_bytes` of outstanding pinned memory are plain numpy allocations.
+    ~5 ms each at C3).  Pinned bytes (handed out + pooled) stay below
+    `cap_bytes` (default min(16 GiB, 1/8 of physical memory)); pooled buffers of
+    other sizes are released to make room.  Arrays below 1 MiB, above
+    `max_bytes`, or that do not fit the cap are plain numpy allocations.
     """
 
-    def __init__(self, max_bytes=512 << 20, cap_bytes=2 << 30):
+    def __init__(self, max_bytes=4 << 30, cap_bytes=None):
+        if cap_bytes is None:
+            try:
+                phys = os.sysconf("SC_PHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+            except (ValueError, OSError, AttributeError):
+                phys = 16 << 30
+            cap_bytes = min(16 << 30, phys // 8)
         self.max_bytes = max_bytes
         self.cap_bytes = cap_bytes
         self._free = {}  # nbytes -> [address]
         self._outstanding = 0
+        self._pooled = 0
         self._lock = threading.Lock()
 
     def empty(self, shape, device=0):
@@ -175,9 +184,16 @@ class PinnedPool:
             return np.empty(shape)
         with self._lock:
             lst = self._free.get(nbytes)
-            addr = lst.pop() if lst else None
-            if addr is None:
-                if self._outstanding + nbytes > self.cap_bytes:
+            if lst:
+                addr = lst.pop()
+                self._pooled -= nbytes
+            else:
+                # make room by releasing pooled buffers of other sizes
+                for size in sorted(self._free, reverse=True):
+                    while self._free[size] and self._outstanding + self._pooled + nbytes > self.cap_bytes:
+                        load().ivhd_host_free(ctypes.c_void_p(self._free[size].pop()))
+                        self._pooled -= size
+                if self._outstanding + self._pooled + nbytes > self.cap_bytes:
                     return np.empty(shape)
                 out = ctypes.c_void_p()
                 if load().ivhd_host_alloc(int(device), nbytes, ctypes.byref(out)) != OK or not out.value:
@@ -191,6 +207,7 @@ class PinnedPool:
     def _release(self, addr, nbytes):
         with self._lock:
             self._outstanding -= nbytes
+            self._pooled += nbytes
             self._free.setdefault(nbytes, []).append(addr)
 
 

@@ -309,3 +309,27 @@ def test_result_arrays_in_recycled_pinned_buffers():
     assert {r2.embedding.points.ctypes.data, r2.state.positions.ctypes.data, r2.state.deltas.ctypes.data} == addrs
     np.testing.assert_array_equal(r2.embedding.points, keep)
     assert _lib.pinned._outstanding == 3 * 200_000 * 2 * 8
+
+
+def test_pinned_pool_cap_releases_pooled_buffers():
+    import gc
+
+    from paper_2303_05455_b200._lib import PinnedPool
+
+    mib = 1 << 20
+    p = PinnedPool(cap_bytes=5 * mib)
+    a = p.empty((mib // 16, 2))  # 1 MiB... (8 bytes x 2 x mib/16 = 1 MiB)
+    b = p.empty((mib // 8, 2))   # 2 MiB
+    assert p._outstanding == 3 * mib
+    c = p.empty((mib // 8, 2))   # 2 MiB more would reach 5 MiB: still fits
+    assert p._outstanding == 5 * mib
+    d = p.empty((mib // 16, 2))  # over the cap: plain numpy
+    assert p._outstanding == 5 * mib and d.shape == (mib // 16, 2)
+    del a, b
+    gc.collect()
+    assert p._outstanding == 2 * mib and p._pooled == 3 * mib
+    e = p.empty((3 * mib // 16, 2))  # 3 MiB: pooled 1 + 2 MiB buffers are released for it
+    assert p._outstanding == 5 * mib and p._pooled == 0
+    e[...] = 1.0
+    c[...] = 2.0
+    assert float(e.sum()) == e.size and float(c.sum()) == 2 * c.size
