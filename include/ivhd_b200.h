@@ -30,6 +30,8 @@
  *   ivhd_neighbor_hit               metrics.neighbor_hit (points)    metrics.py:254-294
  *   ivhd_curve_pass                 metrics._curve_pass (rnx/gnn/    metrics.py:149-182
  *                                   trust/continuity/evaluate)
+ *   ivhd_pair_ranks                 metrics._pair_ranks (shepard_    metrics.py:335-352
+ *                                   and_corank)
  *
  */
 #ifndef IVHD_B200_H
@@ -219,6 +221,12 @@ int ivhd_curve_pass(int device, const double* x, int64_t m, int32_t n, int32_t x
                     int32_t dim, const int32_t* labels, int32_t k_max, const int32_t* report_ks, int32_t n_report,
                     int64_t* agree_out, int64_t* same_ld_out, int64_t* same_hd_out, int64_t* trust_out,
                     int64_t* cont_out);
+/* Exact pair ranks (metrics._pair_ranks, metrics.py:335-352): ranks_out[p] =
+ * 1 + #{k != i : (d2(i,k), k) < (d2(i,j), j)} for i = i_idx[p], j = j_idx[p]
+ * (i != j), squared distances (|a|^2 + |b|^2) - 2 a.b clamped at 0 over the
+ * rows of z (m, n) float64.  Host buffers.  Errors: ivhd_metrics_last_error(). */
+int ivhd_pair_ranks(int device, const double* z, int64_t m, int32_t n, const int64_t* i_idx, const int64_t* j_idx,
+                    int64_t n_pairs, int64_t* ranks_out);
 const char* ivhd_metrics_last_error(void);
 
 #ifdef __cplusplus

@@ -294,9 +294,10 @@ __global__ void k_sqnorm(const double* __restrict__ x, int64_t m, int n, double*
   sq[i] = s;
 }
 
-// out[r][j] = max((sq[r0+r] + sq[j]) - 2 x_{r0+r}.x_j, 0) for r < nb, j < m
-__global__ void __launch_bounds__(256) k_dist_block(const double* __restrict__ x, const double* __restrict__ sq,
-                                                    int64_t m, int n, int64_t r0, int nb, double* __restrict__ out) {
+// out[r][j] = max((sqa[r] + sqb[j]) - 2 a_r.b_j, 0) for r < nb, j < m
+__global__ void __launch_bounds__(256) k_dist_block(const double* __restrict__ a, const double* __restrict__ sqa,
+                                                    const double* __restrict__ b, const double* __restrict__ sqb,
+                                                    int64_t m, int n, int nb, double* __restrict__ out) {
   __shared__ double As[DK][DT + 1], Bs[DK][DT + 1];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
   const int64_t rb = (int64_t)blockIdx.y * DT, cb = (int64_t)blockIdx.x * DT;
@@ -306,8 +307,8 @@ __global__ void __launch_bounds__(256) k_dist_block(const double* __restrict__ x
     for (int q = 0; q < 4; ++q) {
       const int e = t + 256 * q, row = e >> 4, kk = e & 15;
       const int64_t ra = rb + row, cbb = cb + row;
-      As[kk][row] = (ra < nb && k0 + kk < n) ? x[(r0 + ra) * n + k0 + kk] : 0.0;
-      Bs[kk][row] = (cbb < m && k0 + kk < n) ? x[cbb * n + k0 + kk] : 0.0;
+      As[kk][row] = (ra < nb && k0 + kk < n) ? a[ra * n + k0 + kk] : 0.0;
+      Bs[kk][row] = (cbb < m && k0 + kk < n) ? b[cbb * n + k0 + kk] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -329,11 +330,11 @@ __global__ void __launch_bounds__(256) k_dist_block(const double* __restrict__ x
   for (int u = 0; u < 4; ++u) {
     const int64_t r = rb + ty + 16 * u;
     if (r >= nb) continue;
-    const double si = sq[r0 + r];
+    const double si = sqa[r];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int64_t c = cb + tx + 16 * v;
-      if (c < m) out[r * m + c] = fmax((si + sq[c]) - 2.0 * acc[u][v], 0.0);
+      if (c < m) out[r * m + c] = fmax((si + sqb[c]) - 2.0 * acc[u][v], 0.0);
     }
   }
 }
@@ -710,6 +711,44 @@ __global__ void __launch_bounds__(NT) k_curve_rows(const double* __restrict__ hd
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Pair ranks (reference metrics.py:335-352 `_pair_ranks`, used by
+// shepard_and_corank 297-320): the exact rank of j among i's neighbours,
+//     1 + #{k != i : (d2(i,k), k) < (d2(i,j), j)},
+// for sampled pairs (i, j).  Rows of the distinct i are gathered, their
+// distance rows computed by k_dist_block, then one CTA per pair counts.
+__global__ void k_gather_rows(const double* __restrict__ z, const double* __restrict__ sq, int n,
+                              const int64_t* __restrict__ rows, int nb, double* __restrict__ a,
+                              double* __restrict__ sqa) {
+  const int r = blockIdx.x;
+  if (r >= nb) return;
+  const int64_t i = rows[r];
+  for (int c = threadIdx.x; c < n; c += blockDim.x) a[(int64_t)r * n + c] = z[i * n + c];
+  if (threadIdx.x == 0) sqa[r] = sq[i];
+}
+
+__global__ void __launch_bounds__(256) k_pair_count(const double* __restrict__ blk, int64_t m,
+                                                    const int* __restrict__ prow, const int64_t* __restrict__ pi,
+                                                    const int64_t* __restrict__ pj, int np,
+                                                    int64_t* __restrict__ ranks) {
+  __shared__ int s_cnt;
+  const int p = blockIdx.x;
+  if (p >= np) return;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const double* row = blk + (int64_t)prow[p] * m;
+  const int64_t i = pi[p];
+  const int j = (int)pj[p];
+  const double dj = row[j];
+  int c = 0;
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x)
+    if (k != i && lt(row[k], (int)k, dj, j)) ++c;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) ranks[p] = (int64_t)s_cnt + 1;
+}
 }  // namespace curves
 
 }  // namespace metrics
@@ -913,7 +952,7 @@ int ivhd_curve_pass(int device, const double* x, int64_t m, int32_t n, int32_t x
         MTRY(cudaMemcpyAsync(blk, x + r0 * m, sizeof(double) * nb * m, cudaMemcpyHostToDevice, st));
       } else {
         dim3 grid((unsigned)((m + DT - 1) / DT), (unsigned)((nb + DT - 1) / DT));
-        k_dist_block<<<grid, 256, 0, st>>>(dx, sqx, m, n, r0, nb, blk);
+        k_dist_block<<<grid, 256, 0, st>>>(dx + r0 * n, sqx + r0, dx, sqx, m, n, nb, blk);
       }
       const int ctas = std::min(nb, sms * 3);
       k_curve_rows<<<ctas, NT, sizeof(Shared), st>>>(blk, r0, nb, m, dy, sqy, dim, dl, k_max, K, rep, g,
@@ -942,6 +981,91 @@ int ivhd_curve_pass(int device, const double* x, int64_t m, int32_t n, int32_t x
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "curve_pass: %s", cudaGetErrorString(e));
+  return IVHD_OK;
+}
+
+
+int ivhd_pair_ranks(int device, const double* z, int64_t m, int32_t n, const int64_t* i_idx, const int64_t* j_idx,
+                    int64_t n_pairs, int64_t* ranks_out) {
+  using namespace curves;
+  if (!z || !i_idx || !j_idx || !ranks_out) return fail(IVHD_ERR_INVALID_ARG, "null pointer");
+  if (m < 2 || m >= 0x7fffffffLL || n < 1) return fail(IVHD_ERR_INVALID_ARG, "bad shape (m=%lld, n=%d)", (long long)m, n);
+  if (n_pairs < 0 || n_pairs >= 0x7fffffffLL) return fail(IVHD_ERR_INVALID_ARG, "bad pair count");
+  for (int64_t p = 0; p < n_pairs; ++p)
+    if (i_idx[p] < 0 || i_idx[p] >= m || j_idx[p] < 0 || j_idx[p] >= m || i_idx[p] == j_idx[p])
+      return fail(IVHD_ERR_INVALID_ARG, "pair %lld out of range or self", (long long)p);
+  if (n_pairs == 0) return IVHD_OK;
+  // pairs grouped by i (stable), distinct rows in ascending order
+  std::vector<int64_t> ord(n_pairs);
+  for (int64_t p = 0; p < n_pairs; ++p) ord[p] = p;
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return i_idx[a] < i_idx[b]; });
+  std::vector<int64_t> rows;
+  std::vector<int> row_of(n_pairs);
+  for (int64_t q = 0; q < n_pairs; ++q) {
+    const int64_t p = ord[q];
+    if (rows.empty() || rows.back() != i_idx[p]) rows.push_back(i_idx[p]);
+    row_of[q] = (int)rows.size() - 1;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail(IVHD_ERR_CUDA, "stream");
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>((int64_t)rows.size(), ((int64_t)1 << 27) / m));
+  double *dz = nullptr, *sq = nullptr, *a = nullptr, *sqa = nullptr, *blk = nullptr;
+  int64_t *drows = nullptr, *dpi = nullptr, *dpj = nullptr, *dr = nullptr;
+  int* dprow = nullptr;
+  cudaError_t e = cudaSuccess;
+  std::vector<int64_t> hpi(n_pairs), hpj(n_pairs), hr(n_pairs);
+  std::vector<int> hprow(n_pairs);
+  do {
+#define MTRY(call) \
+  if ((e = (call)) != cudaSuccess) break
+    MTRY(cudaMallocAsync(&dz, sizeof(double) * m * n, st));
+    MTRY(cudaMallocAsync(&sq, sizeof(double) * m, st));
+    MTRY(cudaMallocAsync(&a, sizeof(double) * nb_max * n, st));
+    MTRY(cudaMallocAsync(&sqa, sizeof(double) * nb_max, st));
+    MTRY(cudaMallocAsync(&blk, sizeof(double) * nb_max * m, st));
+    MTRY(cudaMallocAsync(&drows, sizeof(int64_t) * rows.size(), st));
+    MTRY(cudaMallocAsync(&dpi, sizeof(int64_t) * n_pairs, st));
+    MTRY(cudaMallocAsync(&dpj, sizeof(int64_t) * n_pairs, st));
+    MTRY(cudaMallocAsync(&dr, sizeof(int64_t) * n_pairs, st));
+    MTRY(cudaMallocAsync(&dprow, sizeof(int) * n_pairs, st));
+    MTRY(cudaMemcpyAsync(dz, z, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+    MTRY(cudaMemcpyAsync(drows, rows.data(), sizeof(int64_t) * rows.size(), cudaMemcpyHostToDevice, st));
+    k_sqnorm<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(dz, m, n, sq);
+    // pair arrays in grouped order; prow = row index within its distance block
+    for (int64_t q = 0; q < n_pairs; ++q) {
+      hpi[q] = i_idx[ord[q]];
+      hpj[q] = j_idx[ord[q]];
+      hprow[q] = (int)(row_of[q] % nb_max);
+    }
+    MTRY(cudaMemcpyAsync(dpi, hpi.data(), sizeof(int64_t) * n_pairs, cudaMemcpyHostToDevice, st));
+    MTRY(cudaMemcpyAsync(dpj, hpj.data(), sizeof(int64_t) * n_pairs, cudaMemcpyHostToDevice, st));
+    MTRY(cudaMemcpyAsync(dprow, hprow.data(), sizeof(int) * n_pairs, cudaMemcpyHostToDevice, st));
+    int64_t q0 = 0;
+    for (int64_t r0 = 0; r0 < (int64_t)rows.size(); r0 += nb_max) {
+      const int nb = (int)std::min<int64_t>(nb_max, (int64_t)rows.size() - r0);
+      k_gather_rows<<<nb, 128, 0, st>>>(dz, sq, n, drows + r0, nb, a, sqa);
+      dim3 grid((unsigned)((m + DT - 1) / DT), (unsigned)((nb + DT - 1) / DT));
+      k_dist_block<<<grid, 256, 0, st>>>(a, sqa, dz, sq, m, n, nb, blk);
+      int64_t q1 = q0;
+      while (q1 < n_pairs && row_of[q1] < r0 + nb) ++q1;
+      if (q1 > q0) k_pair_count<<<(unsigned)(q1 - q0), 256, 0, st>>>(blk, m, dprow + q0, dpi + q0, dpj + q0,
+                                                                   (int)(q1 - q0), dr + q0);
+      MTRY(cudaGetLastError());
+      q0 = q1;
+    }
+    if (e != cudaSuccess) break;
+    MTRY(cudaMemcpyAsync(hr.data(), dr, sizeof(int64_t) * n_pairs, cudaMemcpyDeviceToHost, st));
+    MTRY(cudaStreamSynchronize(st));
+    for (int64_t q = 0; q < n_pairs; ++q) ranks_out[ord[q]] = hr[q];
+#undef MTRY
+  } while (0);
+  for (void* p : {(void*)dz, (void*)sq, (void*)a, (void*)sqa, (void*)blk, (void*)drows, (void*)dpi, (void*)dpj,
+                  (void*)dr, (void*)dprow})
+    if (p) cudaFreeAsync(p, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "pair_ranks: %s", cudaGetErrorString(e));
   return IVHD_OK;
 }
 

@@ -243,3 +243,57 @@ def evaluate_embedding(X, Y, labels=None, k_max=None, nn_max=100, report_ks=(15,
         curves.trust[kk] = 1.0 - scale * trust_pen[kk]
         curves.continuity[kk] = 1.0 - scale * cont_pen[kk]
     return curves
+
+
+# ------------------------------------------------------ Shepard / co-ranks
+
+
+def _unrank_pairs(flat, m):
+    """Linear upper-triangle index -> (i, j), i < j (reference metrics.py:323-332)."""
+    i = (m - 2 - np.floor(np.sqrt(-8.0 * flat + 4.0 * m * (m - 1) - 7) / 2.0 - 0.5)).astype(np.int64)
+    j = (flat + i + 1 - (m * (m - 1)) // 2 + ((m - i) * (m - i - 1)) // 2).astype(np.int64)
+    return i, j
+
+
+def _pair_ranks(Z, i_idx, j_idx, device=0):
+    """Exact rank of each j among i's neighbours on the GPU (ivhd_pair_ranks;
+    reference metrics.py:335-352)."""
+    z = np.ascontiguousarray(Z, dtype=np.float64)
+    ii = np.ascontiguousarray(i_idx, dtype=np.int64)
+    jj = np.ascontiguousarray(j_idx, dtype=np.int64)
+    out = np.empty(len(ii), dtype=np.int64)
+    lib = _lib.load()
+    c_i64 = _lib.ctypes.c_int64
+    rc = lib.ivhd_pair_ranks(int(device), _lib.ptr(z, _lib.ctypes.c_double), z.shape[0], int(z.shape[1]),
+                             _lib.ptr(ii, c_i64), _lib.ptr(jj, c_i64), len(ii), _lib.ptr(out, c_i64))
+    if rc != _lib.OK:
+        msg = (lib.ivhd_metrics_last_error() or b"").decode(errors="replace")
+        if rc == _lib.ERR_INVALID_ARG:
+            raise InvalidArgumentError(msg)
+        raise DeviceError(f"pair ranks failed: {msg}")
+    return out
+
+
+def shepard_and_corank(X, Y, sample_pairs=10000, seed=0, device=0):
+    """Drop-in for metrics.shepard_and_corank (metrics.py:297-320): sampled
+    distance pairs, their exact ranks in X and Y (GPU), and R^2 of the
+    co-ranks against the identity.  Pair sampling is the reference's."""
+    X, Y = _as_matrix(X), _as_matrix(Y)
+    m = X.shape[0]
+    if Y.shape[0] != m:
+        raise DimensionMismatchError("X and Y row counts differ")
+    total = m * (m - 1) // 2
+    if sample_pairs > total:
+        raise InvalidArgumentError(f"at most {total} distinct pairs exist")
+    rng = np.random.default_rng(seed)
+    flat = rng.choice(total, size=sample_pairs, replace=False)
+    i_idx, j_idx = _unrank_pairs(flat, m)
+    deltas = np.linalg.norm(X[i_idx] - X[j_idx], axis=1)
+    dists = np.linalg.norm(Y[i_idx] - Y[j_idx], axis=1)
+    rho = _pair_ranks(X, i_idx, j_idx, device=device)
+    r = _pair_ranks(Y, i_idx, j_idx, device=device)
+    resid = r.astype(np.float64) - rho.astype(np.float64)
+    centered = r - r.mean()
+    ss_tot = float(np.sum(centered * centered))
+    r2 = 1.0 - float(np.sum(resid * resid)) / ss_tot if ss_tot > 0 else 1.0
+    return (deltas, dists), (rho, r), r2

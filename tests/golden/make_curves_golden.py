@@ -78,6 +78,12 @@ def main():
             arrays[f"{name}/rnx_auc_direct"] = np.float64(auc)
             t, c = metrics.trust_continuity(X, Y, ks[0])
             arrays[f"{name}/tc_direct"] = np.array([t, c])
+        if not pre:
+            (dl, ds), (rho, rr), r2 = metrics.shepard_and_corank(X, Y, sample_pairs=min(3000, len(Y) * 4), seed=3)
+            arrays[f"{name}/shepard_rho"] = rho
+            arrays[f"{name}/shepard_r"] = rr
+            arrays[f"{name}/shepard_r2"] = np.float64(r2)
+            arrays[f"{name}/shepard_deltas"] = dl
         print(name, X.shape, cur.summary())
     np.savez_compressed(OUT, **arrays)
 

@@ -173,3 +173,47 @@ def test_curve_counts_tie_crowded_rows_equal_oracle():
     for g, w in zip(got[:3], want[:3]):
         np.testing.assert_array_equal(g, w)
     assert got[3] == want[3] and got[4] == want[4]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [n for n in sorted(curve_inputs()) if not curve_inputs()[n][5]])
+def test_shepard_and_corank_matches_reference(name):
+    """GPU pair ranks (ivhd_pair_ranks) against the reference's
+    shepard_and_corank on the same sampled pairs: exact on integer inputs,
+    at most 1% of ranks differing (near-ties under another fp64 summation
+    order) otherwise."""
+    from paper_2303_05455_b200 import metrics
+
+    X, Y, _, _, _, _ = curve_inputs()[name]
+    gold = np.load(CURVES_GOLD)
+    (dl, _), (rho, r), r2 = metrics.shepard_and_corank(X, Y, sample_pairs=min(3000, len(Y) * 4), seed=3)
+    np.testing.assert_array_equal(dl, gold[f"{name}/shepard_deltas"])
+    if "lattice" in name:
+        np.testing.assert_array_equal(rho, gold[f"{name}/shepard_rho"])
+        np.testing.assert_array_equal(r, gold[f"{name}/shepard_r"])
+        assert r2 == float(gold[f"{name}/shepard_r2"])
+    else:
+        assert np.mean(rho != gold[f"{name}/shepard_rho"]) <= 0.01
+        assert np.mean(r != gold[f"{name}/shepard_r"]) <= 0.01
+        assert r2 == pytest.approx(float(gold[f"{name}/shepard_r2"]), abs=1e-3)
+
+
+@pytest.mark.gpu
+def test_pair_ranks_equal_bruteforce_at_scale():
+    """70k x 50 points, 5000 pairs (several distance blocks): ranks equal a
+    numpy count over the same formula for a subset of pairs."""
+    from paper_2303_05455_b200 import metrics
+
+    rng = np.random.default_rng(4)
+    m = 70000
+    Z = rng.integers(-3, 4, (m, 5)).astype(np.float64)  # integer: exact distances, many ties
+    (_, _), (rho, _), _ = metrics.shepard_and_corank(Z, Z[:, :2], sample_pairs=5000, seed=1)
+    flat = np.random.default_rng(1).choice(m * (m - 1) // 2, size=5000, replace=False)
+    i_idx, j_idx = metrics._unrank_pairs(flat, m)
+    sq = (Z * Z).sum(1)
+    for p in range(0, 5000, 250):
+        i, j = i_idx[p], j_idx[p]
+        row = np.maximum(sq[i] + sq - 2.0 * (Z @ Z[i]), 0.0)
+        row[i] = np.inf
+        want = 1 + np.count_nonzero(row < row[j]) + np.count_nonzero((row == row[j]) & (np.arange(m) < j))
+        assert rho[p] == want
