@@ -30,6 +30,7 @@
  *   ivhd_neighbor_hit               metrics.neighbor_hit (points)    metrics.py:254-294
  *   ivhd_curve_pass                 metrics._curve_pass (rnx/gnn/    metrics.py:149-182
  *                                   trust/continuity/evaluate)
+ *   ivhd_rank_matrix                metrics.compute_ranks            metrics.py:103-146
  *   ivhd_pair_ranks                 metrics._pair_ranks (shepard_    metrics.py:335-352
  *                                   and_corank)
  *
@@ -227,6 +228,12 @@ int ivhd_curve_pass(int device, const double* x, int64_t m, int32_t n, int32_t x
  * rows of z (m, n) float64.  Host buffers.  Errors: ivhd_metrics_last_error(). */
 int ivhd_pair_ranks(int device, const double* z, int64_t m, int32_t n, const int64_t* i_idx, const int64_t* j_idx,
                     int64_t n_pairs, int64_t* ranks_out);
+/* Full rank matrix (metrics.compute_ranks, metrics.py:103-146): ranks_out
+ * (m, m) int64 host buffer, row i = rank 1..m-1 of every other point by
+ * (distance, index), 0 on the diagonal.  x (m, n) float64 points (squared
+ * distances (|a|^2 + |b|^2) - 2 a.b clamped at 0) or, with precomputed, an
+ * (m, m) distance matrix (n == m).  Errors: ivhd_metrics_last_error(). */
+int ivhd_rank_matrix(int device, const double* x, int64_t m, int32_t n, int32_t precomputed, int64_t* ranks_out);
 const char* ivhd_metrics_last_error(void);
 
 #ifdef __cplusplus

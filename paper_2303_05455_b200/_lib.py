@@ -88,6 +88,8 @@ SIGNATURES = {
                                          ctypes.c_int32, c_f64p, c_i32p]),
     "ivhd_host_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
     "ivhd_host_free": (ctypes.c_int, [ctypes.c_void_p]),
+    "ivhd_rank_matrix": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                        c_i64p]),
     "ivhd_pair_ranks": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, c_i64p, c_i64p,
                                        ctypes.c_int64, c_i64p]),
     "ivhd_curve_pass": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,

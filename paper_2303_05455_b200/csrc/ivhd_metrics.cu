@@ -749,6 +749,40 @@ __global__ void __launch_bounds__(256) k_pair_count(const double* __restrict__ b
   __syncthreads();
   if (threadIdx.x == 0) ranks[p] = (int64_t)s_cnt + 1;
 }
+
+// ---------------------------------------------------------------------------
+// Full rank matrix (reference metrics.py:103-146 `_rank_block` /
+// `compute_ranks`): per row, a stable sort of (distance, index) with the
+// diagonal at +inf, ranks 1..M-1, self 0.  Keys: order-preserving uint64 of
+// the fp64 distance (-0 folded to +0, so equal values tie and the stable
+// radix sort keeps index order).
+__global__ void k_rank_keys(const double* __restrict__ blk, int64_t m, int64_t r0, int nb,
+                            unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+  const int64_t n = (int64_t)nb * m;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / m, c = t - r * m;
+    const double d = (c == r0 + r) ? INFINITY : blk[t] + 0.0;
+    unsigned long long k = (unsigned long long)__double_as_longlong(d);
+    k = (k >> 63) ? ~k : (k | 0x8000000000000000ull);
+    keys[t] = k;
+    vals[t] = (int)c;
+  }
+}
+
+__global__ void k_rank_scatter(const int* __restrict__ order, int64_t m, int64_t r0, int nb,
+                               int64_t* __restrict__ ranks) {
+  const int64_t n = (int64_t)nb * m;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / m, p = t - r * m;
+    const int c = order[t];
+    ranks[r * m + c] = (c == r0 + r) ? 0 : p + 1;
+  }
+}
+
+__global__ void k_seg_offsets(int* __restrict__ off, int nb, int64_t m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= nb) off[i] = (int)(i * m);
+}
 }  // namespace curves
 
 }  // namespace metrics
@@ -1066,6 +1100,77 @@ int ivhd_pair_ranks(int device, const double* z, int64_t m, int32_t n, const int
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "pair_ranks: %s", cudaGetErrorString(e));
+  return IVHD_OK;
+}
+
+
+int ivhd_rank_matrix(int device, const double* x, int64_t m, int32_t n, int32_t precomputed, int64_t* ranks_out) {
+  using namespace curves;
+  if (!x || !ranks_out) return fail(IVHD_ERR_INVALID_ARG, "null pointer");
+  if (m < 2) return fail(IVHD_ERR_INVALID_ARG, "need at least two points to rank");
+  if (m >= (1LL << 31) / 2 || (precomputed ? n != m : n < 1))
+    return fail(IVHD_ERR_INVALID_ARG, "bad shape (m=%lld, n=%d)", (long long)m, n);
+  if (cudaSetDevice(device) != cudaSuccess) return fail(IVHD_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail(IVHD_ERR_CUDA, "stream");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  // per block entry: distance 8 + keys 2x8 + vals 2x4 + ranks 8 = 40 bytes; <= 1 GiB, < 2^31 entries
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(m, std::min<int64_t>(((int64_t)1 << 30) / (40 * m),
+                                                                                      ((int64_t)1 << 31) / m - 1)));
+  double *dx = nullptr, *sq = nullptr, *blk = nullptr;
+  unsigned long long *k1 = nullptr, *k2 = nullptr;
+  int *v1 = nullptr, *v2 = nullptr, *off = nullptr;
+  int64_t* rk = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cudaError_t e = cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>((nb_max * m + 255) / 256, (int64_t)sms * 32);
+  do {
+#define MTRY(call) \
+  if ((e = (call)) != cudaSuccess) break
+    MTRY(cudaMallocAsync(&blk, sizeof(double) * nb_max * m, st));
+    MTRY(cudaMallocAsync(&k1, 8 * nb_max * m, st));
+    MTRY(cudaMallocAsync(&k2, 8 * nb_max * m, st));
+    MTRY(cudaMallocAsync(&v1, 4 * nb_max * m, st));
+    MTRY(cudaMallocAsync(&v2, 4 * nb_max * m, st));
+    MTRY(cudaMallocAsync(&rk, 8 * nb_max * m, st));
+    MTRY(cudaMallocAsync(&off, 4 * (nb_max + 1), st));
+    if (!precomputed) {
+      MTRY(cudaMallocAsync(&dx, sizeof(double) * m * n, st));
+      MTRY(cudaMallocAsync(&sq, sizeof(double) * m, st));
+      MTRY(cudaMemcpyAsync(dx, x, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+      k_sqnorm<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(dx, m, n, sq);
+    }
+    MTRY(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tb, k1, k2, v1, v2, (int)(nb_max * m), (int)nb_max, off,
+                                                  off + 1, 0, 64, st));
+    MTRY(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), st));
+    for (int64_t r0 = 0; r0 < m; r0 += nb_max) {
+      const int nb = (int)std::min<int64_t>(nb_max, m - r0);
+      if (precomputed) {
+        MTRY(cudaMemcpyAsync(blk, x + r0 * m, sizeof(double) * nb * m, cudaMemcpyHostToDevice, st));
+      } else {
+        dim3 grid((unsigned)((m + DT - 1) / DT), (unsigned)((nb + DT - 1) / DT));
+        k_dist_block<<<grid, 256, 0, st>>>(dx + r0 * n, sq + r0, dx, sq, m, n, nb, blk);
+      }
+      k_rank_keys<<<g, 256, 0, st>>>(blk, m, r0, nb, k1, v1);
+      k_seg_offsets<<<(nb + 256) / 256, 256, 0, st>>>(off, nb, m);
+      size_t tb2 = tb;
+      MTRY(cub::DeviceSegmentedRadixSort::SortPairs(tmp, tb2, k1, k2, v1, v2, (int)(nb * m), nb, off, off + 1, 0, 64,
+                                                    st));
+      k_rank_scatter<<<g, 256, 0, st>>>(v2, m, r0, nb, rk);
+      MTRY(cudaGetLastError());
+      MTRY(cudaMemcpyAsync(ranks_out + r0 * m, rk, 8 * nb * m, cudaMemcpyDeviceToHost, st));
+    }
+    if (e != cudaSuccess) break;
+    MTRY(cudaStreamSynchronize(st));
+#undef MTRY
+  } while (0);
+  for (void* p : {(void*)dx, (void*)sq, (void*)blk, (void*)k1, (void*)k2, (void*)v1, (void*)v2, (void*)off, (void*)rk, tmp})
+    if (p) cudaFreeAsync(p, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) return fail(IVHD_ERR_CUDA, "rank_matrix: %s", cudaGetErrorString(e));
   return IVHD_OK;
 }
 

@@ -297,3 +297,50 @@ def shepard_and_corank(X, Y, sample_pairs=10000, seed=0, device=0):
     ss_tot = float(np.sum(centered * centered))
     r2 = 1.0 - float(np.sum(resid * resid)) / ss_tot if ss_tot > 0 else 1.0
     return (deltas, dists), (rho, r), r2
+
+
+# ----------------------------------------------------------- rank matrices
+
+
+@dataclass
+class RankData:
+    """Full rank matrices for a (X, Y) pair; rank[i, i] is 0 (metrics.py:18-23)."""
+
+    hd_ranks: np.ndarray
+    ld_ranks: np.ndarray | None = None
+
+
+def _rank_matrix(source, precomputed, device=0):
+    src = np.ascontiguousarray(source, dtype=np.float64)
+    m = src.shape[0]
+    out = np.empty((m, m), dtype=np.int64)
+    lib = _lib.load()
+    rc = lib.ivhd_rank_matrix(int(device), _lib.ptr(src, _lib.ctypes.c_double), m, int(src.shape[1]),
+                              int(bool(precomputed)), _lib.ptr(out, _lib.ctypes.c_int64))
+    if rc != _lib.OK:
+        msg = (lib.ivhd_metrics_last_error() or b"").decode(errors="replace")
+        if rc == _lib.ERR_INVALID_ARG:
+            raise InvalidArgumentError(msg)
+        raise DeviceError(f"rank matrix failed: {msg}")
+    return out
+
+
+def compute_ranks(distances=None, dataset=None, ld_distances=None, device=0):
+    """Drop-in for metrics.compute_ranks (metrics.py:116-146): exact rank
+    matrices under the index tie rule, computed on the GPU (ivhd_rank_matrix)."""
+    if (distances is None) == (dataset is None):
+        raise InvalidArgumentError("pass exactly one of distances / dataset")
+    if distances is not None:
+        D = _as_matrix(distances)
+        if D.shape[0] != D.shape[1]:
+            raise DimensionMismatchError("distance matrix must be square")
+        source, pre = D, True
+    else:
+        source, pre = _as_matrix(dataset), False
+    if source.shape[0] < 2:
+        raise InvalidArgumentError("need at least two points to rank")
+    hd = _rank_matrix(source, pre, device=device)
+    ld = None
+    if ld_distances is not None:
+        ld = compute_ranks(distances=ld_distances, device=device).hd_ranks
+    return RankData(hd_ranks=hd, ld_ranks=ld)

@@ -217,3 +217,55 @@ def test_pair_ranks_equal_bruteforce_at_scale():
         row[i] = np.inf
         want = 1 + np.count_nonzero(row < row[j]) + np.count_nonzero((row == row[j]) & (np.arange(m) < j))
         assert rho[p] == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["lattice_400_ties", "precomp_300", "tiny_40", "mix20_600"])
+def test_compute_ranks_equal_oracle(name):
+    """GPU rank matrix vs the oracle restatement of metrics.py:103-113 (exact on
+    integer / given distances; near-ties may swap neighbours otherwise)."""
+    import oracle as O
+    from paper_2303_05455_b200 import metrics
+
+    X, Y, _, _, _, pre = curve_inputs()[name]
+    if pre:
+        rd = metrics.compute_ranks(distances=X, ld_distances=X[::-1, ::-1])
+        want_hd = O.ivhd_oracle._ranks(X)[0]
+        want_ld = O.ivhd_oracle._ranks(np.ascontiguousarray(X[::-1, ::-1]))[0]
+        np.testing.assert_array_equal(rd.ld_ranks, want_ld)
+    else:
+        rd = metrics.compute_ranks(dataset=X)
+        want_hd = O.ivhd_oracle._ranks(O.ivhd_oracle._sq_dist_matrix(X))[0]
+        assert rd.ld_ranks is None
+    if "mix" in name:
+        assert np.mean(rd.hd_ranks != want_hd) < 1e-3
+    else:
+        np.testing.assert_array_equal(rd.hd_ranks, want_hd)
+    m = len(X)
+    assert (np.diag(rd.hd_ranks) == 0).all()
+    np.testing.assert_array_equal(np.sort(rd.hd_ranks, axis=1), np.broadcast_to(np.arange(m), (m, m)))
+
+
+@pytest.mark.gpu
+def test_compute_ranks_blocks_and_errors():
+    """9000 points: several row blocks; rows are permutations of 0..M-1."""
+    from paper_2303_05455_b200 import metrics
+    from paper_2303_05455_b200.errors import DimensionMismatchError, InvalidArgumentError
+
+    X = np.random.default_rng(2).integers(0, 5, (9000, 3)).astype(np.float64)
+    r = metrics.compute_ranks(dataset=X).hd_ranks
+    assert (np.diag(r) == 0).all()
+    for i in (0, 4321, 8999):
+        row = np.maximum((X * X).sum(1)[i] + (X * X).sum(1) - 2.0 * (X @ X[i]), 0.0)
+        row[i] = np.inf
+        order = np.lexsort((np.arange(9000), row))
+        want = np.empty(9000, dtype=np.int64)
+        want[order] = np.arange(1, 9001)
+        want[i] = 0
+        np.testing.assert_array_equal(r[i], want)
+    with pytest.raises(InvalidArgumentError):
+        metrics.compute_ranks()
+    with pytest.raises(DimensionMismatchError):
+        metrics.compute_ranks(distances=np.zeros((3, 4)))
+    with pytest.raises(InvalidArgumentError):
+        metrics.compute_ranks(dataset=np.zeros((1, 2)))
