@@ -203,7 +203,7 @@ const char* ivhd_knn_last_error(void);
  * computed on `device`: y (m, dim) float64 host points (1 <= dim <= 3), labels
  * (m) int32; cf_nn_out[j] (nn_max doubles) = fraction of same-label points
  * among the j+1 nearest other points, averaged over all points.  Exact grid
- * kNN, (distance, index) order.  1 <= nn_max < m, nn_max <= 128.  nbr_out:
+ * kNN, (distance, index) order.  1 <= nn_max < m, nn_max <= 512.  nbr_out:
  * optional (m, nn_max) int32 neighbour ids.  Errors: ivhd_metrics_last_error(). */
 int ivhd_neighbor_hit(int device, const double* y, int64_t m, int32_t dim, const int32_t* labels,
                       int32_t nn_max, double* cf_nn_out, int32_t* nbr_out);

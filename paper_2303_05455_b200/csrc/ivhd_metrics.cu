@@ -29,8 +29,7 @@
 
 namespace metrics {
 
-constexpr int NH_MAX = 128;              // neighbourhood sizes supported (4 slots per lane)
-constexpr int SPL = NH_MAX / 32;
+constexpr int NH_MAX = 512;              // neighbourhood sizes supported (<= 16 slots per lane)
 constexpr int QWARPS = 8;                // query warps per block
 
 thread_local std::string g_err;
@@ -113,15 +112,17 @@ __global__ void k_gather_points(const double* __restrict__ y, const int32_t* __r
 
 __device__ __forceinline__ bool lt(double da, int ia, double db, int ib) { return da < db || (da == db && ia < ib); }
 
-// One warp per query (queries visited in cell order for cache locality).
+// One warp per query (queries visited in cell order for cache locality);
+// SPL slots per lane hold up to 32 * SPL neighbours.
+template <int SPL>
 __global__ void __launch_bounds__(QWARPS * 32) k_grid_knn(const double* __restrict__ ys, const int32_t* __restrict__ sid,
                                                          const uint32_t* __restrict__ start, int64_t m, Grid G, int kk,
                                                          const int32_t* __restrict__ labels,
                                                          unsigned long long* __restrict__ hits,
                                                          int32_t* __restrict__ nbr_out) {
-  __shared__ unsigned int sh_hits[NH_MAX];
+  __shared__ unsigned int sh_hits[32 * SPL];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < NH_MAX; i += blockDim.x) sh_hits[i] = 0;
+  for (int i = threadIdx.x; i < 32 * SPL; i += blockDim.x) sh_hits[i] = 0;
   __syncthreads();
   const int64_t nw = (int64_t)gridDim.x * QWARPS;
   for (int64_t qs = blockIdx.x * (int64_t)QWARPS + warp; qs < m; qs += nw) {
@@ -894,7 +895,9 @@ int ivhd_neighbor_hit(int device, const double* y, int64_t m, int32_t dim, const
     k_gather_points<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(dy, sid, m, dim, ys);
     if (nbr_out) MTRY(cudaMallocAsync(&dn, sizeof(int32_t) * m * nn_max, st));
     const int blocks = (int)std::min<int64_t>((m + QWARPS - 1) / QWARPS, (int64_t)sms * 16);
-    k_grid_knn<<<blocks, QWARPS * 32, 0, st>>>(ys, sid, start, m, G, nn_max, dl, hits, dn);
+    if (nn_max <= 128) k_grid_knn<4><<<blocks, QWARPS * 32, 0, st>>>(ys, sid, start, m, G, nn_max, dl, hits, dn);
+    else if (nn_max <= 256) k_grid_knn<8><<<blocks, QWARPS * 32, 0, st>>>(ys, sid, start, m, G, nn_max, dl, hits, dn);
+    else k_grid_knn<16><<<blocks, QWARPS * 32, 0, st>>>(ys, sid, start, m, G, nn_max, dl, hits, dn);
     MTRY(cudaGetLastError());
     std::vector<unsigned long long> hh(NH_MAX);
     MTRY(cudaMemcpyAsync(hh.data(), hits, sizeof(unsigned long long) * NH_MAX, cudaMemcpyDeviceToHost, st));

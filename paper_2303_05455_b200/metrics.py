@@ -112,10 +112,22 @@ def default_k_max(m):
     return min(m - 2, 1000)
 
 
+_MAX_REPORT = 8  # report ks per device pass (ivhd_curve_pass)
+
+
 def _curve_pass(X, Y, labels, k_max, report_ks, x_precomputed=False, device=0):
     """GPU restatement of metrics.py:149-182: (agree[0..k_max], same_ld, same_hd,
     trust_pen, cont_pen).  agree is truncated at k_max, which is all the curves
-    read (cumsum(agree)[1:k_max+1])."""
+    read (cumsum(agree)[1:k_max+1]).  More than 8 report ks take extra passes
+    (trust/continuity only)."""
+    report_ks = [int(k) for k in report_ks]
+    if len(report_ks) > _MAX_REPORT:
+        out = _curve_pass(X, Y, labels, k_max, report_ks[:_MAX_REPORT], x_precomputed, device)
+        for a in range(_MAX_REPORT, len(report_ks), _MAX_REPORT):
+            _, _, _, t, c = _curve_pass(X, Y, None, 1, report_ks[a:a + _MAX_REPORT], x_precomputed, device)
+            out[3].update(t)
+            out[4].update(c)
+        return out
     m = X.shape[0]
     if Y.shape[0] != m:
         raise DimensionMismatchError("X and Y row counts differ")

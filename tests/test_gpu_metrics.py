@@ -269,3 +269,37 @@ def test_compute_ranks_blocks_and_errors():
         metrics.compute_ranks(distances=np.zeros((3, 4)))
     with pytest.raises(InvalidArgumentError):
         metrics.compute_ranks(dataset=np.zeros((1, 2)))
+
+
+@pytest.mark.gpu
+def test_many_report_ks_take_extra_passes():
+    """More report ks than one device pass holds (8): same values as one k at a time."""
+    from paper_2303_05455_b200 import metrics
+
+    X, Y, lab, _, _, _ = curve_inputs()["mix20_600"]
+    ks = tuple(range(5, 290, 25))  # 12 ks
+    cur = metrics.evaluate_embedding(X, Y, labels=lab, k_max=50, nn_max=10, report_ks=ks)
+    assert sorted(cur.trust) == list(ks)
+    for k in (5, 205, 280):
+        t, c = metrics.trust_continuity(X, Y, k)
+        assert cur.trust[k] == t and cur.continuity[k] == c
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [129, 300, 512])
+def test_neighbor_hit_large_nn_max_equals_kdtree(k):
+    """nn_max above 128 (8 / 16 slots per lane): neighbour ids equal scipy's
+    cKDTree on continuous 2-D points, and the hit curve follows from them."""
+    from scipy.spatial import cKDTree
+
+    from paper_2303_05455_b200 import metrics
+
+    rng = np.random.default_rng(k)
+    y = rng.standard_normal((6000, 2))
+    lab = (y[:, 0] > 0).astype(np.int64) + 2 * (y[:, 1] > 0.3)
+    cf_nn, cf, nbr = metrics.neighbor_hit(y, lab, nn_max=k, return_neighbors=True)
+    _, idx = cKDTree(y).query(y, k=k + 1)
+    np.testing.assert_array_equal(nbr, idx[:, 1:])
+    same = lab[idx[:, 1:]] == lab[:, None]
+    want = same.cumsum(axis=1).sum(axis=0) / (np.arange(1, k + 1) * len(y))
+    np.testing.assert_allclose(cf_nn, want, rtol=0, atol=1e-15)
