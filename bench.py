@@ -477,9 +477,10 @@ def gpu_arm(args, w):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: 10-cluster Gaussian mixture, exact kNN graph from the package's GPU "
-                    "builder (untimed here; timed separately under 'knn')",
-            "config": {"workload": f"{args.workload}: " + (f"YAHOO-shaped M={m} N={w['n']} kNN graph, "
+            "data": ("synthetic: 10-cluster Gaussian mixture, exact kNN graph from the package's GPU "
+                     "builder (untimed here; timed separately under 'knn')") if w["graph"] == "mixture" else
+                    "synthetic: planted-cluster kNN-shaped graph (synth.planted_graph, untimed)",
+            "config": {"workload": f"{args.workload}: " + (f"{'YAHOO' if w['n'] == 100 else 'MNIST'}-shaped M={m} N={w['n']} kNN graph, "
                                    if w["graph"] == "mixture" else f"planted-cluster graph M={m}, ") +
                                    f"nn={w['nn']} rn={w['rn']} c={w['c']} {w['optimizer']}, "
                                    f"{iters} iterations per step",
