@@ -81,6 +81,7 @@ struct ivhd_ctx {
   int32_t* perm = nullptr;
   int32_t* inv = nullptr;
   bool perm_fixed = false;
+  bool window_order = false;  // locality-ordered input: degree sort inside id windows, in-order schedule
 
   float* ybuf[2] = {nullptr, nullptr};  // 8 floats/vertex capacity
   float* state = nullptr;               // 8 floats/vertex capacity
@@ -369,6 +370,19 @@ __global__ void k_window_keys(const uint32_t* __restrict__ row_ptr, int64_t m, i
     key[i] = ((uint64_t)(nwin - 1 - i / W) << 32) | (uint64_t)(row_ptr[i + 1] - row_ptr[i]);
 }
 
+// Locality statistic of the caller's ids: connections whose endpoints lie
+// within kOrderWindow ids of each other (integer count, order independent).
+__global__ void k_local_edges(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t L,
+                              int64_t W, unsigned long long* __restrict__ count) {
+  unsigned long long c = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = (int64_t)src[e] - (int64_t)dst[e];
+    c += (d < W && d > -W) ? 1ull : 0ull;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
 __global__ void k_inverse(const int32_t* __restrict__ perm, int64_t m, int32_t* __restrict__ inv) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -494,7 +508,17 @@ int pull_ctrl(ivhd_ctx* ctx);
 // Fix the vertex order from the degrees of the first CSR built: stable sort
 // by descending degree (hubs first, so the dynamic tile scheduler starts the
 // longest tiles early).  Positions/state already uploaded are re-ordered.
-int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
+//
+// Locality-ordered inputs (at least half of the connections join ids less
+// than kOrderWindow apart, e.g. the planted graphs of C4/C5) instead sort by
+// degree inside windows of kOrderWindow ids and run the tiles in order, so a
+// tile's nn partners stay in the same few L2 lines: 10^8 planted 6217 ->
+// 5481 us per iteration, 10^7 271 -> 265 (profiles/r01_kernel_experiments.md).
+// Inputs without id locality (real kNN graphs) keep the global degree sort:
+// windows cost them 2.6x in load imbalance.
+constexpr int64_t kOrderWindow = 2048;
+
+int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old, const int32_t* src, const int32_t* dst, int64_t L) {
   const int64_t m = ctx->m;
   const char* order = getenv("IVHD_ORDER");  // experiments: "identity" keeps the caller's order
   if (order && strcmp(order, "identity") == 0) {
@@ -502,6 +526,24 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
     return IVHD_OK;
   }
   cudaStream_t st = ctx->stream;
+  int64_t window = 0;
+  if (const char* w = getenv("IVHD_ORDER_WINDOW")) {  // experiments: force a window (0 = global sort)
+    window = std::max<int64_t>(0, atoll(w));
+  } else if (L > 0 && m > 2 * kOrderWindow) {
+    unsigned long long* dcount = nullptr;
+    unsigned long long hcount = 0;
+    cudaError_t e0 = dalloc(ctx, &dcount, sizeof(unsigned long long));
+    if (e0 == cudaSuccess) e0 = cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), st);
+    if (e0 == cudaSuccess) {
+      k_local_edges<<<grid_for(L, ctx->sm_count), 256, 0, st>>>(src, dst, L, kOrderWindow, dcount);
+      e0 = cudaMemcpyAsync(&hcount, dcount, sizeof(hcount), cudaMemcpyDeviceToHost, st);
+    }
+    if (e0 == cudaSuccess) e0 = cudaStreamSynchronize(st);
+    dfree(ctx, dcount);
+    if (e0 != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "locality statistic: %s", cudaGetErrorString(e0));
+    if (2 * (int64_t)hcount >= L) window = kOrderWindow;
+  }
+  ctx->window_order = window > 0 && window < m;
   uint32_t *deg = nullptr, *deg2 = nullptr;
   int32_t *ids = nullptr, *perm = nullptr;
   void* tmp = nullptr;
@@ -514,11 +556,7 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old) {
     if ((e = dalloc(ctx, &ids, 4 * m)) != cudaSuccess) break;
     if ((e = dalloc(ctx, &perm, 4 * m)) != cudaSuccess) break;
     k_iota<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ids, m);
-    static const int64_t window = [] {
-      const char* w = getenv("IVHD_ORDER_WINDOW");  // experiments: degree sort inside id windows
-      return w ? std::max<int64_t>(0, atoll(w)) : (int64_t)0;
-    }();
-    if (window > 0 && window < m) {
+    if (ctx->window_order) {
       uint64_t *k1 = nullptr, *k2 = nullptr;
       int eb = 33;
       while (eb < 64 && ((int64_t)1 << (eb - 32)) < (m + window - 1) / window) ++eb;
@@ -618,7 +656,7 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
     if ((e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
     if (hbad) break;
-    if (!ctx->perm_fixed && (rc = fix_permutation(ctx, rp_old)) != IVHD_OK) break;
+    if (!ctx->perm_fixed && (rc = fix_permutation(ctx, rp_old, src, dst, L)) != IVHD_OK) break;
     // relabelled row pointers: exclusive scan of the permuted degrees
     k_degrees<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(rp_old, m, keys);
     k_gather_u32<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(keys, ctx->perm, m, deg);
@@ -1471,7 +1509,7 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
     const char* e = getenv("IVHD_LPT");
     return !(e && strcmp(e, "0") == 0);
   }();
-  if (lpt) {
+  if (lpt && !ctx->window_order) {
     const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
     TRY(build_schedule(ctx, ctx->slots[slot], grid));
     A.units = S.sched_units;

@@ -224,3 +224,18 @@ def test_ten_steps_vs_oracle_at_scale(m, nn, opt):
                                                 ref.full.target, ref.full.rand), 0.01)
     fr = O.forces(ref.Y, ref.full, 0.01)
     assert normwise(f, fr) < 1e-5
+
+
+def test_locality_ordered_graph_repeat_runs_bit_identical():
+    # a planted graph has >= 50% id-local connections, so the library picks the
+    # windowed degree order and the in-order schedule (ivhd_capi.cu fix_permutation)
+    nb = planted_graph(60000, 2)
+    cfg = P.EmbeddingConfig(nn=2, rn=1, c=0.1, iterations=100, seed=1)
+    a = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    b = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    np.testing.assert_array_equal(a.embedding.points, b.embedding.points)
+    assert a.trace.stress == b.trace.stress
+    ref = OracleRun(nb, nn=2, rn=1, c=0.1, iterations=10, seed=1)
+    ref.run()
+    c = P.run_embedding(graph=P.KnnGraph(nb), config=P.EmbeddingConfig(nn=2, rn=1, c=0.1, iterations=10, seed=1))
+    assert normwise(c.embedding.points, ref.Y) < 1e-5
