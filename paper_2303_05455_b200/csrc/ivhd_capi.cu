@@ -728,20 +728,34 @@ int build_schedule(ivhd_ctx* ctx, CsrSlot& S, int grid) {
     return e ? atoi(e) : 3;
   }();
   const int n = S.n_units;
-  std::vector<int> order(n);
-  for (int i = 0; i < n; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return S.unit_cost[a] > S.unit_cost[b]; });
   std::vector<std::vector<int>> per(grid);
-  std::vector<std::pair<int64_t, int>> heap;  // (load, block), min-heap
-  for (int b = 0; b < grid; ++b) heap.push_back({0, b});
-  auto cmp = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) { return x > y; };
-  std::make_heap(heap.begin(), heap.end(), cmp);
-  for (int u : order) {
-    std::pop_heap(heap.begin(), heap.end(), cmp);
-    auto& top = heap.back();
-    per[top.second].push_back(u);
-    top.first += S.unit_cost[u] + c0;
-    std::push_heap(heap.begin(), heap.end(), cmp);
+  if (ctx->window_order) {
+    // id-local input: contiguous unit ranges of equal modelled cost, so one
+    // block sweeps a window's tiles back to back and its nn partners are
+    // still in L2 (and L1) when the neighbouring tiles gather them
+    int64_t total = 0, acc = 0;
+    for (int u = 0; u < n; ++u) total += S.unit_cost[u] + c0;
+    int b = 0;
+    for (int u = 0; u < n; ++u) {
+      per[b].push_back(u);
+      acc += S.unit_cost[u] + c0;
+      while (b < grid - 1 && acc * grid >= (int64_t)(b + 1) * total) ++b;
+    }
+  } else {
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return S.unit_cost[a] > S.unit_cost[b]; });
+    std::vector<std::pair<int64_t, int>> heap;  // (load, block), min-heap
+    for (int b = 0; b < grid; ++b) heap.push_back({0, b});
+    auto cmp = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) { return x > y; };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    for (int u : order) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      auto& top = heap.back();
+      per[top.second].push_back(u);
+      top.first += S.unit_cost[u] + c0;
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
   }
   std::vector<int> words, off(grid + 1, 0);
   words.reserve(n);
@@ -1509,7 +1523,11 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
     const char* e = getenv("IVHD_LPT");
     return !(e && strcmp(e, "0") == 0);
   }();
-  if (lpt && !ctx->window_order) {
+  static const bool contig = [] {  // experiments: IVHD_CONTIG=0 runs id-local inputs round robin
+    const char* e = getenv("IVHD_CONTIG");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  if (lpt && (!ctx->window_order || contig)) {
     const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
     TRY(build_schedule(ctx, ctx->slots[slot], grid));
     A.units = S.sched_units;
