@@ -180,19 +180,22 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the step kernel from the newest committed
-    `ncu --set full` summary (profiles/r*_step_kernel_ncu.json, written by
-    tools/ncu_to_profile.py); None if there is none."""
+def ncu_traffic(workload="c3"):
+    """DRAM bytes per launch of the step kernel from the newest committed ncu
+    capture of THIS workload (C3: profiles/r*_step_kernel_ncu.json, written by
+    tools/ncu_to_profile.py; C5: profiles/r*_c5_step_kernel_ncu.json from
+    tools/c5_ncu.sh); None for workloads without a capture."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_step_kernel_ncu.json")))
+    pattern = {"c3": "r[0-9][0-9]_step_kernel_ncu.json", "c5": "r[0-9][0-9]_c5_step_kernel_ncu.json"}.get(workload)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern))) if pattern else []
     if not files:
         return None
     try:
         d = json.load(open(files[-1]))
         return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": "profiles/" + os.path.basename(files[-1]),
-                "note": "dram__bytes_read.sum + dram__bytes_write.sum, one C3 launch under ncu (cold caches)"}
+                "note": f"dram__bytes_read.sum + dram__bytes_write.sum, one {workload.upper()} launch under ncu "
+                        "(cold caches)"}
     except Exception:
         return None
 
@@ -490,8 +493,8 @@ def gpu_arm(args, w):
                              f"{(nbytes + 8 * m) / 1e6:.0f} MB/iteration may stay L2-resident within a step"},
             "s_per_embed": tot / args.steps, "it_per_s": 1.0 / s_iter,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": (ncu_traffic() or {}).get("bytes_per_launch"),
-                         "traffic_source": (ncu_traffic() or {}).get("source"),
+                         "frac": achieved / peak, "traffic": (ncu_traffic(args.workload) or {}).get("bytes_per_launch"),
+                         "traffic_source": (ncu_traffic(args.workload) or {}).get("source"),
                          "algorithmic_bytes_per_launch": nbytes,
                          "note": f"algorithmic bytes {nbytes} per iteration (8L+36M) / device time "
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
