@@ -234,8 +234,6 @@ int occupancy(ivhd_ctx* ctx, KernelInfo k) {
   auto it = ctx->occ.find(k.fn);
   if (it != ctx->occ.end()) return it->second;
   cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
-  if (const char* cv = getenv("IVHD_CARVEOUT"))  // experiment: shared-memory carveout percent
-    cudaFuncSetAttribute(k.fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
   int n = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, kThreads, k.smem) != cudaSuccess || n < 1) n = 1;
   ctx->occ[k.fn] = n;
@@ -520,16 +518,9 @@ constexpr int64_t kOrderWindow = 2048;
 
 int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old, const int32_t* src, const int32_t* dst, int64_t L) {
   const int64_t m = ctx->m;
-  const char* order = getenv("IVHD_ORDER");  // experiments: "identity" keeps the caller's order
-  if (order && strcmp(order, "identity") == 0) {
-    ctx->perm_fixed = true;
-    return IVHD_OK;
-  }
   cudaStream_t st = ctx->stream;
   int64_t window = 0;
-  if (const char* w = getenv("IVHD_ORDER_WINDOW")) {  // experiments: force a window (0 = global sort)
-    window = std::max<int64_t>(0, atoll(w));
-  } else if (L > 0 && m > 2 * kOrderWindow) {
+  if (L > 0 && m > 2 * kOrderWindow) {
     unsigned long long* dcount = nullptr;
     unsigned long long hcount = 0;
     cudaError_t e0 = dalloc(ctx, &dcount, sizeof(unsigned long long));
@@ -723,10 +714,7 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
 // per-thread partial sums keep a fixed order.
 int build_schedule(ivhd_ctx* ctx, CsrSlot& S, int grid) {
   if (S.sched_grid == grid) return IVHD_OK;
-  static const int c0 = [] {
-    const char* e = getenv("IVHD_LPT_C0");
-    return e ? atoi(e) : 3;
-  }();
+  constexpr int c0 = 3;  // modelled fixed cost of a unit, in slot rounds (profiles/r01_c0_sweep.txt)
   const int n = S.n_units;
   std::vector<std::vector<int>> per(grid);
   if (ctx->window_order) {
@@ -820,10 +808,6 @@ int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
   // Programmatic dependent launch: this grid may become resident while the
   // previous iteration drains; it prefetches graph constants and then waits
   // (griddepcontrol.wait) before reading positions, state or ctrl.
-  static const bool pdl = [] {
-    const char* e = getenv("IVHD_PDL");
-    return !(e && strcmp(e, "0") == 0);
-  }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -833,7 +817,7 @@ int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   CU(ctx, cudaLaunchKernelEx(&cfg, k.fn, A));
   return IVHD_OK;
 }
@@ -873,58 +857,8 @@ int ss_now(ivhd_ctx* ctx) {
 }
 
 
-// ---------------------------------------------------------------- probes
-// Diagnostic kernels over the live CSR (one thread per row, thread-per-vertex):
-// mode 0 streams the column ids, 1 also gathers neighbour positions, 2 loads
-// the row's own position instead (coalesced).  Output one float per row.
-__global__ void k_probe(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
-                        const float2* __restrict__ Y, int64_t m, int mode, float* __restrict__ out) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < m; v += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = rp[v], e = rp[v + 1];
-    float acc = 0.f;
-    for (uint32_t k = b; k < e; k += 4) {
-      uint32_t c4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) c4[q] = k + q < e ? __ldg(col + k + q) : 0u;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (k + q >= e) continue;
-        if (mode == 0) acc += (float)(c4[q] & 0xff);
-        else if (mode == 1) { const float2 p = __ldg(Y + (c4[q] & kIdMask)); acc += p.x + p.y; }
-        else { const float2 p = __ldg(Y + v + (c4[q] & 1)); acc += p.x + p.y; }
-      }
-    }
-    out[v] = acc;
-  }
-}
-
 }  // namespace
 
-extern "C" int ivhd_probe(ivhd_ctx* ctx, int slot, int mode, int iters, int blocks_per_sm, double* us_out) {
-  TRY(check_ready(ctx, slot));
-  const CsrSlot& S = ctx->slots[slot];
-  float* out = reinterpret_cast<float*>(ctx->stage);
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
-  const int grid = ctx->sm_count * blocks_per_sm;
-  k_probe<<<grid, 256, 0, ctx->stream>>>(S.row_ptr, S.col, reinterpret_cast<const float2*>(ctx->ybuf[0]), ctx->m, mode, out);
-  cudaEventRecord(a, ctx->stream);
-  for (int i = 0; i < iters; ++i)
-    k_probe<<<grid, 256, 0, ctx->stream>>>(S.row_ptr, S.col, reinterpret_cast<const float2*>(ctx->ybuf[0]), ctx->m, mode, out);
-  cudaEventRecord(b, ctx->stream);
-  cudaEventSynchronize(b);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, a, b);
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  *us_out = 1e3 * ms / iters;
-  CU(ctx, cudaGetLastError());
-  return IVHD_OK;
-}
-
-namespace {
-}  // namespace
 
 // ======================================================================= C ABI
 
@@ -1042,19 +976,9 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
 
 int ivhd_destroy(ivhd_ctx* ctx) {
   if (!ctx) return IVHD_OK;
-  static const bool dbg = getenv("IVHD_DEBUG_DESTROY") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  auto lap = [&](const char* what) {
-    if (!dbg) return;
-    auto t1 = std::chrono::steady_clock::now();
-    fprintf(stderr, "[ivhd_destroy] %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
-    t0 = t1;
-  };
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  lap("sync");
   drop_graphs(ctx);
-  lap("graphs");
   for (auto& s : ctx->slots) {
     dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.tile_dm); dfree(ctx, s.units);
     dfree(ctx, s.sched_units); dfree(ctx, s.sched_off);
@@ -1064,11 +988,8 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   dfree(ctx, ctx->trace); dfree(ctx, ctx->ctrl); dfree(ctx, ctx->opctrl); dfree(ctx, ctx->red_out);
   dfree(ctx, ctx->stage); dfree(ctx, ctx->op_y); dfree(ctx, ctx->op_force);
   dfree(ctx, ctx->snap_y); dfree(ctx, ctx->snap_state);
-  lap("frees");
   if (ctx->ctrl_h) pinned_ctrl_put(ctx->ctrl_h);
-  lap("free_host");
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
-  lap("stream");
   delete ctx;
   return IVHD_OK;
 }
@@ -1519,15 +1440,7 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   const CsrSlot& S = ctx->slots[slot];
   KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm);
   StepArgs A = make_args(ctx, slot, norm, 1);
-  static const bool lpt = [] {
-    const char* e = getenv("IVHD_LPT");
-    return !(e && strcmp(e, "0") == 0);
-  }();
-  static const bool contig = [] {  // experiments: IVHD_CONTIG=0 runs id-local inputs round robin
-    const char* e = getenv("IVHD_CONTIG");
-    return !(e && strcmp(e, "0") == 0);
-  }();
-  if (lpt && (!ctx->window_order || contig)) {
+  {
     const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
     TRY(build_schedule(ctx, ctx->slots[slot], grid));
     A.units = S.sched_units;

@@ -534,9 +534,6 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
 #define IVHD_MINBLOCKS 3
 #endif
 constexpr int kUnroll = IVHD_UNROLL;
-#ifndef IVHD_BACKOFF_NS
-#define IVHD_BACKOFF_NS 0
-#endif
 #ifndef IVHD_STAGES
 #define IVHD_STAGES 3
 #endif
@@ -556,27 +553,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-#ifndef IVHD_WAIT_HINT_NS
-#define IVHD_WAIT_HINT_NS 0
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if constexpr (IVHD_WAIT_HINT_NS > 0) {  // sleep until the phase flips (or the hint expires)
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity), "n"(IVHD_WAIT_HINT_NS)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-  }
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
 }
 // programmatic dependent launch (griddepcontrol): the next iteration's grid
 // may start once every block has signalled; it waits before reading data the
@@ -618,22 +602,9 @@ __device__ __forceinline__ uint32_t ld_col(const uint32_t* p) {
   asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
-#ifndef IVHD_GATHER_LD
-#define IVHD_GATHER_LD 0
-#endif
-// neighbour-position gather: 0 = ld.global.nc (L1 allocate), 1 = no L1
-// allocation, 2 = L2 only (.cg)
-__device__ __forceinline__ float2 ld_pos(const float2* p) {
-  float2 v;
-  if constexpr (IVHD_GATHER_LD == 1) {
-    asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  } else if constexpr (IVHD_GATHER_LD == 2) {
-    asm("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  } else {
-    v = __ldg(p);
-  }
-  return v;
-}
+// neighbour-position gather through the non-coherent path, allocating in L1
+// (hub positions are re-read by many rows of a block)
+__device__ __forceinline__ float2 ld_pos(const float2* p) { return __ldg(p); }
 #ifndef IVHD_UNIT_CACHE
 #define IVHD_UNIT_CACHE 256
 #endif
@@ -655,11 +626,7 @@ __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G,
 #pragma unroll
   for (int q = 0; q < D; ++q) {
     p[q] = make_float2(y0, y1);
-#ifdef IVHD_ABLATE_GATHER  // timing experiment only: no random traffic (wrong results)
-    if (q < deg) p[q] = __ldg(reinterpret_cast<const float2*>(Yin) + (v ^ 1u));
-#else
     if (q < deg) p[q] = ld_pos(reinterpret_cast<const float2*>(Yin) + (cw[q] & kIdMask));
-#endif
   }
   float fx = f[0], fy = f[1], ee = e;
   unsigned dmask = 0;
@@ -752,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar_r[kStages], bar_a[kStages], bar_b[kStages], bar_e[kStages];
   __shared__ StageMeta meta[kStages];
-  __shared__ float4 sm_wp[kStages][kConsumerWarps];
+  __shared__ double4 sm_wp[kStages][kConsumerWarps];
   __shared__ int sm_cnt[kStages];
   __shared__ double4 sm_red[kBlock / 32];
   __shared__ int sm_units[kUnitCache];  // this block's unit words (static schedule)
@@ -801,7 +768,10 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     nv = (int)max(0LL, min((long long)groups, A.v_end - va));
   };
 
-  float te = 0.f, tn = 0.f, to = 0.f, tb = 0.f;  // fused mode: this thread's running partials
+  // fused mode: this thread's running partials, in fp64 (the auto-adapt test
+  // compares the cancelling difference sum|dnew|^2 - sum|dold|^2 with tau)
+  double te = 0.0, tn = 0.0, to = 0.0;
+  float tb = 0.f;
   if (warp == kConsumerWarps) {
     // ---------------------------------------------------- TMA producer warp
     // Lane 0 issues the bulk copies (the whole warp runs the loop).
@@ -887,7 +857,6 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
           ok = __shfl_sync(0xffffffffu, ok, 0);
           nf += ok & 1;
           nc += (ok >> 1) & 1;
-          if (IVHD_BACKOFF_NS > 0 && !ok) __nanosleep(IVHD_BACKOFF_NS);
         }
       }
     griddep_wait();
@@ -1070,7 +1039,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       // sharded: per-unit partials (rank-count independent order).  Warp
       // partial by a fixed butterfly; the warp that completes the unit sums
       // the 8 warp partials in warp order into the unit partial.
-      float pe = acc_e, pn = acc_n, po = acc_o, pb = acc_bad;
+      double pe = acc_e, pn = acc_n, po = acc_o, pb = acc_bad;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         pe += __shfl_xor_sync(0xffffffffu, pe, o);
@@ -1079,14 +1048,14 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
         pb += __shfl_xor_sync(0xffffffffu, pb, o);
       }
       if (lane == 0) {
-        sm_wp[s][warp] = make_float4(pe, pn, po, pb);
+        sm_wp[s][warp] = make_double4(pe, pn, po, pb);
         __threadfence_block();
         if (atomicAdd(&sm_cnt[s], 1) == kConsumerWarps - 1) {
           __threadfence_block();
           double4 t = make_double4(0, 0, 0, 0);
 #pragma unroll
           for (int w = 0; w < kConsumerWarps; ++w) {
-            const float4 q = sm_wp[s][w];
+            const double4 q = sm_wp[s][w];
             t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
           }
           A.partial[A.tile0 + u] = t;
@@ -1106,7 +1075,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   IVHD_TL(36);
   if (warp < kConsumerWarps) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {  // fp32 butterfly, then fp64 across warps
+    for (int o = 16; o > 0; o >>= 1) {  // fp64 butterfly, then warps in order
       te += __shfl_xor_sync(0xffffffffu, te, o);
       tn += __shfl_xor_sync(0xffffffffu, tn, o);
       to += __shfl_xor_sync(0xffffffffu, to, o);

@@ -47,7 +47,7 @@ def mixture_labels(m, n, clusters=10, seed=0, spread=2.0):
     return rng.integers(0, clusters, size=m)
 
 
-def mixture_knn_graph(m, n=100, k=2, clusters=10, seed=0, device=0, block=None):
+def mixture_knn_graph(m, n=100, k=2, clusters=10, seed=0, device=0, block=None, spread=2.0):
     """Exact kNN graph of `mixture_points`, built by this package's GPU kNN
     builder (knng.build_exact_knn: tcgen05 candidate pass + fp64 re-rank).
     Returns (neighbors (m,k) int32, distances (m,k) float64, labels)."""
@@ -55,6 +55,6 @@ def mixture_knn_graph(m, n=100, k=2, clusters=10, seed=0, device=0, block=None):
 
     if isinstance(device, str):
         device = int(device.split(":")[1]) if ":" in device else 0
-    x, labels = mixture_points(m, n, clusters, seed)
+    x, labels = mixture_points(m, n, clusters, seed, spread)
     g = knng.build_exact_knn(x.astype(np.float64), k, device=device)
     return g.neighbors, g.distances, labels
