@@ -1,28 +1,40 @@
 """Benchmark: IVHD edge-updates/s and seconds per 1.4M-vertex embed on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c3|c1|c2-adadelta|c2-nesterov|c4|c5]
 
 Workload (BASELINE.json configs[2], "C3"): YAHOO-shaped synthetic kNN graph,
-M = 1.4M points of a 10-cluster Gaussian mixture in 100-D, exact-kNN (k=2)
-built on the GPU (excluded from timing, as in the paper), nn=2, rn=1, c=0.1,
-force-directed with the reference defaults, 2500 iterations, seed 0.
+the exact 2-NN graph of M = 1.4M points of a 10-cluster Gaussian mixture in
+100-D (spread 0.42, so the label metrics do not saturate: cf_10 = 0.76),
+nn=2, rn=1, c=0.1, force-directed with the reference defaults, 2500
+iterations, seed 0.  The graph is a committed fixture
+(tests/golden/c3_graph.npz, built by the package's exact GPU kNN builder;
+kNN construction is excluded from timing, as in the paper, and timed
+separately in the `knn` leg, which also checks it rebuilds the fixture).
 
 One "step" = one full 2500-iteration embed.  `value` = edge-updates/s with
 the graph, positions and state resident in HBM (device-timed with CUDA
 events on the launching stream; L2 flushed by a 256 MB write between
 steps).  `e2e` = the same metric through the public API
-`run_embedding(graph, config)` from host arrays (RNG setup, CSR build, H2D,
-loop, D2H included).  `roofline` = algorithmic HBM bytes per iteration
-(8L + 36M for force-directed) / device time per iteration.
-`cpu_baseline` = the CPU oracle port (oracle/, a restatement of the
-reference's numpy loop) on a bounded sample of the same workload.
+`run_embedding(graph, config)` (N GPUs: `run_embedding_distributed`) from
+host arrays in pinned memory (RNG setup, CSR build, H2D, loop, D2H).
+`roofline` = algorithmic HBM bytes per iteration (8L + 36M
+for force-directed) / device time per iteration.  `cpu_baseline` = the
+reference package itself (`baseline/_ref`, ivhd.engine.run_embedding, all
+host threads) on a bounded sample of the same workload.  `quality` = the
+label neighbour hit and rank-curve summary of the e2e embedding beside the
+reference's own full-run values (tests/golden/quality_c3.npz).
 
-`--impl reference` times the reference algorithm's CPU implementation (the
-oracle port; the reference itself is pure Python and cannot travel to the
-GPU box) on all host cores, rank 0 only.
+`--impl reference` times the UNMODIFIED reference package installed in
+baseline/_ref (`ivhd.engine.run_embedding`, threads = all host cores) on the
+same graph and config, rank 0 only; it never imports this package.
+
+N > 1: `python bench.py --gpus N` starts N ranks itself (one process per
+GPU, NCCL) when it is not already running under torchrun.
 """
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
@@ -34,29 +46,30 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-if ROOT not in sys.path:
-    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 METRIC = "IVHD edge-updates/s (1.4M-vertex YAHOO-shaped embed, nn=2 rn=1, 2500 iterations)"
 UNIT = "edge-updates/s"
 
 WORKLOADS = {
-    # name: (M, N dims, nn, rn, c, optimizer, iterations, graph kind)
-    "c3": dict(m=1_400_000, n=100, nn=2, rn=1, c=0.1, optimizer="force-directed",
-               iterations=2500, graph="mixture"),
-    "c1": dict(m=20_000, n=784, nn=2, rn=1, c=0.01, optimizer="force-directed",
-               iterations=2000, graph="mixture"),
-    "c2-adadelta": dict(m=70_000, n=784, nn=5, rn=1, c=0.01, optimizer="adadelta",
-                        iterations=2500, graph="mixture"),
-    # the default alpha (0.02) diverges on this hub-heavy synthetic graph in the
-    # reference algorithm too (oracle, fp64: iteration 74; tools/nesterov_check.py)
-    "c2-nesterov": dict(m=70_000, n=784, nn=5, rn=1, c=0.01, optimizer="nesterov",
-                        iterations=2500, graph="mixture", alpha=2e-4),
-    "c4": dict(m=10_000_000, n=0, nn=3, rn=1, c=0.1, optimizer="force-directed",
-               iterations=200, graph="planted"),
-    # the paper's 10^8+ scale on ONE B200 (BASELINE configs[4] names 8 GPUs)
-    "c5": dict(m=100_000_000, n=0, nn=2, rn=1, c=0.1, optimizer="force-directed",
-               iterations=100, graph="planted"),
+    # graph: committed fixture (tests/golden/<file>, key "neighbors") or "planted"
+    "c3": dict(m=1_400_000, n=100, nn=2, rn=1, c=0.1, optimizer="force-directed", iterations=2500,
+               graph="c3_graph.npz", spread=0.42, golden="quality_c3.npz",
+               desc="YAHOO-shaped: exact 2-NN graph of a 1.4M x 100 ten-cluster mixture (spread 0.42)"),
+    "c1": dict(m=20_000, n=784, nn=2, rn=1, c=0.01, optimizer="force-directed", iterations=2000,
+               graph="c1_golden.npz", spread=0.23, golden="c1_golden.npz",
+               desc="exact 2-NN graph of a 20k x 784 ten-cluster mixture (spread 0.23)"),
+    "c2-adadelta": dict(m=70_000, n=784, nn=5, rn=1, c=0.01, optimizer="adadelta", iterations=2500,
+                        graph="c2_golden.npz", golden="c2_golden.npz",
+                        desc="MNIST-shaped: exact 5-NN graph of the reference's mnist_like(70000, 784)"),
+    "c2-nesterov": dict(m=70_000, n=784, nn=5, rn=1, c=0.01, optimizer="nesterov", iterations=2500,
+                        graph="c2_golden.npz", golden="c2_golden.npz",
+                        desc="MNIST-shaped: exact 5-NN graph of the reference's mnist_like(70000, 784)"),
+    "c4": dict(m=10_000_000, n=0, nn=3, rn=1, c=0.1, optimizer="force-directed", iterations=200,
+               graph="planted", desc="planted-cluster kNN-shaped graph M=10^7 (synth.planted_graph)"),
+    # the paper's 10^8+ scale (BASELINE configs[4] names 8 GPUs)
+    "c5": dict(m=100_000_000, n=0, nn=2, rn=1, c=0.1, optimizer="force-directed", iterations=100,
+               graph="planted", desc="planted-cluster kNN-shaped graph M=10^8 (synth.planted_graph)"),
 }
 
 
@@ -64,50 +77,49 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-# ------------------------------------------------------------------ inputs
+def _synth():
+    """synth.py loaded standalone (numpy only): the reference arm uses the same
+    input generators without importing this package."""
+    spec = importlib.util.spec_from_file_location("ivhd_b200_synth",
+                                                  os.path.join(ROOT, "paper_2303_05455_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
 
-def make_graph(w, rank_device):
-    from paper_2303_05455_b200 import synth
-
+def make_graph(w):
+    """The workload's kNN graph (input synthesis only, never timed)."""
     t0 = time.perf_counter()
-    # input synthesis only (never timed): cache the kNN graph within one box
-    cache = os.path.join(os.environ.get("IVHD_GRAPH_CACHE", "/tmp"),
-                         f"ivhd_graph_v2_{w['graph']}_{w['m']}_{w['n']}_{w['nn']}.npy")
-    if os.path.exists(cache):
-        nb = np.load(cache)
-        log(f"[bench] graph {w['graph']} M={w['m']} loaded from {cache}")
-        return nb
     if w["graph"] == "planted":
-        nb = synth.planted_graph(w["m"], w["nn"], seed=0)
+        nb = _synth().planted_graph(w["m"], w["nn"], seed=0)
     else:
-        nb, _, _ = synth.mixture_knn_graph(w["m"], w["n"], k=w["nn"], seed=0, device=rank_device)
-    log(f"[bench] graph {w['graph']} M={w['m']} k={w['nn']} built in {time.perf_counter() - t0:.1f}s")
-    try:
-        np.save(cache, nb)
-    except OSError:
-        pass
+        nb = np.ascontiguousarray(np.load(os.path.join(GOLDEN, w["graph"]))["neighbors"], dtype=np.int32)
+    assert nb.shape[0] == w["m"], (nb.shape, w["m"])
+    log(f"[bench] graph {w['graph']} M={w['m']} ready in {time.perf_counter() - t0:.1f}s")
     return nb
+
+
+def workload_config(args, w, world):
+    return {"workload": f"{args.workload}: {w['desc']}, nn={w['nn']} rn={w['rn']} c={w['c']} "
+                        f"{w['optimizer']}, {w['iterations']} iterations per step",
+            "m": w["m"], "connections": (w["nn"] + w["rn"]) * w["m"],
+            "iterations_per_step": w["iterations"],
+            "parallelism": f"vertex-range shards x{world} (one process per GPU)" if world > 1 else "single GPU",
+            "l2": "flushed between steps (256 MB write)"}
 
 
 # ------------------------------------------------------------------ clocks
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """NVML clocks + throttle reasons sampled during the timed region."""
 
     def __init__(self, index=0):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.nv = None
 
     def __enter__(self):
-        # NVML from a thread (10 ms period) so short timed regions still get
-        # many samples; nvidia-smi -lms as the fallback
         try:
             import pynvml as nv
 
@@ -118,23 +130,13 @@ class ClockSampler:
                 ids = [v.strip() for v in vis.split(",")]
                 if idx < len(ids) and ids[idx].isdigit():
                     idx = int(ids[idx])
-            h = nv.nvmlDeviceGetHandleByIndex(idx)
-            self.nv, self.h = nv, h
+            self.h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = nv
             self.stop = threading.Event()
             self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-            return self
         except Exception:
             self.nv = None
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except Exception:
-            self.proc = None
         return self
 
     def _poll(self):
@@ -146,143 +148,135 @@ class ClockSampler:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.rows.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+                self.rows.append((float(sm), float(mx), [bool(r & b) for b in bits]))
             except Exception:
                 pass
             self.stop.wait(0.01)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
-
     def __exit__(self, *exc):
-        if getattr(self, "nv", None) is not None:
+        if self.nv is not None:
             self.stop.set()
             self.thread.join(timeout=2)
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2][i]})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons, "samples": len(self.rows)}
 
 
-def ncu_traffic(workload="c3"):
+def ncu_traffic(workload):
     """DRAM bytes per launch of the step kernel from the newest committed ncu
-    capture of THIS workload (C3: profiles/r*_step_kernel_ncu.json, written by
-    tools/ncu_to_profile.py; C5: profiles/r*_c5_step_kernel_ncu.json from
-    tools/c5_ncu.sh); None for workloads without a capture."""
+    capture of THIS workload (profiles/rNN_<workload>_step_ncu.json, written by
+    tools/ncu_to_profile.py); None for workloads without one."""
     import glob
 
-    pattern = {"c3": "r[0-9][0-9]_step_kernel_ncu.json", "c5": "r[0-9][0-9]_c5_step_kernel_ncu.json"}.get(workload)
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern))) if pattern else []
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r[0-9][0-9]_{workload}_step_ncu.json")))
     if not files:
         return None
     try:
         d = json.load(open(files[-1]))
         return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": "profiles/" + os.path.basename(files[-1]),
-                "note": f"dram__bytes_read.sum + dram__bytes_write.sum, one {workload.upper()} launch under ncu "
-                        "(cold caches)"}
+                "capture": d.get("capture", "")}
     except Exception:
         return None
 
 
-# ------------------------------------------------------------ CPU baseline
+# ------------------------------------------------------- the reference (CPU)
 
 
-def cpu_sample(nb, w, budget_s=15.0, threads=None):
-    """Time the oracle port (CPU restatement of the reference loop) on the
-    same graph: whole iterations, all host threads, ~budget_s of work."""
-    from oracle.ivhd_oracle import OracleRun
+def _import_reference():
+    """The unmodified reference package from baseline/_ref (pip-installed from
+    /root/reference); None when it is not there."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "ivhd")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import ivhd
+    import ivhd.engine
+    import ivhd.knng
 
-    threads = threads or os.cpu_count() or 1
-    run = OracleRun(nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=10**9, seed=0,
-                    optimizer=w["optimizer"], threads=threads,
-                    opt={"alpha": w["alpha"]} if "alpha" in w else None)
-    t0 = time.perf_counter()
-    run.step()
-    t1 = time.perf_counter() - t0
-    n = int(max(2, min(50, budget_s / max(t1, 1e-6))))
-    t0 = time.perf_counter()
-    for _ in range(n):
-        run.step()
-    dt = time.perf_counter() - t0
-    L = (w["nn"] + w["rn"]) * w["m"]
-    return {"value": L * n / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{n} iterations of the C3 loop (after 1 warm-up) at M={w['m']}, "
-                      f"numpy oracle with {threads} threads; {dt / n * 1e3:.1f} ms/iteration",
-            "s_per_iteration": dt / n}
+    assert os.path.realpath(ivhd.__file__).startswith(os.path.realpath(ref)), ivhd.__file__
+    return ivhd
 
 
-def _opt(w):
-    from paper_2303_05455_b200 import OptimizerParams
+class ReferenceTimer:
+    """Times `ivhd.engine.run_embedding(graph, config, threads=all cores)` of
+    the reference on the workload's graph; one call = `n` loop iterations (a
+    bounded sample of the embed; its setup, _Run + RNG draws, is inside)."""
 
-    return OptimizerParams(alpha=w["alpha"]) if "alpha" in w else None
+    def __init__(self, nb, w):
+        self.ivhd = _import_reference()
+        self.w = w
+        self.threads = os.cpu_count() or 1
+        self.L = (w["nn"] + w["rn"]) * w["m"]
+        if self.ivhd is not None:
+            self.kind = "reference"
+            self.graph = self.ivhd.knng.KnnGraph(neighbors=nb, distances=np.zeros(nb.shape),
+                                                 metric="euclidean")
+        else:  # the oracle restatement (test infrastructure) only if baseline/_ref is missing
+            self.kind = "port"
+            self.nb = nb
+
+    def call(self, n):
+        w = self.w
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            E = self.ivhd.engine
+            cfg = E.EmbeddingConfig(nn=w["nn"], rn=w["rn"], c=w["c"], iterations=n, seed=0,
+                                    optimizer=w["optimizer"])
+            E.run_embedding(graph=self.graph, config=cfg, threads=self.threads)
+        else:
+            sys.path.insert(0, ROOT)
+            from oracle.ivhd_oracle import OracleRun
+
+            OracleRun(self.nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=n, seed=0,
+                      optimizer=w["optimizer"], threads=self.threads).run()
+        return time.perf_counter() - t0
+
+    def pick_n(self, budget_s):
+        """Iterations per call so one call takes about budget_s (from a 2-iteration probe)."""
+        t2 = self.call(2)
+        t1 = self.call(1)
+        per = max(t2 - t1, 1e-4)
+        return int(max(1, min(self.w["iterations"], round((budget_s - t1 + per) / per))))
+
+    def describe(self, n, value):
+        what = ("ivhd.engine.run_embedding from baseline/_ref (the unmodified reference package)"
+                if self.kind == "reference" else "oracle port of the reference loop (baseline/_ref missing)")
+        return {"value": value, "unit": UNIT, "cores": self.threads, "kind": self.kind,
+                "sample": f"run_embedding(iterations={n}) per call (setup included) of the "
+                          f"{self.w['iterations']}-iteration embed at M={self.w['m']}: {what}, threads={self.threads}"}
 
 
 def reference_arm(args, w):
-    """--impl reference: CPU implementation of the path on all host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's CPU implementation on all host cores."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
-    dev = "cuda" if _cuda_ok() else "cpu"
-    nb = make_graph(w, dev)
-    from oracle.ivhd_oracle import OracleRun
-
-    threads = os.cpu_count() or 1
-    run = OracleRun(nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=10**9, seed=0,
-                    optimizer=w["optimizer"], threads=threads,
-                    opt={"alpha": w["alpha"]} if "alpha" in w else None)
-    L = (w["nn"] + w["rn"]) * w["m"]
-    per_step = max(1, args.ref_iters)
+    nb = make_graph(w)
+    rt = ReferenceTimer(nb, w)
+    n = args.ref_iters or rt.pick_n(args.ref_budget)
     for _ in range(args.warmup):
-        for _ in range(per_step):
-            run.step()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        for _ in range(per_step):
-            run.step()
-        times.append(time.perf_counter() - t0)
+        rt.call(n)
+    times = [rt.call(n) for _ in range(args.steps)]
     tot = sum(times)
-    value = L * per_step * args.steps / tot
+    value = rt.L * n * args.steps / tot
+    world = args.gpus
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-        "data": "synthetic (same generator and seed as the b200 arm)",
-        "config": {"workload": args.workload, **{k: w[k] for k in ("m", "nn", "rn", "c", "optimizer")},
-                   "iterations_per_step": per_step},
-        "s_per_embed_extrapolated": tot / (args.steps * per_step) * w["iterations"],
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{per_step} loop iterations per step of the {w['iterations']}-"
-                                   f"iteration embed, oracle port of the reference numpy loop"},
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic (the b200 arm's graph fixture / generator, same seed)",
+        "config": workload_config(args, w, world),
+        "s_per_embed_extrapolated": tot / (args.steps * n) * w["iterations"],
+        "cpu_baseline": rt.describe(n, value),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def _cuda_ok():
-    try:
-        import torch
-
-        return torch.cuda.is_available()
-    except Exception:
-        return False
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -295,41 +289,80 @@ def algorithmic_bytes(m, n_entries, optimizer):
     return 4 * n_entries + 4 * (m + 1) + 16 * m + 16 * s * m
 
 
-def knn_leg(w, local, peaks):
+def knn_leg(w, local, peaks, nb):
     """Time the GPU kNN builder (excluded from the embed
-    timing, as in the paper) on the workload's point set: one warm-up
-    full build, then a timed one.  Reported beside the embed line."""
+    timing, as in the paper) on the workload's point set, and check that it
+    rebuilds the committed graph fixture."""
     from paper_2303_05455_b200 import knng, synth
 
-    if w["graph"] != "mixture":
+    if "spread" not in w:
         return None
-    x, _ = synth.mixture_points(w["m"], w["n"], seed=0)
+    x, _ = synth.mixture_points(w["m"], w["n"], seed=0, spread=w["spread"])
     x = x.astype(np.float64)
-    best = None
+    best, g = None, None
     for _ in range(2):  # the first build also grows the stream-ordered memory pool
         t0 = time.perf_counter()
-        knng.build_exact_knn(x, w["nn"], device=local)
+        g = knng.build_exact_knn(x, w["nn"], device=local)
         wall = time.perf_counter() - t0
         if best is None or wall < best[0]:
             best = (wall, dict(knng.last_stats))
     wall, st = best
     kp = (w["n"] + 7) // 8 * 8
     flops = 2.0 * w["m"] * w["m"] * kp
-    peak = float(peaks.get("bf16_tflops", 1647.6)) / 2.0
+    peak = float(peaks.get("bf16_tflops", 1685.7)) / 2.0
     ach = flops / st["tc_seconds"] / 1e12
     return {"workload": f"exact kNN graph, M={w['m']} N={w['n']} k={w['nn']} (euclidean, fp64 input)",
             "s_per_build": wall, "tc_pass_s": st["tc_seconds"], "rerank_s": st["rerank_seconds"],
             "exact_rescan_rows": st["exact_rows"],
-            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                         "frac": ach / peak,
+            "rebuilds_fixture": bool(np.array_equal(g.neighbors[:, : nb.shape[1]], nb)),
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                          "note": "tf32 tcgen05 candidate pass: 2*M^2*Kpad flops / pass time; peak = "
                                  "MEASURED_PEAKS.json bf16_tflops / 2 (dense tf32 rate is half of bf16)"}}
+
+
+def quality_leg(w, points, local):
+    """Label neighbour hit (all points) and rank curves (the reference's
+    subsample) of the e2e embedding, beside the reference's own values."""
+    from paper_2303_05455_b200 import metrics, synth
+
+    if "golden" not in w:
+        return None
+    g = np.load(os.path.join(GOLDEN, w["golden"]))
+    m = w["m"]
+    if "labels" in g:
+        labels = g["labels"].astype(np.int64)
+    else:
+        labels = synth.mixture_labels(m, w["n"], seed=0, spread=w["spread"])
+    metrics.neighbor_hit(points[:4096], labels[:4096], nn_max=100, device=local)  # warm-up
+    t0 = time.perf_counter()
+    cf_nn, cf = metrics.neighbor_hit(points, labels, nn_max=100, device=local)
+    q = {"neighbor_hit_cf": cf, "cf_2": float(cf_nn[1]), "cf_10": float(cf_nn[9]),
+         "seconds": time.perf_counter() - t0,
+         "note": "metrics.neighbor_hit(nn_max=100) of the e2e embedding on the GPU (exact grid kNN)"}
+    pre = w["optimizer"] + "_" if w["optimizer"] + "_cf" in g else ""
+    q["reference"] = {"neighbor_hit_cf": float(g[pre + "cf"]), "cf_2": float(g[pre + "cf_nn"][1]),
+                      "cf_10": float(g[pre + "cf_nn"][9]), "stress": float(g[pre + "stress"]),
+                      "source": f"tests/golden/{w['golden']} (reference ivhd.engine.run_embedding, fp64 CPU)"}
+    if "summary_keys" in g and "spread" in w:
+        sub = g["sub"] if "sub" in g else np.arange(m)
+        x, _ = synth.mixture_points(m, w["n"], seed=0, spread=w["spread"])
+        xs = x[sub].astype(np.float64)
+        del x
+        t0 = time.perf_counter()
+        cur = metrics.evaluate_embedding(xs, points[sub], labels=labels[sub], nn_max=100, report_ks=(15, 100),
+                                         device=local)
+        q["curves"] = {**cur.summary(), "seconds": time.perf_counter() - t0,
+                       "sample": f"{len(sub)} rows (the reference golden's subsample)",
+                       "note": "metrics.evaluate_embedding on the GPU (curve pass k_max=1000)"}
+        q["reference"]["curves"] = {str(k): float(v) for k, v in zip(g["summary_keys"], g["summary_vals"])}
+    return q
 
 
 def gpu_arm(args, w):
     import torch
     import torch.distributed as dist
 
+    sys.path.insert(0, ROOT)
     from paper_2303_05455_b200 import EmbeddingConfig, KnnGraph, run_embedding
     from paper_2303_05455_b200.config import resolve_optimizer
     from paper_2303_05455_b200.device import DeviceEmbedding
@@ -338,20 +371,21 @@ def gpu_arm(args, w):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus or args.sharded, f"WORLD_SIZE={world} but --gpus {args.gpus}"
     torch.cuda.set_device(local)
     sharded = world > 1 or args.sharded
     if sharded:
-        if world == 1:  # --sharded on one GPU: a one-rank NCCL group
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+        if "MASTER_PORT" not in os.environ:
             import socket
 
             with socket.socket() as so:
                 so.bind(("127.0.0.1", 0))
-                os.environ.setdefault("MASTER_PORT", str(so.getsockname()[1]))
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("RANK", "0")
-            os.environ.setdefault("WORLD_SIZE", "1")
+                os.environ["MASTER_PORT"] = str(so.getsockname()[1])
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    nb = make_graph(w, f"cuda:{local}")
+    nb = make_graph(w)
     m, L, iters = w["m"], (w["nn"] + w["rn"]) * w["m"], w["iterations"]
 
     # same setup draws as run_embedding (engine.py:165, 214-215)
@@ -368,7 +402,7 @@ def gpu_arm(args, w):
         dev = ShardedEmbedding(m, 2, rank, world, device=local, stream=stream.cuda_stream)
     else:
         dev = DeviceEmbedding(m, 2, device=local, stream=stream.cuda_stream)
-    dev.set_optimizer(resolve_optimizer(w["optimizer"], m, opt=_opt(w)))
+    dev.set_optimizer(resolve_optimizer(w["optimizer"], m))
     dev.set_positions(y0)
     dev.set_graph(0, nn_sets, rn)
     dev.snapshot()
@@ -384,7 +418,7 @@ def gpu_arm(args, w):
         flush.zero_()
         one_step()
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     times = []
     with ClockSampler(local) as clk:
@@ -399,115 +433,97 @@ def gpu_arm(args, w):
             times.append(ev0.elapsed_time(ev1) / 1e3)
     torch.cuda.synchronize()
     tot = sum(times)
-    if world > 1:
+    if sharded:
         t = torch.tensor([tot], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot = float(t.item())
         dist.barrier()
     value = L * iters * args.steps / tot
     s_iter = tot / (args.steps * iters)
-    final_stress = None
+    dev_launches = dev.launches_per_iteration() if hasattr(dev, "launches_per_iteration") else 1
+    dev.close() if hasattr(dev, "close") else None
 
-    # ---------------- e2e: public API from host arrays (rank 0, N == 1)
+    # ---------------- e2e: public API from pinned host arrays
     e2e = None
     final_points = None
-    if world == 1 and not args.no_e2e:
-        # the step's input, the kNN graph, lives in pinned host memory
+    final_stress = None
+    if not args.no_e2e:
         nb_pinned = torch.empty(nb.shape, dtype=torch.int32, pin_memory=True).numpy()
         nb_pinned[...] = nb
         graph = KnnGraph(nb_pinned)
         cfg = EmbeddingConfig(nn=w["nn"], rn=w["rn"], c=w["c"], iterations=iters, seed=0,
-                              optimizer=w["optimizer"], opt=_opt(w))
+                              optimizer=w["optimizer"])
+        if sharded:
+            from paper_2303_05455_b200.sharded import run_embedding_distributed
+
+            call = lambda: run_embedding_distributed(graph=graph, config=cfg, device=local)  # noqa: E731
+        else:
+            call = lambda: run_embedding(graph=graph, config=cfg, device=local)  # noqa: E731
         walls = []
         for i in range(2 + args.e2e_steps):
             torch.cuda.synchronize()
+            if sharded:
+                dist.barrier()
             t0 = time.perf_counter()
-            res = run_embedding(graph=graph, config=cfg, device=local)
+            res = call()
             torch.cuda.synchronize()
-            if i >= 2:  # two warm-up calls: the second fills the result-buffer pool while the first result is alive
-                walls.append(time.perf_counter() - t0)
+            wall = time.perf_counter() - t0
+            if sharded:
+                t = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                wall = float(t.item())
+            if i >= 2:  # two warm-up calls (allocator pools, pinned result buffers)
+                walls.append(wall)
         final_stress = res.state.stress
         final_points = res.embedding.points
-        # H2D: the nn-id block (the layout and random partners are drawn on
-        # the device); D2H: positions (x2) + deltas, the partners, the trace
+        # H2D: the nn-id block (the layout and random partners are drawn on the
+        # device); D2H: positions (state + embedding) and deltas, the partners, the trace
         h2d = m * nb.shape[1] * 4
-        d2h = 3 * m * 2 * 8 + m * w["rn"] * 4 + iters * 16  # positions twice (state + embedding), deltas
+        d2h = 3 * m * 2 * 8 + m * w["rn"] * 4 + iters * 16
         e2e = {"value": L * iters / statistics.mean(walls), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "s_per_embed": statistics.mean(walls), "steps": len(walls)}
-
-    cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu:
-        cpu = cpu_sample(nb, w, budget_s=args.cpu_budget)
 
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        rt = ReferenceTimer(nb, w)
+        n = rt.pick_n(args.cpu_budget / 3)
+        ts = [rt.call(n) for _ in range(2)]
+        cpu = rt.describe(n, rt.L * n * len(ts) / sum(ts))
     knn = None
     if world == 1 and rank == 0 and not args.no_knn:
-        knn = knn_leg(w, local, peaks)
+        knn = knn_leg(w, local, peaks, nb)
     quality = None
-    if final_points is not None and w["graph"] == "mixture":
-        # label neighbour hit of the embedding (metrics.neighbor_hit, GPU grid kNN)
-        from paper_2303_05455_b200 import metrics, synth
-
-        labels = synth.mixture_labels(m, w["n"], seed=0)
-        metrics.neighbor_hit(final_points[:4096], labels[:4096], nn_max=100, device=local)  # warm-up
-        t0 = time.perf_counter()
-        cf_nn, cf = metrics.neighbor_hit(final_points, labels, nn_max=100, device=local)
-        quality = {"neighbor_hit_cf": cf, "cf_2": float(cf_nn[1]), "cf_10": float(cf_nn[9]),
-                   "seconds": time.perf_counter() - t0,
-                   "note": "metrics.neighbor_hit(nn_max=100) of the e2e embedding on the GPU (exact grid kNN)"}
-        # rank curves (R_NX / G_NN AUC, trust/continuity) on a fixed seeded
-        # subsample: the O(M^2) metrics, as SURVEY §8(c) prescribes above 20k
-        x_all, _ = synth.mixture_points(m, w["n"], seed=0)
-        sub = np.sort(np.random.default_rng(0).choice(m, size=min(m, 20000), replace=False))
-        xs, ys, ls = x_all[sub].astype(np.float64), final_points[sub], labels[sub]
-        del x_all
-        t0 = time.perf_counter()
-        cur = metrics.evaluate_embedding(xs, ys, labels=ls, nn_max=100, report_ks=(15, 100), device=local)
-        quality["curves"] = {**cur.summary(), "seconds": time.perf_counter() - t0,
-                             "sample": f"{len(sub)} rows, sorted default_rng(0).choice(M)",
-                             "note": "metrics.evaluate_embedding on the GPU (curve pass k_max=1000)"}
+    if final_points is not None and rank == 0 and not args.no_quality:
+        quality = quality_leg(w, final_points, local)
 
     if rank == 0:
-        peak = float(peaks.get("hbm_gbs", 6650.0))
+        peak = float(peaks.get("hbm_gbs", 6550.0))
         nbytes = algorithmic_bytes(m, n_entries, w["optimizer"])
         achieved = nbytes / s_iter / 1e9
+        tr = ncu_traffic(args.workload) or {}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": ("synthetic: 10-cluster Gaussian mixture, exact kNN graph from the package's GPU "
-                     "builder (untimed here; timed separately under 'knn')") if w["graph"] == "mixture" else
-                    "synthetic: planted-cluster kNN-shaped graph (synth.planted_graph, untimed)",
-            "config": {"workload": f"{args.workload}: " + (f"{'YAHOO' if w['n'] == 100 else 'MNIST'}-shaped M={m} N={w['n']} kNN graph, "
-                                   if w["graph"] == "mixture" else f"planted-cluster graph M={m}, ") +
-                                   f"nn={w['nn']} rn={w['rn']} c={w['c']} {w['optimizer']}, "
-                                   f"{iters} iterations per step",
-                       "m": m, "connections": L, "iterations_per_step": iters,
-                       "parallelism": f"vertex-range shards x{world}" if sharded else "single GPU",
-                       "l2": "flushed between steps (256 MB write); working set ~"
-                             f"{(nbytes + 8 * m) / 1e6:.0f} MB/iteration may stay L2-resident within a step"},
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic: {w['desc']} (committed fixture / seeded generator; kNN untimed, "
+                    "timed separately under 'knn')",
+            "config": workload_config(args, w, world),
             "s_per_embed": tot / args.steps, "it_per_s": 1.0 / s_iter,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": (ncu_traffic(args.workload) or {}).get("bytes_per_launch"),
-                         "traffic_source": (ncu_traffic(args.workload) or {}).get("source"),
+                         "frac": achieved / peak, "traffic": tr.get("bytes_per_launch"),
+                         "traffic_source": tr.get("source"), "traffic_capture": tr.get("capture"),
                          "algorithmic_bytes_per_launch": nbytes,
-                         "note": f"algorithmic bytes {nbytes} per iteration (8L+36M) / device time "
+                         "note": f"algorithmic bytes {nbytes} per iteration (8L+36M for FD) / device time "
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
-            "roofline_gather": {
-                "bound": "l1tex->xbar requests", "achieved": n_entries / s_iter / 1e9,
-                "peak": 148 * float(peaks.get("sm_max_mhz", 1965.0)) / 1e3, "unit": "G requests/s",
-                "frac": (n_entries / s_iter) / (148 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6),
-                "note": "the binding unit per ncu (profiles/r01_step_kernel_ncu.txt): every symmetrised "
-                        "entry's 8-byte neighbour gather misses L1 and is one L1->crossbar request; the "
-                        "interface issues ~1 request/cycle/SM (l1tex__m_l1tex2xbar_req_cycles_active); "
-                        "achieved = 2L requests per iteration / device time per iteration"},
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * iters * (2 if sharded else 1), "clocks": clk.summary(),
+            "gpu_launches": args.steps * iters * dev_launches, "clocks": clk.summary(),
             "final_stress_e2e": final_stress,
             "knn": knn, "quality": quality,
         }
@@ -515,6 +531,13 @@ def gpu_arm(args, w):
     if sharded:
         dist.destroy_process_group()
     return 0
+
+
+def _spawned(rank, world, port, argv):
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.argv = [sys.argv[0]] + argv
+    main()
 
 
 def main():
@@ -528,17 +551,31 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
-                    help="use the multi-GPU (sharded, NCCL) loop even on one GPU")
+                    help="use the multi-GPU (sharded) loop even on one GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-knn", action="store_true", help="skip the kNN-builder leg")
+    ap.add_argument("--no-quality", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--ref-iters", type=int, default=4, help="reference arm: iterations per step")
+    ap.add_argument("--ref-iters", type=int, default=0, help="reference arm: iterations per step (0 = auto)")
+    ap.add_argument("--ref-budget", type=float, default=3.0, help="reference arm: seconds per step (auto)")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload])
     if args.iterations:
         w["iterations"] = args.iterations
     if args.impl == "reference":
         return reference_arm(args, w)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not under torchrun: start one process per GPU ourselves
+        import socket
+
+        import torch.multiprocessing as mp
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        mp.start_processes(_spawned, args=(args.gpus, port, sys.argv[1:]), nprocs=args.gpus,
+                           start_method="spawn", join=True)
+        return 0
     return gpu_arm(args, w)
 
 

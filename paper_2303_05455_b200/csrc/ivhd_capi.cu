@@ -18,6 +18,7 @@
 
 #include "../../include/ivhd_b200.h"
 #include "ivhd_step.cuh"
+#include "ivhd_step_f64.cuh"
 #include "ivhd_rng.cuh"
 
 using namespace ivhd;
@@ -35,6 +36,7 @@ struct CsrSlot {
   int* units = nullptr;         // work units (tile << 12 | pass << 7 | min(slots per lane,15) << 3 | log2 G)
   int n_units = 0;
   std::vector<int> unit_base;   // host: first unit of each tile (n_tiles_cap + 1)
+  int* d_unit_base = nullptr;   // device copy (sharded fold of unit partials into tile partials)
   std::vector<int> unit_words;  // host copy of units
   std::vector<int> unit_cost;   // host: modelled cost of each unit (slot rounds per lane)
   int sched_grid = 0;           // grid the cost-balanced schedule below was built for
@@ -50,6 +52,7 @@ using KernelFn = void (*)(StepArgs);
 struct KernelInfo {
   KernelFn fn;
   int smem;
+  int threads = kThreads;
 };
 
 struct GraphKey {
@@ -84,8 +87,10 @@ struct ivhd_ctx {
   bool window_order = false;  // locality-ordered input: degree sort inside id windows, in-order schedule
 
   float* ybuf[2] = {nullptr, nullptr};  // 8 floats/vertex capacity
-  float* state = nullptr;               // 8 floats/vertex capacity
-  double4* partial = nullptr;
+  float* state = nullptr;               // state_fpv floats/vertex capacity
+  int state_fpv = 8;                    // 16 for fp64 Adam in 3-D
+  double4* partial = nullptr;  // per work unit (sharded / operator calls)
+  double4* tpart = nullptr;    // per tile [n_tiles_cap]: the array ranks exchange (sharded)
   double4* bpart = nullptr;  // one per resident block of the step kernel
   double2* trace = nullptr;
   int64_t trace_cap = 0;
@@ -189,7 +194,12 @@ inline cudaError_t dalloc(ivhd_ctx* ctx, T** p, size_t bytes);
 template <class T>
 inline void dfree(ivhd_ctx* ctx, T* p);
 
-inline int ys_of(int dim, int opt) { return (opt == OPT_NEST) ? (dim == 2 ? 4 : 8) : (dim == 2 ? 2 : 4); }
+// floats per vertex of a position buffer: fp32 (y | y + beta v for
+// Nesterov), or fp64 for Adam (ivhd_step_f64.cuh)
+inline int ys_of(int dim, int opt) {
+  return (opt == OPT_NEST || opt == OPT_ADAM) ? (dim == 2 ? 4 : 8) : (dim == 2 ? 2 : 4);
+}
+inline bool f64_of(int opt) { return opt == OPT_ADAM; }
 
 // ------------------------------------------------------------ kernel table
 
@@ -201,11 +211,11 @@ KernelInfo kinfo() {
 template <int DIM, bool W, int N>
 KernelInfo pick_opt(int opt) {
   switch (opt) {
+    case OPT_ADAM: return KernelInfo{step_kernel_f64<DIM, W, N>, 0, kBlock};
     case OPT_FD: return kinfo<DIM, OPT_FD, W, N>();
     case OPT_SGD: return kinfo<DIM, OPT_SGD, W, N>();
     case OPT_MOM: return kinfo<DIM, OPT_MOM, W, N>();
     case OPT_NEST: return kinfo<DIM, OPT_NEST, W, N>();
-    case OPT_ADAM: return kinfo<DIM, OPT_ADAM, W, N>();
     case OPT_ADADELTA: return kinfo<DIM, OPT_ADADELTA, W, N>();
     default: return kinfo<DIM, OPT_NONE, W, N>();
   }
@@ -235,7 +245,7 @@ int occupancy(ivhd_ctx* ctx, KernelInfo k) {
   if (it != ctx->occ.end()) return it->second;
   cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   int n = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, kThreads, k.smem) != cudaSuccess || n < 1) n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, k.threads, k.smem) != cudaSuccess || n < 1) n = 1;
   ctx->occ[k.fn] = n;
   return n;
 }
@@ -304,11 +314,15 @@ __global__ void k_d2f(const double* __restrict__ in, float* __restrict__ out, in
 // relabelled order: out[r] = y[perm[r]]; Nesterov look = y + beta*v
 __global__ void k_pack_positions(const double* __restrict__ y, int64_t m, int dim, int ys,
                                  const int32_t* __restrict__ perm, const float* __restrict__ vel,
-                                 int vel_stride, float beta, float* __restrict__ out) {
+                                 int vel_stride, float beta, float* __restrict__ out, int f64 = 0) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     float* o = out + i * ys;
     const int64_t src = perm[i];
+    if (f64) {  // fp64 layout (Adam): ys / 2 doubles per vertex
+      for (int d = 0; d < dim; ++d) reinterpret_cast<double*>(o)[d] = y[src * dim + d];
+      continue;
+    }
     const int look_off = (ys == 4 && dim == 2) ? 2 : 4;
     for (int d = 0; d < dim; ++d) {
       const float v = (float)y[src * dim + d];
@@ -320,11 +334,16 @@ __global__ void k_pack_positions(const double* __restrict__ y, int64_t m, int di
 
 // device layout (relabelled) -> double (m, dim) in caller order
 __global__ void k_unpack_positions(const float* __restrict__ in, int64_t m, int dim, int ys,
-                                   const int32_t* __restrict__ perm, double* __restrict__ y) {
+                                   const int32_t* __restrict__ perm, double* __restrict__ y, int f64 = 0) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t dst = perm[i];
-    for (int d = 0; d < dim; ++d) y[dst * dim + d] = (double)in[i * ys + d];
+    if (f64) {
+      const double* q = reinterpret_cast<const double*>(in + i * ys);
+      for (int d = 0; d < dim; ++d) y[dst * dim + d] = q[d];
+    } else {
+      for (int d = 0; d < dim; ++d) y[dst * dim + d] = (double)in[i * ys + d];
+    }
   }
 }
 
@@ -337,12 +356,21 @@ __global__ void k_unpermute_f64(const double* __restrict__ in, int64_t m, int di
 
 __global__ void k_deltas(const float* __restrict__ a, const float* __restrict__ b, int64_t m,
                          int dim, int ys, int commit, const int32_t* __restrict__ perm,
-                         double* __restrict__ out) {
+                         double* __restrict__ out, int f64 = 0) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t dst = perm[i];
-    for (int d = 0; d < dim; ++d)
-      out[dst * dim + d] = commit ? (double)a[i * ys + d] - (double)b[i * ys + d] : 0.0;
+    for (int d = 0; d < dim; ++d) {
+      double va, vb;
+      if (f64) {
+        va = reinterpret_cast<const double*>(a + i * ys)[d];
+        vb = reinterpret_cast<const double*>(b + i * ys)[d];
+      } else {
+        va = a[i * ys + d];
+        vb = b[i * ys + d];
+      }
+      out[dst * dim + d] = commit ? va - vb : 0.0;
+    }
   }
 }
 
@@ -379,6 +407,32 @@ __global__ void k_local_edges(const int32_t* __restrict__ src, const int32_t* __
   }
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// Sharded relabelling: deal the degree-sorted vertices (position p of
+// `sorted`) over the 8 rank groups of C ids in snake order (0..7, 7..0, ...),
+// so every group gets the same mix of hubs and leaves, i.e. equal edge
+// counts for equal vertex ranges.  Groups g < gfull hold C ids, group gfull
+// holds cap_p < C (the padded tail), later groups none: the first
+// (gfull + 1) * cap_p positions are dealt over gfull + 1 groups, the rest
+// over the gfull full ones.  Always 8 groups, so the order (and the fixed
+// tile reduction order) is the same for 1, 2, 4 and 8 ranks.
+__global__ void k_snake_deal(const int32_t* __restrict__ sorted, int64_t m, int64_t C, int gfull, int64_t cap_p,
+                             int32_t* __restrict__ out) {
+  const int64_t n1 = (int64_t)(gfull + 1) * cap_p;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g, idx;
+    if (p < n1) {
+      const int64_t n = gfull + 1, r = p / n, j = p % n;
+      g = (r & 1) ? n - 1 - j : j;
+      idx = r;
+    } else {
+      const int64_t q = p - n1, n = gfull, r = q / n, j = q % n;
+      g = (r & 1) ? n - 1 - j : j;
+      idx = cap_p + r;
+    }
+    out[g * C + idx] = sorted[p];
+  }
 }
 
 __global__ void k_inverse(const int32_t* __restrict__ perm, int64_t m, int32_t* __restrict__ inv) {
@@ -449,6 +503,21 @@ __global__ void k_tile_g(const uint32_t* __restrict__ rp, int64_t m, int n_tiles
       tile_g[t] = (uint8_t)G;
       tile_dm[t] = mx;  // unclamped: the slots-per-lane bound must cover hub rows
     }
+  }
+}
+
+// Sharded mode: fold this rank's work-unit partials into one partial per tile
+// (units of a tile in unit order), so the exchanged array is indexed by tile
+// and every rank owns the contiguous chunk of its tile range.
+__global__ void k_fold_tiles(const double4* __restrict__ unit_part, const int* __restrict__ unit_base, int t0,
+                             int t1, double4* __restrict__ tpart) {
+  for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
+    double4 s = make_double4(0, 0, 0, 0);
+    for (int u = unit_base[t]; u < unit_base[t + 1]; ++u) {
+      const double4 q = unit_part[u];
+      s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+    }
+    tpart[t] = s;
   }
 }
 
@@ -537,6 +606,7 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old, const int32_t* src, c
   ctx->window_order = window > 0 && window < m;
   uint32_t *deg = nullptr, *deg2 = nullptr;
   int32_t *ids = nullptr, *perm = nullptr;
+  float* big_scratch = nullptr;
   void* tmp = nullptr;
   size_t tb = 0;
   TRY(pull_ctrl(ctx));
@@ -570,11 +640,23 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old, const int32_t* src, c
       if ((e = dalloc(ctx, &tmp, std::max<size_t>(tb, 16))) != cudaSuccess) break;
       if ((e = cub::DeviceRadixSort::SortPairsDescending(tmp, tb, deg, deg2, ids, perm, (int)m, 0, 32, st)) !=
           cudaSuccess) break;
+      if (ctx->sharded) {  // equal-edge rank groups (k_snake_deal); ids stays the scratch
+        const int64_t C = (int64_t)(ctx->n_tiles_cap / 8) * ctx->tile_v;
+        const int gfull = (int)(m / C);
+        const int64_t cap_p = m - (int64_t)gfull * C;
+        k_snake_deal<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(perm, m, C, gfull, cap_p, ids);
+        if ((e = cudaGetLastError()) != cudaSuccess) break;
+        std::swap(ids, perm);
+      }
     }
     if (ctx->pos_set) {
       // data is currently in the old order (ctx->perm / ctx->inv): re-order
-      float* scratch = reinterpret_cast<float*>(ctx->stage);  // 32 bytes/vertex
       const int ys = ys_now(ctx), ss = ss_now(ctx);
+      float* scratch = reinterpret_cast<float*>(ctx->stage);  // 32 bytes/vertex
+      if (ss > 8) {  // fp64 Adam state in 3-D: 64 bytes/vertex
+        if ((e = dalloc(ctx, &big_scratch, sizeof(float) * ss * m)) != cudaSuccess) break;
+        scratch = big_scratch;
+      }
       float* y = ctx->ybuf[ctx->ctrl_h->cur];
       k_permute_rows<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(y, m, ys, perm, ctx->inv, scratch);
       if ((e = cudaMemcpyAsync(y, scratch, sizeof(float) * ys * m, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
@@ -589,7 +671,7 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old, const int32_t* src, c
     k_inverse<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ctx->perm, m, ctx->inv);
     e = cudaStreamSynchronize(st);
   } while (0);
-  dfree(ctx, deg); dfree(ctx, deg2); dfree(ctx, ids); dfree(ctx, perm); dfree(ctx, tmp);
+  dfree(ctx, deg); dfree(ctx, deg2); dfree(ctx, ids); dfree(ctx, perm); dfree(ctx, tmp); dfree(ctx, big_scratch);
   if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "vertex relabelling: %s", cudaGetErrorString(e));
   ctx->perm_fixed = true;
   return IVHD_OK;
@@ -694,6 +776,10 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
     if ((e = dalloc(ctx, &S.units, sizeof(int) * units.size())) != cudaSuccess) break;
     if ((e = cudaMemcpyAsync(S.units, units.data(), sizeof(int) * units.size(), cudaMemcpyHostToDevice, st)) !=
         cudaSuccess) break;
+    if (S.d_unit_base == nullptr &&
+        (e = dalloc(ctx, &S.d_unit_base, sizeof(int) * (ctx->n_tiles_cap + 1))) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(S.d_unit_base, S.unit_base.data(), sizeof(int) * (ctx->n_tiles_cap + 1),
+                             cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
     e = cudaStreamSynchronize(st);
   } while (0);
   dfree(ctx, keys); dfree(ctx, keys2); dfree(ctx, vals); dfree(ctx, vals2); dfree(ctx, rp_old); dfree(ctx, deg);
@@ -776,6 +862,8 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   A.ybuf1 = ctx->ybuf[1];
   A.state = ctx->state;
   A.partial = ctx->partial;
+  A.tpart = ctx->tpart;
+  A.unit_base = S.d_unit_base;
   A.bpart = ctx->bpart;
   A.trace = ctx->trace;
   A.ctrl = ctx->ctrl;
@@ -794,7 +882,9 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
     const int t0 = (int)(ctx->shard_begin / ctx->tile_v), t1 = (int)(ctx->shard_end / ctx->tile_v);
     A.tile0 = S.unit_base[t0];
     A.n_tiles = S.unit_base[t1] - S.unit_base[t0];
-    A.n_tiles_global = S.n_units;
+    A.n_tiles_global = ctx->n_tiles_cap;  // the finalizer reduces the exchanged tile partials
+    A.v_begin = ctx->shard_begin;
+    A.v_end = std::min<int64_t>(ctx->shard_end, ctx->m);
   } else {
     A.tile0 = 0;
     A.n_tiles = S.unit_base[ctx->n_tiles];
@@ -810,7 +900,7 @@ int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
   // (griddepcontrol.wait) before reading positions, state or ctrl.
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(k.threads);
   cfg.dynamicSmemBytes = k.smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute at[1];
@@ -852,7 +942,8 @@ int ys_now(ivhd_ctx* ctx) { return ys_of(ctx->dim, ctx->opt.kind); }
 
 int ss_now(ivhd_ctx* ctx) {
   const int k = ctx->opt.kind;
-  const int nv = (k == OPT_FD || k == OPT_MOM || k == OPT_NEST) ? 1 : (k == OPT_ADAM || k == OPT_ADADELTA) ? 2 : 0;
+  if (k == OPT_ADAM) return ctx->dim == 2 ? 8 : 16;  // fp64 {v, s}
+  const int nv = (k == OPT_FD || k == OPT_MOM || k == OPT_NEST) ? 1 : (k == OPT_ADADELTA) ? 2 : 0;
   return nv == 0 ? 0 : (ctx->dim == 2 ? 2 * nv : 4 * nv);
 }
 
@@ -938,6 +1029,7 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   alloc((void**)&ctx->ybuf[1], sizeof(float) * 8 * vc);
   alloc((void**)&ctx->state, sizeof(float) * 8 * vc);
   alloc((void**)&ctx->partial, sizeof(double4) * 32 * ctx->n_tiles_cap);  // <= 32 units per tile
+  alloc((void**)&ctx->tpart, sizeof(double4) * ctx->n_tiles_cap);
   alloc((void**)&ctx->bpart, sizeof(double4) * 8 * ctx->sm_count);  // <= 2048/288 blocks per SM
   alloc((void**)&ctx->ctrl, sizeof(Ctrl));
   alloc((void**)&ctx->opctrl, sizeof(Ctrl));
@@ -981,10 +1073,10 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   drop_graphs(ctx);
   for (auto& s : ctx->slots) {
     dfree(ctx, s.row_ptr); dfree(ctx, s.col); dfree(ctx, s.ew); dfree(ctx, s.tile_g); dfree(ctx, s.tile_dm); dfree(ctx, s.units);
-    dfree(ctx, s.sched_units); dfree(ctx, s.sched_off);
+    dfree(ctx, s.sched_units); dfree(ctx, s.sched_off); dfree(ctx, s.d_unit_base);
   }
   dfree(ctx, ctx->perm); dfree(ctx, ctx->inv);
-  dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial); dfree(ctx, ctx->bpart);
+  dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial); dfree(ctx, ctx->tpart); dfree(ctx, ctx->bpart);
   dfree(ctx, ctx->trace); dfree(ctx, ctx->ctrl); dfree(ctx, ctx->opctrl); dfree(ctx, ctx->red_out);
   dfree(ctx, ctx->stage); dfree(ctx, ctx->op_y); dfree(ctx, ctx->op_force);
   dfree(ctx, ctx->snap_y); dfree(ctx, ctx->snap_state);
@@ -1101,7 +1193,7 @@ int ivhd_init_positions(ivhd_ctx* ctx, uint64_t* rng, double lo, double hi) {
   const bool nest = ctx->opt.kind == IVHD_OPT_NESTEROV;
   k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
       ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
-      (float)ctx->hyper.beta, ctx->ybuf[ctx->ctrl_h->cur]);
+      (float)ctx->hyper.beta, ctx->ybuf[ctx->ctrl_h->cur], f64_of(ctx->opt.kind));
   CU(ctx, cudaGetLastError());
   ctx->ctrl_h->status = 0;
   ctx->ctrl_h->last_commit = 0;
@@ -1309,7 +1401,7 @@ int ivhd_set_positions(ivhd_ctx* ctx, const double* y) {
   float* dst = ctx->ybuf[ctx->ctrl_h->cur];
   k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
       ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
-      (float)ctx->hyper.beta, dst);
+      (float)ctx->hyper.beta, dst, f64_of(ctx->opt.kind));
   CU(ctx, cudaGetLastError());
   ctx->ctrl_h->status = 0;
   ctx->ctrl_h->last_commit = 0;
@@ -1325,7 +1417,7 @@ int ivhd_get_positions(ivhd_ctx* ctx, double* y_out) {
   TRY(pull_ctrl(ctx));
   const int ys = ys_of(ctx->dim, ctx->opt.kind);
   k_unpack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-      ctx->ybuf[ctx->ctrl_h->cur], ctx->m, ctx->dim, ys, ctx->perm, ctx->stage);
+      ctx->ybuf[ctx->ctrl_h->cur], ctx->m, ctx->dim, ys, ctx->perm, ctx->stage, f64_of(ctx->opt.kind));
   CU(ctx, cudaGetLastError());
   CU(ctx, cudaMemcpyAsync(y_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim, cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -1341,7 +1433,7 @@ int ivhd_get_deltas(ivhd_ctx* ctx, double* d_out) {
   const int cur = ctx->ctrl_h->cur;
   k_deltas<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
       ctx->ybuf[cur], ctx->ybuf[cur ^ 1], ctx->m, ctx->dim, ys, ctx->ctrl_h->last_commit, ctx->perm,
-      ctx->stage);
+      ctx->stage, f64_of(ctx->opt.kind));
   CU(ctx, cudaGetLastError());
   CU(ctx, cudaMemcpyAsync(d_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim, cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -1356,18 +1448,33 @@ int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p) {
   TRY(pull_ctrl(ctx));
   const int old_ys = ys_of(ctx->dim, ctx->opt.kind);
   const int new_ys = ys_of(ctx->dim, p->kind);
-  if (ctx->pos_set && old_ys != new_ys) {
+  const int old_f64 = f64_of(ctx->opt.kind), new_f64 = f64_of(p->kind);
+  // fp64 Adam state in 3-D: 8 doubles per vertex (16 floats)
+  const int need_fpv = (new_f64 && ctx->dim == 3) ? 16 : 8;
+  if (need_fpv > ctx->state_fpv) {
+    float* ns = nullptr;
+    CU(ctx, dalloc(ctx, &ns, sizeof(float) * need_fpv * ctx->v_cap));
+    dfree(ctx, ctx->state);
+    dfree(ctx, ctx->snap_state);
+    ctx->snap_state = nullptr;
+    ctx->snap_valid = false;
+    ctx->state = ns;
+    ctx->state_fpv = need_fpv;
+    drop_graphs(ctx);
+  }
+  if (ctx->pos_set && (old_ys != new_ys || old_f64 != new_f64)) {
     // re-pack the current positions for the new layout (velocity starts at 0)
     float* cur = ctx->ybuf[ctx->ctrl_h->cur];
     k_unpack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(cur, ctx->m, ctx->dim,
-                                                                                old_ys, ctx->perm, ctx->stage);
-    CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * 8 * ctx->v_cap, ctx->stream));
+                                                                                old_ys, ctx->perm, ctx->stage,
+                                                                                old_f64);
+    CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * ctx->state_fpv * ctx->v_cap, ctx->stream));
     k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
         ctx->stage, ctx->m, ctx->dim, new_ys, ctx->perm, p->kind == IVHD_OPT_NESTEROV ? ctx->state : nullptr,
-        vel_stride(ctx->dim), (float)p->beta, cur);
+        vel_stride(ctx->dim), (float)p->beta, cur, new_f64);
     CU(ctx, cudaGetLastError());
   }
-  CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * 8 * ctx->v_cap, ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * ctx->state_fpv * ctx->v_cap, ctx->stream));
   ctx->opt = *p;
   ctx->opt_set = true;
   Hyper h{};
@@ -1381,6 +1488,9 @@ int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p) {
   h.gs = (float)p->gamma_s;
   h.rho = (float)p->rho;
   h.eps = (float)p->eps;
+  h.gv_d = p->gamma_v;
+  h.gs_d = p->gamma_s;
+  h.eps_d = p->eps;
   ctx->hyper = h;
   ctx->ctrl_h->step = p->step;
   ctx->ctrl_h->adam_t = 0;
@@ -1558,11 +1668,12 @@ int ivhd_snapshot(ivhd_ctx* ctx) {
   CU(ctx, cudaSetDevice(ctx->device));
   const size_t bytes = sizeof(float) * 8 * ctx->v_cap;
   if (!ctx->snap_y) CU(ctx, dalloc(ctx, &ctx->snap_y, bytes));
-  if (!ctx->snap_state) CU(ctx, dalloc(ctx, &ctx->snap_state, bytes));
+  if (!ctx->snap_state) CU(ctx, dalloc(ctx, &ctx->snap_state, sizeof(float) * ctx->state_fpv * ctx->v_cap));
   TRY(pull_ctrl(ctx));
   const size_t used = sizeof(float) * 8 * ctx->m;
   CU(ctx, cudaMemcpyAsync(ctx->snap_y, ctx->ybuf[ctx->ctrl_h->cur], used, cudaMemcpyDeviceToDevice, ctx->stream));
-  CU(ctx, cudaMemcpyAsync(ctx->snap_state, ctx->state, used, cudaMemcpyDeviceToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->snap_state, ctx->state, sizeof(float) * ctx->state_fpv * ctx->m,
+                          cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->snap_ctrl = *ctx->ctrl_h;
   ctx->snap_valid = true;
   CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1576,7 +1687,8 @@ int ivhd_restore(ivhd_ctx* ctx) {
   const size_t used = sizeof(float) * 8 * ctx->m;
   *ctx->ctrl_h = ctx->snap_ctrl;
   CU(ctx, cudaMemcpyAsync(ctx->ybuf[ctx->snap_ctrl.cur], ctx->snap_y, used, cudaMemcpyDeviceToDevice, ctx->stream));
-  CU(ctx, cudaMemcpyAsync(ctx->state, ctx->snap_state, used, cudaMemcpyDeviceToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->state, ctx->snap_state, sizeof(float) * ctx->state_fpv * ctx->m,
+                          cudaMemcpyDeviceToDevice, ctx->stream));
   TRY(push_ctrl(ctx));
   return IVHD_OK;  // asynchronous: ordered before the next launch on the stream
 }
@@ -1596,6 +1708,15 @@ int ivhd_synchronize(ivhd_ctx* ctx) {
 
 // ------------------------------------------------------------ sharded mode
 
+// unit partials of this rank's tiles -> tile partials (the fp64 kernel writes tiles directly)
+static int fold_tiles(ivhd_ctx* ctx, const CsrSlot& S) {
+  if (f64_of(ctx->opt.kind)) return IVHD_OK;
+  const int t0 = (int)(ctx->shard_begin / ctx->tile_v), t1 = (int)(ctx->shard_end / ctx->tile_v);
+  if (t1 > t0) k_fold_tiles<<<(t1 - t0 + 255) / 256, 256, 0, ctx->stream>>>(ctx->partial, S.d_unit_base, t0, t1, ctx->tpart);
+  CU(ctx, cudaGetLastError());
+  return IVHD_OK;
+}
+
 int ivhd_tile_vertices(ivhd_ctx* ctx, int64_t* tile_v_out, int64_t* n_tiles_out) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
   if (tile_v_out) *tile_v_out = ctx->tile_v;
@@ -1613,6 +1734,7 @@ int ivhd_shard_set_range(ivhd_ctx* ctx, int64_t v_begin, int64_t v_end) {
   ctx->sharded = true;
   CU(ctx, cudaSetDevice(ctx->device));
   CU(ctx, cudaMemsetAsync(ctx->partial, 0, sizeof(double4) * 32 * ctx->n_tiles_cap, ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->tpart, 0, sizeof(double4) * ctx->n_tiles_cap, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   return IVHD_OK;
 }
@@ -1624,7 +1746,7 @@ int ivhd_shard_buffers(ivhd_ctx* ctx, uint64_t* ybuf0, uint64_t* ybuf1, int64_t*
   if (ybuf0) *ybuf0 = reinterpret_cast<uint64_t>(ctx->ybuf[0]);
   if (ybuf1) *ybuf1 = reinterpret_cast<uint64_t>(ctx->ybuf[1]);
   if (floats_per_vertex) *floats_per_vertex = ys_of(ctx->dim, ctx->opt.kind);
-  if (partials) *partials = reinterpret_cast<uint64_t>(ctx->partial);
+  if (partials) *partials = reinterpret_cast<uint64_t>(ctx->tpart);
   if (cur_out) *cur_out = ctx->ctrl_h->cur;
   return IVHD_OK;
 }
@@ -1644,6 +1766,7 @@ int ivhd_step_local(ivhd_ctx* ctx, int slot, int norm, double c) {
   StepArgs A = make_args(ctx, slot, norm, 0);
   const CsrSlot& S = ctx->slots[slot];
   if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
+  TRY(fold_tiles(ctx, S));
   ctx->shard_slot = slot;
   return IVHD_OK;
 }
@@ -1707,6 +1830,7 @@ int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out) {
   shard_io(ctx, A);
   const CsrSlot& S = ctx->slots[slot];
   if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
+  TRY(fold_tiles(ctx, S));
   ctx->shard_slot = slot;
   if (exchange_out) *exchange_out = reinterpret_cast<uint64_t>(ctx->ybuf[ctx->shard_cur ^ 1]);
   return IVHD_OK;

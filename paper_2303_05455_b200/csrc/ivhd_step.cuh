@@ -100,6 +100,7 @@ struct Hyper {
   float beta, gv, gs, rho, eps;
   double g1, g2;         // step-size factors: b is kept in fp64 like the reference
   double tau;
+  double gv_d, gs_d, eps_d;  // Adam moments in fp64 (ivhd_step_f64.cuh)
   int adapt;
 };
 
@@ -110,7 +111,9 @@ struct StepArgs {
   float* ybuf0;
   float* ybuf1;
   float* state;
-  double4* partial;
+  double4* partial;       // per work unit (sharded / operator calls)
+  double4* tpart;         // per tile: sharded mode's exchanged partials
+  const int* unit_base;   // first unit of each tile
   double4* bpart;         // fused mode: one partial per block (its units, in order)
   double2* trace;
   Ctrl* ctrl;
@@ -1111,7 +1114,7 @@ template <int OPT>
 __global__ void __launch_bounds__(kBlock) finalize_kernel(StepArgs A) {
   __shared__ double4 sm_red[kBlock / 32];
   if (A.ctrl->status != 0) return;
-  finalize_block<OPT>(A, sm_red, A.partial, A.n_tiles_global);
+  finalize_block<OPT>(A, sm_red, A.tpart, A.n_tiles_global);
   if (!A.fixed_io) return;
   // async sharded mode: the buffer just written becomes current; after a
   // rollback (rare) it is refilled with the unchanged positions

@@ -189,7 +189,7 @@ def _phase_name(rnn_on, l1_on):
 class _Session:
     """Setup of one run (engine.py:162-221) with the particle system on the GPU."""
 
-    def __init__(self, graph, config, dataset, helper_graph, device):
+    def __init__(self, graph, config, dataset, helper_graph, device, make_device=None):
         self.config = config
         self.rng = np.random.default_rng(config.seed)
         self.data = None if dataset is None else np.asarray(dataset.data, dtype=np.float64)
@@ -242,7 +242,8 @@ class _Session:
         if m <= self.nn_sets.shape[1] + config.rn:
             raise InvalidArgumentError(f"M={m} too small for nn={self.nn_sets.shape[1]} plus rn={config.rn}")
 
-        self.dev = DeviceEmbedding(m, config.target_dim, device=device)
+        # one GPU (DeviceEmbedding) or this rank's shard (sharded.ShardedEmbedding)
+        self.dev = (make_device or DeviceEmbedding)(m, config.target_dim, device=device)
         self.dev.set_optimizer(resolve_optimizer(config.optimizer, m, config.integrator, config.opt))
         # one PCG64 stream, reference order (engine.py:165, 214-215): the
         # layout, then the random partners — drawn on the device (numpy's
@@ -438,6 +439,12 @@ def run_embedding(graph=None, config=None, dataset=None, helper_graph=None, obse
     del threads
     config = coerce_config(config)
     sess = _Session(graph, config, dataset, helper_graph, device)
+    return _drive(sess, config, observer)
+
+
+def _drive(sess, config, observer):
+    """The loop of engine.py:331-414 over device segments (shared by
+    run_embedding and sharded.run_embedding_distributed)."""
     dev = sess.dev
     total = config.iterations
     trace = StressTrace()

@@ -107,27 +107,17 @@ class ShardedEmbedding:
         self.v0, self.v1 = self.ranges[self.rank]
         backend.shard_set_range(self.v0, self.v1)
 
-    # set-up: identical on every rank (same graph, same seeded draws)
-    def set_graph(self, slot, nn_sets, rn_assign):
-        self.backend.set_graph(slot, nn_sets, rn_assign)
+    # set-up (graph, draws, optimizer, positions, read-back) is identical on
+    # every rank: delegated to the rank's DeviceEmbedding
+    def __getattr__(self, name):
+        if name == "backend":
+            raise AttributeError(name)
+        return getattr(self.backend, name)
 
-    def set_connections(self, *a, **k):
-        self.backend.set_connections(*a, **k)
-
-    def set_positions(self, y):
-        self.backend.set_positions(y)
-
-    def set_optimizer(self, params):
-        self.backend.set_optimizer(params)
-
-    def positions(self):
-        return self.backend.positions()
-
-    def snapshot(self):
-        self.backend.snapshot()
-
-    def restore(self):
-        self.backend.restore()
+    def launches_per_iteration(self):
+        """Kernels per iteration: local update, tile fold, finalizer (NCCL's
+        all-gathers come on top)."""
+        return 3
 
     def step(self, slot, norm, c):
         """One synchronous iteration: local update, exchange, fixed-order
@@ -207,3 +197,32 @@ class ShardedEmbedding:
                 for _ in range(chunk):
                     self._iteration(slot, norm)
         return g
+
+
+def run_embedding_distributed(graph=None, config=None, dataset=None, helper_graph=None, group=None,
+                              device=None):
+    """`run_embedding` (engine.py:312-414) across the ranks of a
+    torch.distributed process group, one GPU per rank: every rank calls it
+    with the same graph and config and gets the same RunResult (the full
+    embedding is replicated on every rank).  Observers are not supported
+    here (the steering server drives one GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    from .config import coerce_config
+    from .embed import _drive, _Session
+
+    config = coerce_config(config)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if device is None:
+        device = torch.cuda.current_device()
+    stream = torch.cuda.current_stream(device)
+    if stream.cuda_stream == 0:  # graph capture needs a real stream
+        stream = torch.cuda.Stream(device=device)
+
+    def make(m, dim, device=device):
+        return ShardedEmbedding(m, dim, rank, world, device=device, stream=stream.cuda_stream, group=group)
+
+    with torch.cuda.stream(stream):
+        sess = _Session(graph, config, dataset, helper_graph, device, make_device=make)
+        return _drive(sess, config, None)

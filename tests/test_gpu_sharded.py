@@ -1,0 +1,127 @@
+"""The sharded (multi-GPU) loop's device side on one B200.
+
+Two "ranks" live in one process as two library contexts with the real
+per-unit partials, the tile fold (k_fold_tiles) and the fixed-order
+finalizer; the exchange that NCCL performs between GPUs (the all-gather of
+the position slices and of the tile partials) is done here by device
+copies between the contexts, in the same order (all ranks step, exchange,
+all ranks finalize).  The graph has hubs, so tiles with G > 1 lanes per
+vertex split into several work units (units != tiles) — the case whose
+partials round 1 exchanged from the wrong indices.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.ivhd_oracle import OracleRun
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2303_05455_b200")
+
+
+def normwise(a, b):
+    return float(np.abs(np.asarray(a) - b).max() / np.abs(b).max())
+
+
+def hub_graph(m=20000, k=3, seed=0):
+    rng = np.random.default_rng(seed)
+    nb = (np.arange(m)[:, None] + rng.integers(1, 200, size=(m, k))) % m
+    hubs = rng.choice(m, size=12, replace=False)
+    rows = rng.choice(m, size=m // 5, replace=False)
+    nb[rows, 0] = hubs[rng.integers(0, len(hubs), size=len(rows))]  # in-degree ~330 per hub
+    nb[nb == np.arange(m)[:, None]] = (nb[nb == np.arange(m)[:, None]] + 1) % m
+    return nb.astype(np.int32)
+
+
+def _setup(nb, world, rank, stream, optimizer="force-directed", iters=12, integrator=None):
+    from paper_2303_05455_b200.config import resolve_optimizer
+    from paper_2303_05455_b200.sharded import ShardedEmbedding
+
+    m = nb.shape[0]
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer=optimizer, integrator=integrator)
+    sh = ShardedEmbedding(m, 2, rank, world, device=0, stream=stream.cuda_stream)
+    sh.set_optimizer(resolve_optimizer(optimizer, m, integrator=integrator and P.IntegratorParams(**integrator)))
+    sh.set_positions(orc.Y)
+    sh.set_graph(0, nb[:, :3], orc.rn_assign)
+    return sh, orc
+
+
+def _emulated(nb, world, iters, **kw):
+    """world contexts on one GPU; returns per-rank (positions, stress, b)."""
+    from paper_2303_05455_b200.sharded import _CudaArray
+
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ranks = [_setup(nb, world, r, stream, iters=iters, **kw)[0] for r in range(world)]
+        tile_v, n_tiles = ranks[0].backend.tiles()
+        fpv = ranks[0].backend.shard_buffers()["floats_per_vertex"]
+        for sh in ranks:
+            sh.backend.shard_begin(0, 0.1, iters)
+        for _ in range(iters):
+            views = []
+            for sh in ranks:
+                yptr = sh.backend.shard_step(0, "l2")
+                b = sh.backend.shard_buffers()
+                y = torch.as_tensor(_CudaArray(yptr, n_tiles * tile_v * fpv, "<f4"), device="cuda")
+                p = torch.as_tensor(_CudaArray(b["partials"], n_tiles * 4, "<f8"), device="cuda")
+                views.append((y, p))
+            # all-gather: rank q's chunk of every exchanged array goes to every rank
+            for q, sh in enumerate(ranks):
+                yc = slice(sh.v0 * fpv, sh.v1 * fpv)
+                pc = slice(sh.v0 // tile_v * 4, sh.v1 // tile_v * 4)
+                for r in range(world):
+                    if r != q:
+                        views[r][0][yc].copy_(views[q][0][yc])
+                        views[r][1][pc].copy_(views[q][1][pc])
+            for sh in ranks:
+                sh.backend.shard_finalize()
+        out = []
+        for sh in ranks:
+            st, bb, done, div = sh.backend.shard_end()
+            assert done == iters and not div
+            out.append((sh.positions(), st, bb))
+        stream.synchronize()
+        for sh in ranks:
+            sh.close()
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_emulated_ranks_match_one_rank_and_oracle(world):
+    nb = hub_graph()
+    iters = 12
+    one = _emulated(nb, 1, iters)[0]
+    many = _emulated(nb, world, iters)
+    for y, st, bb in many:  # every rank holds the same state ...
+        np.testing.assert_array_equal(y, many[0][0])
+        np.testing.assert_array_equal(st, many[0][1])
+    # ... bit-identical to one rank (tile partials in fixed tile order)
+    np.testing.assert_array_equal(many[0][0], one[0])
+    np.testing.assert_array_equal(many[0][1], one[1])
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0)
+    orc.run()
+    assert normwise(many[0][0], orc.Y) < 1e-5
+    np.testing.assert_allclose(many[0][1], orc.trace_stress, rtol=1e-5)
+    np.testing.assert_allclose(many[0][2], orc.trace_b, rtol=0)
+
+
+def test_emulated_ranks_rollbacks_and_adam():
+    nb = hub_graph(seed=1)
+    iters = 10
+    integ = {"b": 0.5, "tau": 1e-6}
+    many = _emulated(nb, 2, iters, integrator=integ)
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, integrator=integ)
+    orc.run()
+    b = np.asarray(orc.trace_b)
+    assert (b[1:] != b[:-1]).sum() >= 3, "expected auto-adapt rollbacks"
+    np.testing.assert_array_equal(many[0][0], many[1][0])
+    np.testing.assert_allclose(many[0][2], b, rtol=0)
+    assert normwise(many[0][0], orc.Y) < 1e-5
+    # float64 Adam kernel writes tile partials directly
+    many = _emulated(nb, 2, iters, optimizer="adam")
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer="adam")
+    orc.run()
+    np.testing.assert_array_equal(many[0][0], many[1][0])
+    assert normwise(many[0][0], orc.Y) < 1e-5

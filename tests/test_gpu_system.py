@@ -82,7 +82,9 @@ def test_sharded_async_loop_rollback_and_divergence(integ, iters, diverges):
     from paper_2303_05455_b200.embed import init_layout, sample_random_neighbors
     from paper_2303_05455_b200.sharded import ShardedEmbedding
 
-    nb = _problem(3000)
+    # 6000 ids: an id-local input, so the sharded and the fused loop use the
+    # same (windowed) vertex order and agree bit for bit even while blowing up
+    nb = _problem(6000)
     m = nb.shape[0]
     rng = np.random.default_rng(2)
     y0 = init_layout(m, 2, rng)
@@ -333,3 +335,30 @@ def test_pinned_pool_cap_releases_pooled_buffers():
     e[...] = 1.0
     c[...] = 2.0
     assert float(e.sum()) == e.size and float(c.sum()) == 2 * c.size
+
+
+def test_run_embedding_distributed_world1_matches_run_embedding():
+    """The public multi-GPU entry point (sharded.run_embedding_distributed) on
+    a one-rank NCCL group: same RunResult contract and trajectory as
+    run_embedding on a hub-heavy mixture kNN graph (snake-dealt rank groups:
+    a different vertex order, so equal to fp32 summation order)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_05455_b200 import synth
+    from paper_2303_05455_b200.sharded import run_embedding_distributed
+
+    nb, _, _ = synth.mixture_knn_graph(30000, 50, k=3, seed=3, spread=0.5)
+    cfg = P.EmbeddingConfig(nn=3, rn=1, c=0.1, iterations=50, seed=5)
+    a = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        b = run_embedding_distributed(graph=P.KnnGraph(nb), config=cfg)
+    finally:
+        dist.destroy_process_group()
+    assert b.state.iteration == 50 and len(b.trace.stress) == 50
+    assert np.abs(b.embedding.points - a.embedding.points).max() / np.abs(a.embedding.points).max() < 1e-5
+    np.testing.assert_allclose(b.trace.stress, a.trace.stress, rtol=1e-5)
+    assert b.trace.step_size == a.trace.step_size
+    np.testing.assert_array_equal(b.state.rn_assignments, a.state.rn_assignments)

@@ -8,13 +8,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2303_05455_b200 import EmbeddingConfig, KnnGraph, run_embedding, metrics, synth
 
 m = int(os.environ.get("M", 1_400_000))
+n = int(os.environ.get("N", 100))
+c = float(os.environ.get("C", 0.1))
+iters = int(os.environ.get("ITERS", 2500))
 spreads = [float(s) for s in os.environ.get("SPREADS", "0.25,0.35,0.5,0.7,1.0").split(",")]
 os.makedirs("gpurun_out", exist_ok=True)
 for sp in spreads:
     t0 = time.perf_counter()
-    nb, dist, labels = synth.mixture_knn_graph(m, 100, k=2, seed=0, spread=sp)
+    nb, dist, labels = synth.mixture_knn_graph(m, n, k=2, seed=0, spread=sp)
     tk = time.perf_counter() - t0
-    cfg = EmbeddingConfig(nn=2, rn=1, c=0.1, iterations=2500, seed=0)
+    cfg = EmbeddingConfig(nn=2, rn=1, c=c, iterations=iters, seed=0)
     t0 = time.perf_counter()
     res = run_embedding(graph=KnnGraph(nb), config=cfg)
     te = time.perf_counter() - t0
@@ -24,4 +27,4 @@ for sp in spreads:
     print(f"spread {sp}: knn {tk:.1f}s embed {te:.2f}s stress {res.state.stress:.2f} "
           f"cf_2 {cf_nn[1]:.4f} cf_10 {cf_nn[9]:.4f} cf {cf:.4f} graph-nn1-label-agree {g_hit:.4f}", flush=True)
     if os.environ.get("SAVE"):
-        np.savez_compressed(f"gpurun_out/c3_graph_spread{sp}.npz", neighbors=nb)
+        np.savez_compressed(f"gpurun_out/graph_m{m}_n{n}_spread{sp}.npz", neighbors=nb)
