@@ -25,6 +25,7 @@
  *   ivhd_get_deltas                 EmbeddingState.deltas            engine.py:379
  *   ivhd_snapshot / ivhd_restore    (new) device-side checkpoint     SURVEY.md §5 checkpoint row
  *   ivhd_shard_* / ivhd_step_*      (new) vertex-range sharding
+ *   ivhd_peer_*                     (new) fused NVLink P2P exchange
  *   ivhd_knn_build                  knng.build_exact_knn             knng.py:158-194
  *                                   (euclidean / cosine)
  *   ivhd_neighbor_hit               metrics.neighbor_hit (points)    metrics.py:254-294
@@ -44,14 +45,15 @@
 extern "C" {
 #endif
 
-#define IVHD_ABI_VERSION 2
+#define IVHD_ABI_VERSION 3
 
 enum ivhd_status {
   IVHD_OK = 0,
   IVHD_ERR_INVALID_ARG = 1, /* -> InvalidArgumentError / DimensionMismatchError */
   IVHD_ERR_CUDA = 2,        /* CUDA runtime failure (message has the CUDA error) */
   IVHD_ERR_DIVERGED = 3,    /* -> NumericalDivergenceError(iteration, state)    */
-  IVHD_ERR_STATE = 4        /* call order violated (e.g. run before set_graph)  */
+  IVHD_ERR_STATE = 4,       /* call order violated (e.g. run before set_graph)  */
+  IVHD_ERR_PEER = 5         /* peer exchange: a rank did not arrive in time      */
 };
 
 enum ivhd_norm { IVHD_NORM_L2 = 0, IVHD_NORM_L1 = 1 };
@@ -183,6 +185,30 @@ int ivhd_shard_begin(ivhd_ctx* ctx, int slot, double c, int64_t n_iter, int* cur
 int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out);
 int ivhd_shard_finalize(ivhd_ctx* ctx);
 int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out);
+
+/* Fused peer exchange over NVLink (sharded mode, one process per GPU on one
+ * node, up to 8 ranks).  Replaces the per-iteration NCCL
+ * all-gather: the step kernel stores every updated position straight into
+ * each peer's replica and its tile partials into each peer's partial array
+ * (P2P stores overlap the update tile by tile), raises its arrival flag on
+ * every rank, and a one-block finalizer waits for all ranks' flags and takes
+ * the same decision on every rank.  Set-up, after ivhd_shard_set_range:
+ *   ivhd_peer_export(ctx, world, rank, h)   moves the exchanged buffers to
+ *       cudaMalloc memory and writes their CUDA IPC handles
+ *       (IVHD_PEER_HANDLE_BYTES bytes) into h;
+ *   every rank gathers all handles in rank order (e.g. all_gather_object);
+ *   ivhd_peer_import(ctx, all)              opens the peers' buffers.
+ * In-process (several contexts of one process, tests): ivhd_peer_export on
+ * each, then ivhd_peer_import_local(ctx, ctxs) with the contexts in rank order.
+ * Afterwards ivhd_run drives the whole exchange on the device (CUDA graphs of
+ * step + finalizer launches, no host work per iteration); ivhd_shard_step /
+ * ivhd_shard_finalize launch the two kernels one at a time (the in-process
+ * emulation interleaves them over ranks).  A rank that does not arrive within
+ * 10 s makes the others fail with IVHD_ERR_PEER instead of hanging. */
+#define IVHD_PEER_HANDLE_BYTES 256
+int ivhd_peer_export(ivhd_ctx* ctx, int world, int rank, uint8_t* handle_out);
+int ivhd_peer_import(ivhd_ctx* ctx, const uint8_t* all_handles);
+int ivhd_peer_import_local(ivhd_ctx* ctx, ivhd_ctx* const* ctxs);
 
 /* Exact kNN graph of the rows of a host (m, n) float64 matrix, computed on
  * `device` (knng.build_exact_knn, knng.py:158-194): row i lists its k nearest

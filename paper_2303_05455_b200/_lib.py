@@ -16,11 +16,12 @@ from .errors import DeviceError, IvhdError, InvalidArgumentError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("IVHD_B200_LIB", os.path.join(HERE, "libivhd_b200.so"))
 
-OK, ERR_INVALID_ARG, ERR_CUDA, ERR_DIVERGED, ERR_STATE = range(5)
+OK, ERR_INVALID_ARG, ERR_CUDA, ERR_DIVERGED, ERR_STATE, ERR_PEER = range(6)
+PEER_HANDLE_BYTES = 256
 NORM = {"l2": 0, "l1": 1}
 OPT_KIND = {"force-directed": 0, "sgd": 1, "momentum": 2, "nesterov": 3, "adam": 4, "adadelta": 5}
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 c_i32p = ctypes.POINTER(ctypes.c_int32)
 c_f64p = ctypes.POINTER(ctypes.c_double)
 c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -57,6 +58,9 @@ SIGNATURES = {
     "ivhd_shard_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_u64p]),
     "ivhd_shard_finalize": (ctypes.c_int, [ctypes.c_void_p]),
     "ivhd_shard_end": (ctypes.c_int, [ctypes.c_void_p, c_f64p, c_f64p, c_i64p]),
+    "ivhd_peer_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_u8p]),
+    "ivhd_peer_import": (ctypes.c_int, [ctypes.c_void_p, c_u8p]),
+    "ivhd_peer_import_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "ivhd_set_connections": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, c_u8p, c_f64p,
                                             c_f64p, ctypes.c_int64]),
     "ivhd_set_positions": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),

@@ -119,6 +119,16 @@ struct ivhd_ctx {
   int shard_slot = 0;   // connection slot of the last ivhd_shard_step
   int64_t graph_epoch = 0;  // bumped whenever captured launch arguments go stale
 
+  // fused peer exchange (ivhd_peer_*): buffers peers write into are cudaMalloc'd (IPC)
+  bool peer_on = false;
+  int world = 1, rank = 0;
+  bool ybuf_malloc = false;            // ybuf[0..1] are cudaMalloc (not pool) memory
+  double4* tp2 = nullptr;              // [2][n_tiles_cap] tile partials by stamp parity
+  unsigned long long* flags = nullptr; // [8] arrival flags, one slot per rank
+  unsigned long long* stamp = nullptr; // iterations exchanged
+  PeerArgs pe{};
+  std::vector<void*> ipc_opened;       // cudaIpcOpenMemHandle pointers to close
+
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int graph_chunk = 64;
 
@@ -230,6 +240,14 @@ KernelInfo pick_norm(int opt, int norm) {
 KernelInfo pick_kernel(int dim, int opt, bool weighted, int norm) {
   if (dim == 2) return weighted ? pick_norm<2, true>(opt, norm) : pick_norm<2, false>(opt, norm);
   return weighted ? pick_norm<3, true>(opt, norm) : pick_norm<3, false>(opt, norm);
+}
+
+KernelFn pick_finalize_peer(int opt) {
+  switch (opt) {
+    case OPT_FD: return finalize_peer_kernel<OPT_FD>;
+    case OPT_ADAM: return finalize_peer_kernel<OPT_ADAM>;
+    default: return finalize_peer_kernel<OPT_SGD>;
+  }
 }
 
 KernelFn pick_finalize(int opt) {
@@ -885,6 +903,7 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
     A.n_tiles_global = ctx->n_tiles_cap;  // the finalizer reduces the exchanged tile partials
     A.v_begin = ctx->shard_begin;
     A.v_end = std::min<int64_t>(ctx->shard_end, ctx->m);
+    if (ctx->peer_on) A.pe = ctx->pe;
   } else {
     A.tile0 = 0;
     A.n_tiles = S.unit_base[ctx->n_tiles];
@@ -1076,6 +1095,15 @@ int ivhd_destroy(ivhd_ctx* ctx) {
     dfree(ctx, s.sched_units); dfree(ctx, s.sched_off); dfree(ctx, s.d_unit_base);
   }
   dfree(ctx, ctx->perm); dfree(ctx, ctx->inv);
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (ctx->ybuf_malloc) {
+    cudaFree(ctx->ybuf[0]);
+    cudaFree(ctx->ybuf[1]);
+    ctx->ybuf[0] = ctx->ybuf[1] = nullptr;
+  }
+  if (ctx->tp2) cudaFree(ctx->tp2);
+  if (ctx->flags) cudaFree(ctx->flags);
+  if (ctx->stamp) cudaFree(ctx->stamp);
   dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial); dfree(ctx, ctx->tpart); dfree(ctx, ctx->bpart);
   dfree(ctx, ctx->trace); dfree(ctx, ctx->ctrl); dfree(ctx, ctx->opctrl); dfree(ctx, ctx->red_out);
   dfree(ctx, ctx->stage); dfree(ctx, ctx->op_y); dfree(ctx, ctx->op_force);
@@ -1531,6 +1559,27 @@ static int ensure_trace(ivhd_ctx* ctx, int64_t n) {
   return IVHD_OK;
 }
 
+// After a run segment: status, trace and done count (engine.py:373-377 contract).
+static int read_trace(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out) {
+  TRY(pull_ctrl(ctx));
+  const Ctrl& C = *ctx->ctrl_h;
+  if (C.status == 3) return fail(ctx, IVHD_ERR_PEER, "peer exchange: a rank did not arrive within the time limit");
+  const bool diverged = C.status != 0;
+  const int64_t done = diverged ? C.diverged_at : C.iter;
+  const int64_t ntr = diverged ? done + 1 : done;
+  if (ntr > 0 && (stress_out || step_out)) {
+    std::vector<double2> tr(ntr);
+    CU(ctx, cudaMemcpy(tr.data(), ctx->trace, sizeof(double2) * ntr, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < ntr; ++i) {
+      if (stress_out) stress_out[i] = tr[i].x;
+      if (step_out) step_out[i] = tr[i].y;
+    }
+  }
+  if (done_out) *done_out = done;
+  if (diverged) return fail(ctx, IVHD_ERR_DIVERGED, "embedding diverged at local iteration %lld", (long long)done);
+  return IVHD_OK;
+}
+
 int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double* stress_out,
              double* step_out, int64_t* done_out) {
   TRY(check_ready(ctx, slot));
@@ -1538,7 +1587,8 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   if (norm != IVHD_NORM_L2 && norm != IVHD_NORM_L1) return fail(ctx, IVHD_ERR_INVALID_ARG, "unknown norm %d", norm);
   if (n_iter < 0) return fail(ctx, IVHD_ERR_INVALID_ARG, "n_iter must be >= 0");
   if (!ctx->pos_set) return fail(ctx, IVHD_ERR_STATE, "positions not set");
-  if (ctx->sharded) return fail(ctx, IVHD_ERR_STATE, "context is sharded; use ivhd_step_local/finalize");
+  if (ctx->sharded && !ctx->peer_on)
+    return fail(ctx, IVHD_ERR_STATE, "context is sharded; use ivhd_shard_* or the peer exchange (ivhd_peer_*)");
   TRY(ensure_trace(ctx, n_iter));
   TRY(pull_ctrl(ctx));
   if (ctx->ctrl_h->status != 0) return fail(ctx, IVHD_ERR_DIVERGED, "context already diverged");
@@ -1549,17 +1599,26 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   TRY(push_ctrl(ctx));
   const CsrSlot& S = ctx->slots[slot];
   KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm);
-  StepArgs A = make_args(ctx, slot, norm, 1);
-  {
+  const bool peer = ctx->peer_on;
+  StepArgs A = make_args(ctx, slot, norm, peer ? 0 : 1);
+  if (!peer) {
     const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
     TRY(build_schedule(ctx, ctx->slots[slot], grid));
     A.units = S.sched_units;
     A.boff = S.sched_off;
   }
+  // one iteration: the fused kernel (one GPU), or step + peer finalizer
+  auto launch_step = [&](ivhd_ctx* c, KernelInfo k, const StepArgs& a) -> int {
+    if (!peer) return ::launch_step(c, k, a);
+    if (a.n_tiles > 0) TRY(::launch_step(c, k, a));
+    pick_finalize_peer(c->opt.kind)<<<1, kBlock, 0, c->stream>>>(a);
+    CU(c, cudaGetLastError());
+    return IVHD_OK;
+  };
   int64_t left = n_iter;
   const int chunk = ctx->graph_chunk;
   if (left >= chunk) {
-    const GraphKey key{slot, norm, ctx->opt.kind, S.ew != nullptr ? 1 : 0};
+    const GraphKey key{slot, norm, ctx->opt.kind, (S.ew != nullptr ? 1 : 0) | (peer ? 2 : 0)};
     auto it = ctx->graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (it == ctx->graphs.end()) {
@@ -1584,22 +1643,7 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
     }
   }
   for (; left > 0; --left) TRY(launch_step(ctx, fn, A));
-  TRY(pull_ctrl(ctx));
-  const Ctrl& C = *ctx->ctrl_h;
-  const bool diverged = C.status != 0;
-  const int64_t done = diverged ? C.diverged_at : C.iter;
-  const int64_t ntr = diverged ? done + 1 : done;
-  if (ntr > 0 && (stress_out || step_out)) {
-    std::vector<double2> tr(ntr);
-    CU(ctx, cudaMemcpy(tr.data(), ctx->trace, sizeof(double2) * ntr, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < ntr; ++i) {
-      if (stress_out) stress_out[i] = tr[i].x;
-      if (step_out) step_out[i] = tr[i].y;
-    }
-  }
-  if (done_out) *done_out = done;
-  if (diverged) return fail(ctx, IVHD_ERR_DIVERGED, "embedding diverged at local iteration %lld", (long long)done);
-  return IVHD_OK;
+  return read_trace(ctx, stress_out, step_out, done_out);
 }
 
 static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* y, bool want_forces,
@@ -1827,11 +1871,16 @@ int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out) {
   if (!ctx->sharded) return fail(ctx, IVHD_ERR_STATE, "call ivhd_shard_set_range first");
   CU(ctx, cudaSetDevice(ctx->device));
   StepArgs A = make_args(ctx, slot, norm, 0);
-  shard_io(ctx, A);
   const CsrSlot& S = ctx->slots[slot];
+  ctx->shard_slot = slot;
+  if (ctx->peer_on) {  // fused peer exchange: the kernel publishes to every rank itself
+    if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
+    if (exchange_out) *exchange_out = 0;
+    return IVHD_OK;
+  }
+  shard_io(ctx, A);
   if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
   TRY(fold_tiles(ctx, S));
-  ctx->shard_slot = slot;
   if (exchange_out) *exchange_out = reinterpret_cast<uint64_t>(ctx->ybuf[ctx->shard_cur ^ 1]);
   return IVHD_OK;
 }
@@ -1840,6 +1889,11 @@ int ivhd_shard_finalize(ivhd_ctx* ctx) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
   CU(ctx, cudaSetDevice(ctx->device));
   StepArgs A = make_args(ctx, ctx->shard_slot, 0, 0);
+  if (ctx->peer_on) {
+    pick_finalize_peer(ctx->opt.kind)<<<1, kBlock, 0, ctx->stream>>>(A);
+    CU(ctx, cudaGetLastError());
+    return IVHD_OK;
+  }
   shard_io(ctx, A);
   pick_finalize(ctx->opt.kind)<<<1, kBlock, 0, ctx->stream>>>(A);
   CU(ctx, cudaGetLastError());
@@ -1850,22 +1904,119 @@ int ivhd_shard_finalize(ivhd_ctx* ctx) {
 int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
   CU(ctx, cudaSetDevice(ctx->device));
-  TRY(pull_ctrl(ctx));
-  const Ctrl& C = *ctx->ctrl_h;
-  const bool diverged = C.status != 0;
-  const int64_t done = diverged ? C.diverged_at : C.iter;
-  const int64_t ntr = diverged ? done + 1 : done;
-  if (ntr > 0 && (stress_out || step_out)) {
-    std::vector<double2> tr(ntr);
-    CU(ctx, cudaMemcpy(tr.data(), ctx->trace, sizeof(double2) * ntr, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < ntr; ++i) {
-      if (stress_out) stress_out[i] = tr[i].x;
-      if (step_out) step_out[i] = tr[i].y;
+  const int rc = read_trace(ctx, stress_out, step_out, done_out);
+  ctx->shard_cur = ctx->ctrl_h->cur;
+  return rc;
+}
+
+// ------------------------------------------------------ fused peer exchange
+
+// Move the buffers peers write into to cudaMalloc memory (CUDA IPC needs it)
+// and allocate the tile partials [2][n_tiles_cap], arrival flags and stamp.
+static int peer_alloc(ivhd_ctx* ctx, int world, int rank) {
+  if (!ctx->sharded) return fail(ctx, IVHD_ERR_STATE, "call ivhd_shard_set_range first");
+  if (world < 1 || world > kMaxPeers + 1 || rank < 0 || rank >= world)
+    return fail(ctx, IVHD_ERR_INVALID_ARG, "peer exchange: world %d rank %d (1..8 ranks)", world, rank);
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (!ctx->ybuf_malloc) {
+    const size_t bytes = sizeof(float) * 8 * ctx->v_cap;
+    for (int b = 0; b < 2; ++b) {
+      float* nb = nullptr;
+      CU(ctx, cudaMalloc(&nb, bytes));
+      CU(ctx, cudaMemcpy(nb, ctx->ybuf[b], bytes, cudaMemcpyDeviceToDevice));
+      dfree(ctx, ctx->ybuf[b]);
+      ctx->ybuf[b] = nb;
     }
+    ctx->ybuf_malloc = true;
   }
-  if (done_out) *done_out = done;
-  ctx->shard_cur = C.cur;
-  if (diverged) return fail(ctx, IVHD_ERR_DIVERGED, "embedding diverged at local iteration %lld", (long long)done);
+  if (!ctx->tp2) CU(ctx, cudaMalloc(&ctx->tp2, sizeof(double4) * 2 * ctx->n_tiles_cap));
+  if (!ctx->flags) CU(ctx, cudaMalloc(&ctx->flags, sizeof(unsigned long long) * 8));
+  if (!ctx->stamp) CU(ctx, cudaMalloc(&ctx->stamp, sizeof(unsigned long long)));
+  CU(ctx, cudaMemset(ctx->tp2, 0, sizeof(double4) * 2 * ctx->n_tiles_cap));
+  CU(ctx, cudaMemset(ctx->flags, 0, sizeof(unsigned long long) * 8));
+  CU(ctx, cudaMemset(ctx->stamp, 0, sizeof(unsigned long long)));
+  CU(ctx, cudaDeviceSynchronize());
+  ctx->world = world;
+  ctx->rank = rank;
+  PeerArgs& pe = ctx->pe;
+  pe = PeerArgs{};
+  pe.n_peers = 0;
+  pe.rank = rank;
+  pe.world = world;
+  pe.t0 = (int)(ctx->shard_begin / ctx->tile_v);
+  pe.t1 = (int)(ctx->shard_end / ctx->tile_v);
+  pe.tp_local = ctx->tp2;
+  pe.fl_local = ctx->flags;
+  pe.stamp = ctx->stamp;
+  pe.n_tiles_cap = ctx->n_tiles_cap;
+  pe.timeout_ns = 10LL * 1000 * 1000 * 1000;
+  drop_graphs(ctx);
+  return IVHD_OK;
+}
+
+int ivhd_peer_export(ivhd_ctx* ctx, int world, int rank, uint8_t* handle_out) {
+  if (!ctx || !handle_out) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  TRY(peer_alloc(ctx, world, rank));
+  cudaIpcMemHandle_t h[4];
+  CU(ctx, cudaIpcGetMemHandle(&h[0], ctx->ybuf[0]));
+  CU(ctx, cudaIpcGetMemHandle(&h[1], ctx->ybuf[1]));
+  CU(ctx, cudaIpcGetMemHandle(&h[2], ctx->tp2));
+  CU(ctx, cudaIpcGetMemHandle(&h[3], ctx->flags));
+  static_assert(sizeof(h) <= IVHD_PEER_HANDLE_BYTES, "handle size");
+  memset(handle_out, 0, IVHD_PEER_HANDLE_BYTES);
+  memcpy(handle_out, h, sizeof(h));
+  return IVHD_OK;
+}
+
+static void peer_finish(ivhd_ctx* ctx) {
+  ctx->pe.on = 1;
+  ctx->peer_on = true;
+  drop_graphs(ctx);
+}
+
+int ivhd_peer_import(ivhd_ctx* ctx, const uint8_t* all_handles) {
+  if (!ctx || !all_handles) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  if (!ctx->tp2) return fail(ctx, IVHD_ERR_STATE, "call ivhd_peer_export first");
+  CU(ctx, cudaSetDevice(ctx->device));
+  PeerArgs& pe = ctx->pe;
+  pe.n_peers = 0;
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == ctx->rank) continue;
+    cudaIpcMemHandle_t h[4];
+    memcpy(h, all_handles + (size_t)q * IVHD_PEER_HANDLE_BYTES, sizeof(h));
+    void* p[4];
+    for (int i = 0; i < 4; ++i) {
+      CU(ctx, cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess));
+      ctx->ipc_opened.push_back(p[i]);
+    }
+    const int k = pe.n_peers++;
+    pe.y0[k] = static_cast<float*>(p[0]);
+    pe.y1[k] = static_cast<float*>(p[1]);
+    pe.tp[k] = static_cast<double4*>(p[2]);
+    pe.fl[k] = static_cast<unsigned long long*>(p[3]);
+  }
+  peer_finish(ctx);
+  return IVHD_OK;
+}
+
+int ivhd_peer_import_local(ivhd_ctx* ctx, ivhd_ctx* const* ctxs) {
+  if (!ctx || !ctxs) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  if (!ctx->tp2) return fail(ctx, IVHD_ERR_STATE, "call ivhd_peer_export first");
+  PeerArgs& pe = ctx->pe;
+  pe.n_peers = 0;
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == ctx->rank) continue;
+    const ivhd_ctx* o = ctxs[q];
+    if (!o || !o->tp2 || o->world != ctx->world || o->rank != q)
+      return fail(ctx, IVHD_ERR_STATE, "peer context %d not exported for world %d", q, ctx->world);
+    const int k = pe.n_peers++;
+    pe.y0[k] = o->ybuf[0];
+    pe.y1[k] = o->ybuf[1];
+    pe.tp[k] = o->tp2;
+    pe.fl[k] = o->flags;
+  }
+  peer_finish(ctx);
   return IVHD_OK;
 }
 

@@ -93,6 +93,30 @@ struct Ctrl {
   double c;             // random-pair weight
   unsigned int arrive;  // blocks finished this launch
   unsigned int next_tile;
+  unsigned int parrive; // peer mode: blocks that published this launch
+  unsigned int pad1;
+};
+
+constexpr int kMaxPeers = 7;  // up to 8 ranks (one node)
+
+// Fused peer exchange (sharded mode over NVLink P2P, one process per GPU):
+// the step kernel stores each updated position into every peer's replica and
+// its tile partials into every peer's partial array, then raises its arrival
+// flag on every peer; finalize_peer_kernel waits for all ranks' flags and
+// takes the (identical) decision.  Buffers below are the peers' (CUDA IPC).
+struct PeerArgs {
+  int on;                         // 1: peer mode
+  int n_peers, rank, world;
+  int t0, t1;                     // this rank's tiles
+  float* y0[kMaxPeers];           // peers' position buffers 0 / 1
+  float* y1[kMaxPeers];
+  double4* tp[kMaxPeers];         // peers' tile partials [2][n_tiles_cap] (by stamp parity)
+  unsigned long long* fl[kMaxPeers];  // peers' arrival flags [world]
+  double4* tp_local;              // own tile partials [2][n_tiles_cap]
+  unsigned long long* fl_local;   // own arrival flags [world]
+  unsigned long long* stamp;      // iterations exchanged so far (device word; survives ivhd_restore)
+  int n_tiles_cap;
+  long long timeout_ns;           // finalizer wait limit before it reports a peer failure
 };
 
 struct Hyper {
@@ -133,6 +157,7 @@ struct StepArgs {
   int out_index;          // fixed_io: which context buffer ybuf1 is (becomes ctrl->cur)
   long long v_cap_floats; // fixed_io: floats per position buffer (rollback copy)
   Hyper h;
+  PeerArgs pe;
 };
 
 // ------------------------------------------------------------------ layout
@@ -458,6 +483,21 @@ __device__ __forceinline__ void st_state(float* p, const float (&s)[SS > 0 ? SS 
 // grad = -2 force, optim.py:259-263).  State vectors live in sv: FD delta /
 // momentum velocity at [0, DIM); Adam (v, s) and Adadelta (E[g^2], E[d^2])
 // at [0, DIM) and [V, V+DIM) with V = 2 (dim 2) or 4 (dim 3).
+// Store one vertex's new position record (YS floats) at base + v * YS.
+template <int DIM, int OPT>
+__device__ __forceinline__ void store_pos(float* base, long long v, const float (&yn)[DIM], const float (&la)[DIM]) {
+  if constexpr (OPT == OPT_NEST) {
+    if constexpr (DIM == 2) {
+      *reinterpret_cast<float4*>(base + (size_t)v * 4) = make_float4(yn[0], yn[1], la[0], la[1]);
+    } else {
+      *reinterpret_cast<float4*>(base + (size_t)v * 8) = make_float4(yn[0], yn[1], yn[2], 0.f);
+      *reinterpret_cast<float4*>(base + (size_t)v * 8 + 4) = make_float4(la[0], la[1], la[2], 0.f);
+    }
+  } else {
+    st_vec<DIM>(base + (size_t)v * Layout<DIM, OPT>::YS, yn);
+  }
+}
+
 template <int DIM, int OPT>
 __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restrict__ Yout, long long v,
                                              const float (&yi)[DIM], float (&sv)[Layout<DIM, OPT>::SS > 0 ? Layout<DIM, OPT>::SS : 1],
@@ -506,18 +546,13 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
     }
   }
   if constexpr (L::SS > 0) st_state<L::SS>(A.state + (size_t)v * L::SS, sv);
-  if constexpr (OPT == OPT_NEST) {
-    float la[DIM];
+  float la[DIM];
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) la[d] = yn[d] + A.h.beta * sv[d];  // optim.py:174-175
-    if constexpr (DIM == 2) {
-      *reinterpret_cast<float4*>(Yout + (size_t)v * 4) = make_float4(yn[0], yn[1], la[0], la[1]);
-    } else {
-      *reinterpret_cast<float4*>(Yout + (size_t)v * 8) = make_float4(yn[0], yn[1], yn[2], 0.f);
-      *reinterpret_cast<float4*>(Yout + (size_t)v * 8 + 4) = make_float4(la[0], la[1], la[2], 0.f);
-    }
-  } else {
-    st_vec<DIM>(Yout + (size_t)v * L::YS, yn);
+  for (int d = 0; d < DIM; ++d) la[d] = OPT == OPT_NEST ? yn[d] + A.h.beta * sv[d] : yn[d];  // optim.py:174-175
+  store_pos<DIM, OPT>(Yout, v, yn, la);
+  if (A.pe.on) {  // fused exchange: the same record into every peer's replica (NVLink P2P stores)
+    const bool out1 = Yout == A.ybuf1;
+    for (int q = 0; q < A.pe.n_peers; ++q) store_pos<DIM, OPT>(out1 ? A.pe.y1[q] : A.pe.y0[q], v, yn, la);
   }
   acc_bad += all_finite(yn, DIM) ? 0.f : 1.f;
 }
@@ -698,6 +733,57 @@ struct StageMeta {
   int nv;           // vertices in the unit
   int pad[3];
 };
+
+// ------------------------------------------------------------ peer mode
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// End of a peer-mode step launch, called by every thread of every block:
+// the block's P2P position stores are ordered before its arrival (system-scope
+// fence after the block barrier); the last block to arrive folds this rank's
+// unit partials into tile partials, stores them into its own and every peer's
+// partial array (slot = stamp parity), and raises flag[rank] = stamp on every
+// rank.  `scratch` is >= 1 int of shared memory.
+__device__ __noinline__ void peer_publish(const StepArgs& A, int* scratch, bool from_units) {
+  block_sync();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&A.ctrl->parrive) : "memory");
+    scratch[0] = old == gridDim.x - 1;
+  }
+  block_sync();
+  if (!scratch[0]) return;
+  __threadfence();
+  const unsigned long long stamp = *A.pe.stamp + 1;
+  const size_t par = (size_t)(stamp & 1) * A.pe.n_tiles_cap;
+  for (int t = A.pe.t0 + threadIdx.x; t < A.pe.t1; t += blockDim.x) {
+    double4 s = make_double4(0, 0, 0, 0);
+    if (from_units) {  // fp32 kernel: fold the tile's unit partials in unit order
+      for (int u = A.unit_base[t]; u < A.unit_base[t + 1]; ++u) {
+        const double4 q = A.partial[u];
+        s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+      }
+    } else {  // fp64 kernel: tile partials already in tpart
+      s = A.tpart[t];
+    }
+    A.pe.tp_local[par + t] = s;
+    for (int q = 0; q < A.pe.n_peers; ++q) A.pe.tp[q][par + t] = s;
+  }
+  block_sync();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(A.pe.fl_local + A.pe.rank, stamp);
+    for (int q = 0; q < A.pe.n_peers; ++q) st_release_sys(A.pe.fl[q] + A.pe.rank, stamp);
+    A.ctrl->parrive = 0;  // every block of this launch has arrived
+  }
+}
 
 // ------------------------------------------------------------------ kernel
 // Persistent blocks take work units statically (u = blockIdx.x + k*grid;
@@ -1071,7 +1157,10 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     }
   }
 
-  if (!A.fuse_finalize) return;
+  if (!A.fuse_finalize) {
+    if (A.pe.on) peer_publish(A, sm_units, true);
+    return;
+  }
   IVHD_TL(38);
   // block partial: warp sums in a fixed butterfly, then warps in order
   block_sync();
@@ -1107,6 +1196,46 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   __syncwarp();
   finalize_warp<OPT>(A, A.bpart, (int)gridDim.x);
   IVHD_TL(39);
+}
+
+// Peer-mode finalizer: one block.  Waits until every rank has raised its
+// flag for this iteration (system-scope acquire; a rank that does not arrive
+// within pe.timeout_ns sets status 3 = peer failure instead of hanging), then
+// reduces all tile partials of the iteration in tile order and decides.
+template <int OPT>
+__global__ void __launch_bounds__(kBlock) finalize_peer_kernel(StepArgs A) {
+  __shared__ double4 sm_red[kBlock / 32];
+  __shared__ int s_fail;
+  griddep_wait();
+  if (A.ctrl->status != 0) return;
+  const unsigned long long stamp = *A.pe.stamp + 1;
+  if (threadIdx.x == 0) s_fail = 0;
+  block_sync();
+  if (threadIdx.x < A.pe.world) {
+    const unsigned long long* f = A.pe.fl_local + threadIdx.x;
+    long long t0 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int fail = 0;
+    while (ld_acquire_sys(f) < stamp) {
+      long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > A.pe.timeout_ns) {
+        fail = 1;
+        break;
+      }
+      __nanosleep(100);
+    }
+    if (fail) atomicExch(&s_fail, 1);
+  }
+  block_sync();
+  if (s_fail) {
+    if (threadIdx.x == 0) A.ctrl->status = 3;
+    return;
+  }
+  __threadfence();
+  const double4* tp = A.pe.tp_local + (size_t)(stamp & 1) * A.pe.n_tiles_cap;
+  finalize_block<OPT>(A, sm_red, tp, A.pe.n_tiles_cap);
+  if (threadIdx.x == 0) *A.pe.stamp = stamp;
 }
 
 // Standalone finalizer (sharded mode, after the exchange): one block.

@@ -131,6 +131,14 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
         Yout[v * FL::DP + d] = yn[d];
         ok &= isfinite(yn[d]);
       }
+      if (A.pe.on) {  // fused exchange: into every peer's replica (NVLink P2P stores)
+        const bool out1 = reinterpret_cast<float*>(Yout) == A.ybuf1;
+        for (int q = 0; q < A.pe.n_peers; ++q) {
+          double* py = reinterpret_cast<double*>(out1 ? A.pe.y1[q] : A.pe.y0[q]);
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) py[v * FL::DP + d] = yn[d];
+        }
+      }
       pe = e;
       pb = ok ? 0.0 : 1.0;
     }
@@ -142,7 +150,13 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
       if (tid == 0) A.tpart[t] = r;
     }
   }
-  if (!A.fuse_finalize) return;
+  if (!A.fuse_finalize) {
+    if (A.pe.on) {
+      __shared__ int scratch;
+      peer_publish(A, &scratch, false);
+    }
+    return;
+  }
   // block partial in fixed order, then the last block to arrive decides
   const double4 r = block_sum4(make_double4(te, 0.0, 0.0, tb), sm_red);
   if (warp != 0) return;

@@ -225,6 +225,24 @@ class DeviceEmbedding:
         self._check(code)
         return e.value, s.value, bool(com.value), False
 
+    # fused peer exchange (include/ivhd_b200.h, ivhd_peer_*)
+    def peer_export(self, world, rank):
+        """Move the exchanged buffers to IPC-able memory; returns this rank's
+        handle bytes (to be all-gathered in rank order)."""
+        h = np.zeros(_lib.PEER_HANDLE_BYTES, dtype=np.uint8)
+        self._check(self.lib.ivhd_peer_export(self.h, int(world), int(rank), h.ctypes.data_as(c_u8p)))
+        return h.tobytes()
+
+    def peer_import(self, handles):
+        """handles: the ranks' peer_export bytes, in rank order."""
+        buf = np.frombuffer(b"".join(handles), dtype=np.uint8).copy()
+        self._check(self.lib.ivhd_peer_import(self.h, buf.ctypes.data_as(c_u8p)))
+
+    def peer_import_local(self, devs):
+        """In-process peers: the DeviceEmbedding of every rank, in rank order."""
+        arr = (ctypes.c_void_p * len(devs))(*[d.h.value for d in devs])
+        self._check(self.lib.ivhd_peer_import_local(self.h, arr))
+
     # asynchronous sharded loop (include/ivhd_b200.h, ivhd_shard_*)
     def shard_begin(self, slot, c, n_iter):
         """Returns (index of the buffer holding the current positions, graph

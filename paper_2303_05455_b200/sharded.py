@@ -5,22 +5,28 @@ from the same positions Y_n (engine.py:360-372), so vertex ranges are
 independent given Y_n and one exchange per iteration suffices.
 
 Each rank holds the full (relabelled) symmetrised CSR and a full replica of
-the positions, updates the vertices of its tile-aligned range [v0, v1) with
-the fused step kernel (ivhd_step_local), then all-gathers
+the positions and updates the vertices of its tile-aligned range [v0, v1)
+(equal tile counts; the vertex order deals the degree-sorted vertices over
+8 rank groups so every range has the same edge count).  Two exchanges:
 
-  * its slice of the new positions (8 B/vertex in 2-D), and
-  * its per-tile partials {stress, sum|dnew|^2, sum|dold|^2, #non-finite},
+* "p2p" (default on GPUs) — the fused exchange of ivhd_peer_* (one process
+  per GPU, one node): the step kernel stores each updated position straight
+  into every peer's replica over NVLink (CUDA IPC mappings) as it is
+  computed, so the transfer overlaps the update tile by tile; its last block
+  stores the rank's tile partials into every peer and raises an arrival flag
+  on every rank; a one-block finalizer waits for all flags and reduces the
+  tile partials in tile order.  No NCCL, no host work per iteration: the
+  iterations run as CUDA-graph replays of (step, finalizer).
+* "nccl" — the step writes its slice locally, then the slice and the
+  rank's tile partials are all-gathered in place through torch.distributed
+  (NCCL; gloo in the CPU tests) and ivhd_shard_finalize reduces them.  Kept
+  as the portable baseline and for the CPU tests.
 
-and every rank runs the same fixed-order finalizer (ivhd_step_finalize) over
-the full tile array — so the auto-adapt commit/rollback decision, the trace
-and the positions are identical on all ranks and for every rank count (tiles
-and their reduction order do not depend on it).  The fused single-GPU loop
-sums per-thread running partials instead, so its trace agrees with the
-sharded one to fp32 summation order (the per-vertex update is the same).
-
-The exchange goes through torch.distributed (NCCL over NVLink on GPUs, gloo
-for the CPU tests); the library launches on the caller's CUDA stream so the
-collectives are ordered with the kernels.
+Either way every rank reduces the same per-tile partials in the same order,
+so the auto-adapt decision, the trace and the positions are identical on
+all ranks and for every rank count.  The fused single-GPU loop sums
+per-thread running partials instead, so its trace agrees with the sharded
+one to fp32 summation order.
 """
 
 import numpy as np
@@ -94,11 +100,15 @@ class ShardedEmbedding:
     """One rank's share of a distributed IVHD run (same surface as
     DeviceEmbedding for set-up; `run` drives the per-iteration exchange)."""
 
-    def __init__(self, m, dim, rank, world, device=0, stream=0, group=None, backend=None):
+    def __init__(self, m, dim, rank, world, device=0, stream=0, group=None, backend=None, exchange=None):
         if backend is None:
             from .device import DeviceEmbedding
 
             backend = DeviceShardBackend(DeviceEmbedding(m, dim, device=device, stream=stream), stream)
+            exchange = exchange or "p2p"
+        self.exchange = exchange or "nccl"
+        if self.exchange not in ("p2p", "nccl"):
+            raise InvalidArgumentError(f"unknown exchange {exchange!r}")
         self.backend = backend
         self._graphs = {}
         self.m, self.dim, self.rank, self.world, self.group = int(m), int(dim), int(rank), int(world), group
@@ -106,6 +116,17 @@ class ShardedEmbedding:
         self.ranges = shard_ranges(n_tiles_cap, tile_v, self.world)
         self.v0, self.v1 = self.ranges[self.rank]
         backend.shard_set_range(self.v0, self.v1)
+        if self.exchange == "p2p":
+            # fused NVLink exchange (include/ivhd_b200.h ivhd_peer_*): every
+            # rank publishes its buffers' CUDA IPC handles, opens the others'
+            mine = backend.peer_export(self.world, self.rank)
+            handles = [mine]
+            if self.world > 1:
+                import torch.distributed as dist
+
+                handles = [None] * self.world
+                dist.all_gather_object(handles, mine, group=group)
+            backend.peer_import(handles)
 
     # set-up (graph, draws, optimizer, positions, read-back) is identical on
     # every rank: delegated to the rank's DeviceEmbedding
@@ -115,9 +136,10 @@ class ShardedEmbedding:
         return getattr(self.backend, name)
 
     def launches_per_iteration(self):
-        """Kernels per iteration: local update, tile fold, finalizer (NCCL's
-        all-gathers come on top)."""
-        return 3
+        """Kernels per iteration: p2p = the step kernel (it publishes to the
+        peers itself) + the finalizer; nccl = local update, tile fold,
+        finalizer (NCCL's all-gathers come on top)."""
+        return 2 if self.exchange == "p2p" else 3
 
     def step(self, slot, norm, c):
         """One synchronous iteration: local update, exchange, fixed-order
@@ -147,6 +169,8 @@ class ShardedEmbedding:
         graph (kernels + NCCL collectives) and replayed, so the host issues one
         launch per chunk instead of ~5 calls per iteration."""
         be = self.backend
+        if self.exchange == "p2p":  # the device drives the whole exchange
+            return be.run(slot, norm, c, n_iter)
         n_iter = int(n_iter)
         parity, epoch = be.shard_begin(slot, c, n_iter)
         chunk = self.graph_chunk if graph_chunk is None else int(graph_chunk)

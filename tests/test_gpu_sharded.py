@@ -41,7 +41,9 @@ def _setup(nb, world, rank, stream, optimizer="force-directed", iters=12, integr
 
     m = nb.shape[0]
     orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer=optimizer, integrator=integrator)
-    sh = ShardedEmbedding(m, 2, rank, world, device=0, stream=stream.cuda_stream)
+    # exchange="nccl": no automatic peer set-up (that needs a process group);
+    # the p2p emulation below connects the contexts itself
+    sh = ShardedEmbedding(m, 2, rank, world, device=0, stream=stream.cuda_stream, exchange="nccl")
     sh.set_optimizer(resolve_optimizer(optimizer, m, integrator=integrator and P.IntegratorParams(**integrator)))
     sh.set_positions(orc.Y)
     sh.set_graph(0, nb[:, :3], orc.rn_assign)
@@ -125,3 +127,98 @@ def test_emulated_ranks_rollbacks_and_adam():
     orc.run()
     np.testing.assert_array_equal(many[0][0], many[1][0])
     assert normwise(many[0][0], orc.Y) < 1e-5
+
+
+def _emulated_p2p(nb, world, iters, optimizer="force-directed", integrator=None):
+    """The fused peer exchange (ivhd_peer_*) with `world` contexts in one
+    process: ivhd_peer_export on each, ivhd_peer_import_local with the
+    contexts as peers; per iteration every rank's step kernel (it stores into
+    the others' replicas and raises their flags), then every finalizer (its
+    flags are already up: nothing waits on a kernel that has not run)."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ranks = [_setup(nb, world, r, stream, optimizer=optimizer, iters=iters, integrator=integrator)[0]
+                 for r in range(world)]
+        devs = [sh.backend.dev for sh in ranks]
+        for r, d in enumerate(devs):
+            d.peer_export(world, r)
+        for d in devs:
+            d.peer_import_local(devs)
+        for d in devs:
+            d.shard_begin(0, 0.1, iters)
+        for _ in range(iters):
+            for d in devs:
+                d.shard_step(0, "l2")
+            for d in devs:
+                d.shard_finalize()
+        out = []
+        for d in devs:
+            st, bb, done, div = d.shard_end()
+            assert done == iters and not div
+            out.append((d.positions(), st, bb))
+        stream.synchronize()
+        for d in devs:
+            d.close()
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_peer_exchange_emulated_matches_nccl_path_and_oracle(world):
+    nb = hub_graph()
+    iters = 12
+    ref = _emulated(nb, 2, iters)[0]  # the NCCL-style exchange (device copies)
+    many = _emulated_p2p(nb, world, iters)
+    for y, st, bb in many:
+        np.testing.assert_array_equal(y, many[0][0])
+        np.testing.assert_array_equal(st, many[0][1])
+    # same tiles, same fold order, same decisions: bit-identical to the NCCL path
+    np.testing.assert_array_equal(many[0][0], ref[0])
+    np.testing.assert_array_equal(many[0][1], ref[1])
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0)
+    orc.run()
+    assert normwise(many[0][0], orc.Y) < 1e-5
+    np.testing.assert_allclose(many[0][2], orc.trace_b, rtol=0)
+
+
+def test_peer_exchange_emulated_rollbacks_and_adam():
+    nb = hub_graph(seed=1)
+    iters = 10
+    integ = {"b": 0.5, "tau": 1e-6}
+    many = _emulated_p2p(nb, 2, iters, integrator=integ)
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, integrator=integ)
+    orc.run()
+    b = np.asarray(orc.trace_b)
+    assert (b[1:] != b[:-1]).sum() >= 3
+    np.testing.assert_array_equal(many[0][0], many[1][0])
+    np.testing.assert_allclose(many[0][2], b, rtol=0)
+    assert normwise(many[0][0], orc.Y) < 1e-5
+    many = _emulated_p2p(nb, 2, iters, optimizer="adam")
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer="adam")
+    orc.run()
+    np.testing.assert_array_equal(many[0][0], many[1][0])
+    assert normwise(many[0][0], orc.Y) < 1e-5
+
+
+def test_peer_exchange_world1_run_matches_fused_loop():
+    """ivhd_run on a one-rank peer context: CUDA graphs of (step, finalizer)."""
+    from paper_2303_05455_b200.config import resolve_optimizer
+    from paper_2303_05455_b200.device import DeviceEmbedding
+
+    nb = hub_graph(seed=2)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        sh, orc = _setup(nb, 1, 0, stream, iters=150)
+        d = sh.backend.dev
+        d.peer_import([d.peer_export(1, 0)])
+        st, bb, done, div = d.run(0, "l2", 0.1, 150)
+        assert done == 150 and not div
+        y = d.positions()
+        d.close()
+    ref = DeviceEmbedding(nb.shape[0], 2)
+    ref.set_optimizer(resolve_optimizer("force-directed", nb.shape[0]))
+    ref.set_positions(orc.Y)
+    ref.set_graph(0, nb[:, :3], orc.rn_assign)
+    s2, b2, _, _ = ref.run(0, "l2", 0.1, 150)
+    assert np.abs(y - ref.positions()).max() / np.abs(ref.positions()).max() < 1e-5
+    np.testing.assert_allclose(st, s2, rtol=1e-5)
+    np.testing.assert_array_equal(bb, b2)

@@ -21,7 +21,12 @@ def ncu(rep, *args):
     return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True, check=True).stdout
 
 
-def main(rep, out):
+NOTE = "ncu --set full --clock-control none; one launch"
+
+
+def main(rep, out, note=None):
+    global NOTE
+    NOTE = note or NOTE
     rows = list(csv.reader(ncu(rep, "--page", "raw", "--csv").splitlines()))
     hdr, units, vals = rows[0], rows[1], rows[2]
     kernel = vals[hdr.index("Kernel Name")]
@@ -50,12 +55,12 @@ def main(rep, out):
             lines.append((int(x[4] or 0), f"{fname}:{x[0]}", x[1].strip()[:96]))
             instr.append((float(x[h2.index("Instructions Executed")] or 0), f"{fname}:{x[0]}", x[1].strip()[:96]))
     dram = met.get("dram__bytes_read.sum", 0) + met.get("dram__bytes_write.sum", 0)
-    summary = {"kernel": kernel, "capture": rep.split("/")[-1], "dram_bytes_per_launch": dram,
+    summary = {"kernel": kernel, "capture": rep.split("/")[-1] + " (" + NOTE + ")", "dram_bytes_per_launch": dram,
                "metrics": met, "stall_mix_pct": {k: round(100 * v / tot, 1) for k, v in
                                                  sorted(stalls.items(), key=lambda t: -t[1]) if v / tot > 0.01}}
     json.dump(summary, open(out + ".json", "w"), indent=1)
     with open(out + ".txt", "w") as f:
-        f.write(f"kernel: {kernel}\ncapture: {rep}\n(ncu --set full --clock-control none; one launch, cold caches)\n\n")
+        f.write(f"kernel: {kernel}\ncapture: {rep}\n({NOTE})\n\n")
         for k, v in met.items():
             f.write(f"{k:66s} {v:.6g}\n")
         f.write("\nstall mix (pc sampling): " + ", ".join(f"{k} {v}%" for k, v in summary["stall_mix_pct"].items()))
@@ -68,4 +73,4 @@ def main(rep, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
