@@ -209,6 +209,17 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
 int ivhd_peer_export(ivhd_ctx* ctx, int world, int rank, uint8_t* handle_out);
 int ivhd_peer_import(ivhd_ctx* ctx, const uint8_t* all_handles);
 int ivhd_peer_import_local(ivhd_ctx* ctx, ivhd_ctx* const* ctxs);
+/* The step kernel stores a position only into the replicas of the ranks that
+ * gather it (halo masks from the connection sets).  At the end of a segment
+ * ivhd_run completes the local replica (both position buffers) with every
+ * peer's own range and then waits for all ranks (barrier = 1), so positions /
+ * deltas read back on any rank are complete.  ivhd_peer_pull does the same
+ * on demand; barrier = 0 skips the all-rank wait (in-process emulation, where
+ * the ranks' kernels run one after another). */
+int ivhd_peer_pull(ivhd_ctx* ctx, int barrier);
+/* Position records this rank stores into peers per iteration (sum over its
+ * vertices of the ranks that gather them) and their bytes. */
+int ivhd_peer_halo(ivhd_ctx* ctx, int64_t* records_out, int64_t* bytes_out);
 
 /* Exact kNN graph of the rows of a host (m, n) float64 matrix, computed on
  * `device` (knng.build_exact_knn, knng.py:158-194): row i lists its k nearest

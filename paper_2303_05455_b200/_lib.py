@@ -61,6 +61,8 @@ SIGNATURES = {
     "ivhd_peer_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_u8p]),
     "ivhd_peer_import": (ctypes.c_int, [ctypes.c_void_p, c_u8p]),
     "ivhd_peer_import_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "ivhd_peer_pull": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "ivhd_peer_halo": (ctypes.c_int, [ctypes.c_void_p, c_i64p, c_i64p]),
     "ivhd_set_connections": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, c_u8p, c_f64p,
                                             c_f64p, ctypes.c_int64]),
     "ivhd_set_positions": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),

@@ -127,6 +127,8 @@ struct ivhd_ctx {
   unsigned long long* flags = nullptr; // [8] arrival flags, one slot per rank
   unsigned long long* stamp = nullptr; // iterations exchanged
   PeerArgs pe{};
+  uint8_t* hmask = nullptr;            // [v_cap] halo masks (ranks that gather each own vertex)
+  bool masks_stale = true;
   std::vector<void*> ipc_opened;       // cudaIpcOpenMemHandle pointers to close
 
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -539,6 +541,57 @@ __global__ void k_fold_tiles(const double4* __restrict__ unit_part, const int* _
   }
 }
 
+// Halo masks of this rank's vertices: bit r of mask[v] is set when a row
+// owned by rank r (r != own) lists v, i.e. rank r gathers v's position.  The
+// symmetrised CSR makes that the set of ranks of v's own row entries.
+__global__ void k_halo_mask(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t v0,
+                            int64_t v1, int64_t range_v, int own, uint8_t* __restrict__ mask) {
+  for (int64_t v = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < v1; v += (int64_t)gridDim.x * blockDim.x) {
+    unsigned mk = mask[v];
+    for (uint32_t k = rp[v]; k < rp[v + 1]; ++k) mk |= 1u << (int)((col[k] & kIdMask) / range_v);
+    mask[v] = (uint8_t)(mk & ~(1u << own));
+  }
+}
+
+// After a peer-mode run: complete this rank's replica (both buffers) with
+// every peer's own range read over NVLink — the halo exchange only kept the
+// entries this rank gathers current.
+__global__ void k_peer_pull(float4* __restrict__ dst0, float4* __restrict__ dst1, const float4* __restrict__ src0,
+                            const float4* __restrict__ src1, int64_t f4_begin, int64_t f4_end) {
+  for (int64_t i = f4_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < f4_end;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    dst0[i] = src0[i];
+    dst1[i] = src1[i];
+  }
+}
+
+// All-rank barrier at the end of a peer-mode segment: raise flag [8 + rank]
+// on every rank, wait until all ranks raised theirs (same timeout and status
+// 3 as the finalizer).
+__global__ void k_peer_barrier(PeerArgs pe, Ctrl* ctrl) {
+  const unsigned long long s = pe.stamp[1] + 1;
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(pe.fl_local + 8 + pe.rank, s);
+    for (int q = 0; q < pe.n_peers; ++q) st_release_sys(pe.fl[q] + 8 + pe.rank, s);
+  }
+  if (threadIdx.x < pe.world) {
+    long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys(pe.fl_local + 8 + threadIdx.x) < s) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > pe.timeout_ns) {
+        ctrl->status = 3;
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) pe.stamp[1] = s;
+}
+
 // fixed-order reduction of partial tiles into one double4 (operator calls)
 __global__ void __launch_bounds__(kBlock) k_reduce_partials(const double4* __restrict__ p, int n,
                                                             double4* __restrict__ out) {
@@ -806,6 +859,7 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
   if (e != cudaSuccess) return fail(ctx, IVHD_ERR_CUDA, "CSR build: %s", cudaGetErrorString(e));
   if (hbad) return fail(ctx, IVHD_ERR_INVALID_ARG, "connection endpoint outside [0, %lld)", (long long)m);
   S.valid = true;
+  ctx->masks_stale = true;  // peer mode: halo masks follow the connection sets
   return IVHD_OK;
 }
 
@@ -1102,6 +1156,7 @@ int ivhd_destroy(ivhd_ctx* ctx) {
     ctx->ybuf[0] = ctx->ybuf[1] = nullptr;
   }
   if (ctx->tp2) cudaFree(ctx->tp2);
+  dfree(ctx, ctx->hmask);
   if (ctx->flags) cudaFree(ctx->flags);
   if (ctx->stamp) cudaFree(ctx->stamp);
   dfree(ctx, ctx->ybuf[0]); dfree(ctx, ctx->ybuf[1]); dfree(ctx, ctx->state); dfree(ctx, ctx->partial); dfree(ctx, ctx->tpart); dfree(ctx, ctx->bpart);
@@ -1559,6 +1614,9 @@ static int ensure_trace(ivhd_ctx* ctx, int64_t n) {
   return IVHD_OK;
 }
 
+static int peer_masks(ivhd_ctx* ctx);
+static int peer_pull(ivhd_ctx* ctx, bool barrier);
+
 // After a run segment: status, trace and done count (engine.py:373-377 contract).
 static int read_trace(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out) {
   TRY(pull_ctrl(ctx));
@@ -1600,6 +1658,7 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   const CsrSlot& S = ctx->slots[slot];
   KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm);
   const bool peer = ctx->peer_on;
+  if (peer && ctx->masks_stale) TRY(peer_masks(ctx));
   StepArgs A = make_args(ctx, slot, norm, peer ? 0 : 1);
   if (!peer) {
     const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
@@ -1643,6 +1702,7 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
     }
   }
   for (; left > 0; --left) TRY(launch_step(ctx, fn, A));
+  if (peer && n_iter > 0) TRY(peer_pull(ctx, true));
   return read_trace(ctx, stress_out, step_out, done_out);
 }
 
@@ -1874,6 +1934,10 @@ int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out) {
   const CsrSlot& S = ctx->slots[slot];
   ctx->shard_slot = slot;
   if (ctx->peer_on) {  // fused peer exchange: the kernel publishes to every rank itself
+    if (ctx->masks_stale) {
+      TRY(peer_masks(ctx));
+      A.pe = ctx->pe;
+    }
     if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
     if (exchange_out) *exchange_out = 0;
     return IVHD_OK;
@@ -1931,11 +1995,12 @@ static int peer_alloc(ivhd_ctx* ctx, int world, int rank) {
     ctx->ybuf_malloc = true;
   }
   if (!ctx->tp2) CU(ctx, cudaMalloc(&ctx->tp2, sizeof(double4) * 2 * ctx->n_tiles_cap));
-  if (!ctx->flags) CU(ctx, cudaMalloc(&ctx->flags, sizeof(unsigned long long) * 8));
-  if (!ctx->stamp) CU(ctx, cudaMalloc(&ctx->stamp, sizeof(unsigned long long)));
+  // flags: [0, 8) iteration arrivals, [8, 16) end-of-run barrier; stamp: [0] iterations, [1] barriers
+  if (!ctx->flags) CU(ctx, cudaMalloc(&ctx->flags, sizeof(unsigned long long) * 16));
+  if (!ctx->stamp) CU(ctx, cudaMalloc(&ctx->stamp, sizeof(unsigned long long) * 2));
   CU(ctx, cudaMemset(ctx->tp2, 0, sizeof(double4) * 2 * ctx->n_tiles_cap));
-  CU(ctx, cudaMemset(ctx->flags, 0, sizeof(unsigned long long) * 8));
-  CU(ctx, cudaMemset(ctx->stamp, 0, sizeof(unsigned long long)));
+  CU(ctx, cudaMemset(ctx->flags, 0, sizeof(unsigned long long) * 16));
+  CU(ctx, cudaMemset(ctx->stamp, 0, sizeof(unsigned long long) * 2));
   CU(ctx, cudaDeviceSynchronize());
   ctx->world = world;
   ctx->rank = rank;
@@ -1969,10 +2034,75 @@ int ivhd_peer_export(ivhd_ctx* ctx, int world, int rank, uint8_t* handle_out) {
   return IVHD_OK;
 }
 
-static void peer_finish(ivhd_ctx* ctx) {
+// Halo masks of the own range from every valid connection set (called when
+// the peer exchange is set up and after every CSR build in peer mode).
+static int peer_masks(ivhd_ctx* ctx) {
+  if (!ctx->peer_on) return IVHD_OK;
+  if (!ctx->hmask) CU(ctx, dalloc(ctx, &ctx->hmask, (size_t)ctx->v_cap));
+  CU(ctx, cudaMemsetAsync(ctx->hmask, 0, (size_t)ctx->v_cap, ctx->stream));
+  const int64_t range_v = (int64_t)(ctx->n_tiles_cap / ctx->world) * ctx->tile_v;
+  const int64_t v1 = std::min<int64_t>(ctx->shard_end, ctx->m);
+  for (const CsrSlot& S : ctx->slots)
+    if (S.valid && v1 > ctx->shard_begin)
+      k_halo_mask<<<grid_for(v1 - ctx->shard_begin, ctx->sm_count), 256, 0, ctx->stream>>>(
+          S.row_ptr, S.col, ctx->shard_begin, v1, range_v, ctx->rank, ctx->hmask);
+  CU(ctx, cudaGetLastError());
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->pe.mask = ctx->hmask;
+  ctx->masks_stale = false;
+  return IVHD_OK;
+}
+
+static int peer_finish(ivhd_ctx* ctx) {
   ctx->pe.on = 1;
   ctx->peer_on = true;
   drop_graphs(ctx);
+  return peer_masks(ctx);
+}
+
+// End of a peer-mode run segment: complete the local replica (both buffers)
+// with every peer's own range, then an all-rank barrier (flags [8, 16)) so no
+// rank starts its next segment — which overwrites its buffers — while another
+// is still reading them.
+static int peer_pull(ivhd_ctx* ctx, bool barrier) {
+  const int64_t range_v = (int64_t)(ctx->n_tiles_cap / ctx->world) * ctx->tile_v;
+  const int ys = ys_of(ctx->dim, ctx->opt.kind);
+  const PeerArgs& pe = ctx->pe;
+  for (int k = 0; k < pe.n_peers; ++k) {
+    const int q = pe.prank[k];
+    const int64_t a = (int64_t)q * range_v * ys / 4, b = std::min<int64_t>(ctx->m, (int64_t)(q + 1) * range_v) * ys / 4 + 1;
+    if (b <= a) continue;
+    k_peer_pull<<<grid_for(b - a, ctx->sm_count), 256, 0, ctx->stream>>>(
+        reinterpret_cast<float4*>(ctx->ybuf[0]), reinterpret_cast<float4*>(ctx->ybuf[1]),
+        reinterpret_cast<const float4*>(pe.y0[k]), reinterpret_cast<const float4*>(pe.y1[k]), a, b);
+  }
+  if (barrier) k_peer_barrier<<<1, 32, 0, ctx->stream>>>(pe, ctx->ctrl);
+  CU(ctx, cudaGetLastError());
+  return IVHD_OK;
+}
+
+int ivhd_peer_halo(ivhd_ctx* ctx, int64_t* records_out, int64_t* bytes_out) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (!ctx->peer_on) return fail(ctx, IVHD_ERR_STATE, "peer exchange not set up");
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->masks_stale) TRY(peer_masks(ctx));
+  const int64_t v0 = ctx->shard_begin, v1 = std::min<int64_t>(ctx->shard_end, ctx->m);
+  std::vector<uint8_t> mk(std::max<int64_t>(v1 - v0, 0));
+  if (!mk.empty()) CU(ctx, cudaMemcpy(mk.data(), ctx->hmask + v0, mk.size(), cudaMemcpyDeviceToHost));
+  int64_t n = 0;
+  for (uint8_t b : mk) n += __builtin_popcount(b);
+  if (records_out) *records_out = n;
+  if (bytes_out) *bytes_out = n * (int64_t)sizeof(float) * ys_of(ctx->dim, ctx->opt.kind);
+  return IVHD_OK;
+}
+
+int ivhd_peer_pull(ivhd_ctx* ctx, int barrier) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (!ctx->peer_on) return fail(ctx, IVHD_ERR_STATE, "peer exchange not set up");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(peer_pull(ctx, barrier != 0));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return IVHD_OK;
 }
 
 int ivhd_peer_import(ivhd_ctx* ctx, const uint8_t* all_handles) {
@@ -1991,13 +2121,13 @@ int ivhd_peer_import(ivhd_ctx* ctx, const uint8_t* all_handles) {
       ctx->ipc_opened.push_back(p[i]);
     }
     const int k = pe.n_peers++;
+    pe.prank[k] = q;
     pe.y0[k] = static_cast<float*>(p[0]);
     pe.y1[k] = static_cast<float*>(p[1]);
     pe.tp[k] = static_cast<double4*>(p[2]);
     pe.fl[k] = static_cast<unsigned long long*>(p[3]);
   }
-  peer_finish(ctx);
-  return IVHD_OK;
+  return peer_finish(ctx);
 }
 
 int ivhd_peer_import_local(ivhd_ctx* ctx, ivhd_ctx* const* ctxs) {
@@ -2011,13 +2141,13 @@ int ivhd_peer_import_local(ivhd_ctx* ctx, ivhd_ctx* const* ctxs) {
     if (!o || !o->tp2 || o->world != ctx->world || o->rank != q)
       return fail(ctx, IVHD_ERR_STATE, "peer context %d not exported for world %d", q, ctx->world);
     const int k = pe.n_peers++;
+    pe.prank[k] = q;
     pe.y0[k] = o->ybuf[0];
     pe.y1[k] = o->ybuf[1];
     pe.tp[k] = o->tp2;
     pe.fl[k] = o->flags;
   }
-  peer_finish(ctx);
-  return IVHD_OK;
+  return peer_finish(ctx);
 }
 
 }  // extern "C"

@@ -117,6 +117,8 @@ struct PeerArgs {
   unsigned long long* stamp;      // iterations exchanged so far (device word; survives ivhd_restore)
   int n_tiles_cap;
   long long timeout_ns;           // finalizer wait limit before it reports a peer failure
+  int prank[kMaxPeers];           // rank of peer slot k
+  const uint8_t* mask;            // halo: bit r of mask[v] = rank r has a row that gathers v
 };
 
 struct Hyper {
@@ -550,9 +552,11 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
 #pragma unroll
   for (int d = 0; d < DIM; ++d) la[d] = OPT == OPT_NEST ? yn[d] + A.h.beta * sv[d] : yn[d];  // optim.py:174-175
   store_pos<DIM, OPT>(Yout, v, yn, la);
-  if (A.pe.on) {  // fused exchange: the same record into every peer's replica (NVLink P2P stores)
+  if (A.pe.on) {  // fused exchange: the same record into the replica of every peer that gathers it
     const bool out1 = Yout == A.ybuf1;
-    for (int q = 0; q < A.pe.n_peers; ++q) store_pos<DIM, OPT>(out1 ? A.pe.y1[q] : A.pe.y0[q], v, yn, la);
+    const unsigned mk = A.pe.mask[v];
+    for (int q = 0; q < A.pe.n_peers; ++q)
+      if ((mk >> A.pe.prank[q]) & 1u) store_pos<DIM, OPT>(out1 ? A.pe.y1[q] : A.pe.y0[q], v, yn, la);
   }
   acc_bad += all_finite(yn, DIM) ? 0.f : 1.f;
 }

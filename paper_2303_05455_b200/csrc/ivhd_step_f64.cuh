@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
       }
       if (A.pe.on) {  // fused exchange: into every peer's replica (NVLink P2P stores)
         const bool out1 = reinterpret_cast<float*>(Yout) == A.ybuf1;
+        const unsigned mk = A.pe.mask[v];
         for (int q = 0; q < A.pe.n_peers; ++q) {
+          if (!((mk >> A.pe.prank[q]) & 1u)) continue;
           double* py = reinterpret_cast<double*>(out1 ? A.pe.y1[q] : A.pe.y0[q]);
 #pragma unroll
           for (int d = 0; d < DIM; ++d) py[v * FL::DP + d] = yn[d];

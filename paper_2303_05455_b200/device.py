@@ -243,6 +243,17 @@ class DeviceEmbedding:
         arr = (ctypes.c_void_p * len(devs))(*[d.h.value for d in devs])
         self._check(self.lib.ivhd_peer_import_local(self.h, arr))
 
+    def peer_pull(self, barrier=True):
+        """Complete the local replica with every peer's own range (ivhd_run
+        does this at the end of each segment)."""
+        self._check(self.lib.ivhd_peer_pull(self.h, int(bool(barrier))))
+
+    def peer_halo(self):
+        """(records, bytes) this rank stores into peers per iteration."""
+        n, b = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.lib.ivhd_peer_halo(self.h, ctypes.byref(n), ctypes.byref(b)))
+        return n.value, b.value
+
     # asynchronous sharded loop (include/ivhd_b200.h, ivhd_shard_*)
     def shard_begin(self, slot, c, n_iter):
         """Returns (index of the buffer holding the current positions, graph
