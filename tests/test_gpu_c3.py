@@ -18,6 +18,10 @@ compare the CUDA path directly with the reference at full size:
 
 C4 (configs[3]): the 10^7-vertex planted graph, nn=3: 10 iterations against
 the oracle (positions 1e-5, stress 1e-5, b exact).
+
+C1 (configs[0]) and C2 (configs[1], Adadelta and Nesterov at the default
+alpha): full runs against the reference's own results
+(tests/golden/c1_golden.npz, c2_golden.npz from make_c1c2_golden.py).
 """
 
 import hashlib
@@ -126,3 +130,48 @@ def test_c4_ten_iterations_vs_oracle():
     assert normwise(res.embedding.points, ref.Y) < 1e-5
     np.testing.assert_allclose(res.trace.stress, ref.trace_stress, rtol=1e-5)
     assert res.trace.step_size == [float(b) for b in ref.trace_b]
+
+
+def test_c1_full_run_matches_reference():
+    """C1 (configs[0]): 20k x 784 mixture (spread 0.23, cf ~ 0.70), exact 2-NN
+    graph from the reference's build_exact_knn, nn=2 rn=1 c=0.01, FD, 2000
+    iterations — against the reference's own full run
+    (tests/golden/c1_golden.npz, make_c1c2_golden.py): stress, every step
+    decision, neighbour hit and the rank-curve summary over all 20k rows."""
+    from paper_2303_05455_b200 import metrics, synth
+
+    g = np.load(os.path.join(GOLDEN, "c1_golden.npz"))
+    nb, labels = g["neighbors"], g["labels"].astype(np.int64)
+    cfg = P.EmbeddingConfig(nn=2, rn=1, c=0.01, iterations=2000, seed=0)
+    res = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    y = res.embedding.points
+    assert res.state.stress == pytest.approx(float(g["stress"]), rel=0.01)
+    np.testing.assert_allclose(res.trace.stress[:10], g["trace_stress"][:10], rtol=1e-5)
+    assert res.trace.step_size == list(g["trace_b"])
+    cf_nn, cf = metrics.neighbor_hit(y, labels, nn_max=100)
+    assert cf == pytest.approx(float(g["cf"]), rel=0.01)
+    x, _ = synth.mixture_points(20000, 784, seed=0, spread=float(g["spread"]))
+    got = metrics.evaluate_embedding(x.astype(np.float64), y, labels=labels, nn_max=100,
+                                     report_ks=(15, 100)).summary()
+    for key, val in zip(g["summary_keys"], g["summary_vals"]):
+        key = str(key)
+        assert got[key] == pytest.approx(float(val), rel=0.01, abs=1e-3 * max(1.0, abs(float(val)))), key
+
+
+@pytest.mark.parametrize("opt", ["adadelta", "nesterov"])
+def test_c2_full_run_matches_reference(opt):
+    """C2 (configs[1]): the reference's mnist_like(70000, 784) exact 5-NN graph,
+    nn=5 rn=1 c=0.01, 2500 iterations at the default alpha — final stress, the
+    first 10 stresses and the neighbour hit against the reference's run."""
+    from paper_2303_05455_b200 import metrics
+
+    g = np.load(os.path.join(GOLDEN, "c2_golden.npz"))
+    nb, labels = g["neighbors"], g["labels"].astype(np.int64)
+    cfg = P.EmbeddingConfig(nn=5, rn=1, c=0.01, iterations=2500, seed=0, optimizer=opt)
+    res = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
+    assert res.state.stress == pytest.approx(float(g[f"{opt}_stress"]), rel=0.01)
+    np.testing.assert_allclose(res.trace.stress[:10], g[f"{opt}_trace_stress"][:10], rtol=1e-5)
+    assert res.trace.step_size == list(g[f"{opt}_trace_b"])
+    cf_nn, cf = metrics.neighbor_hit(res.embedding.points, labels, nn_max=100)
+    assert cf == pytest.approx(float(g[f"{opt}_cf"]), rel=0.01)
+    assert cf_nn[9] == pytest.approx(float(g[f"{opt}_cf_nn"][9]), rel=0.01)
