@@ -53,7 +53,8 @@ enum ivhd_status {
   IVHD_ERR_CUDA = 2,        /* CUDA runtime failure (message has the CUDA error) */
   IVHD_ERR_DIVERGED = 3,    /* -> NumericalDivergenceError(iteration, state)    */
   IVHD_ERR_STATE = 4,       /* call order violated (e.g. run before set_graph)  */
-  IVHD_ERR_PEER = 5         /* peer exchange: a rank did not arrive in time      */
+  IVHD_ERR_PEER = 5,        /* peer exchange: a rank did not arrive in time      */
+  IVHD_PAUSED_DEGENERATE = 6 /* not an error: see ivhd_degenerate_pending         */
 };
 
 enum ivhd_norm { IVHD_NORM_L2 = 0, IVHD_NORM_L1 = 1 };
@@ -146,6 +147,24 @@ int ivhd_stress(ivhd_ctx* ctx, int slot, int norm, double c, const double* y,
                 double* stress_out);
 
 int ivhd_synchronize(ivhd_ctx* ctx);
+
+/* Degenerate random pairs (forces.py:158-174: d == 0, t != 0 get a unit
+ * direction drawn from run.rng, in connection order, magnitude w * t).  The
+ * kernel looks each one up in a host-filled table; when an iteration meets
+ * one without an entry, ivhd_run stops before committing it and returns
+ * IVHD_PAUSED_DEGENERATE with *done_out = iterations completed (their trace
+ * filled); ivhd_compute_forces returns it likewise.  The caller reads the
+ * entries, draws the directions from the run's generator and resumes:
+ *   ivhd_degenerate_pending(ctx, cap, &n, rows, entries)   row (caller's ids),
+ *       entry index in that row: out-halves in connection order, then
+ *       in-halves in connection order
+ *   ivhd_set_degenerate(ctx, n, rows, entries, vecs)       vecs (n, dim) =
+ *       +w*t*u for the connection's source row, -w*t*u for its destination row;
+ *       valid for the paused iteration (or the next forces call) only. */
+int ivhd_degenerate_pending(ivhd_ctx* ctx, int64_t cap, int64_t* n_out, int32_t* rows_out,
+                            int32_t* entries_out);
+int ivhd_set_degenerate(ivhd_ctx* ctx, int64_t n, const int32_t* rows, const int32_t* entries,
+                        const double* vecs);
 
 /* Device-side checkpoint of positions + optimizer state + control block
  * (restore is asynchronous on the context stream; used to restart a run

@@ -16,7 +16,7 @@ from .errors import DeviceError, IvhdError, InvalidArgumentError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("IVHD_B200_LIB", os.path.join(HERE, "libivhd_b200.so"))
 
-OK, ERR_INVALID_ARG, ERR_CUDA, ERR_DIVERGED, ERR_STATE, ERR_PEER = range(6)
+OK, ERR_INVALID_ARG, ERR_CUDA, ERR_DIVERGED, ERR_STATE, ERR_PEER, PAUSED_DEGENERATE = range(7)
 PEER_HANDLE_BYTES = 256
 NORM = {"l2": 0, "l1": 1}
 OPT_KIND = {"force-directed": 0, "sgd": 1, "momentum": 2, "nesterov": 3, "adam": 4, "adadelta": 5}
@@ -62,6 +62,8 @@ SIGNATURES = {
     "ivhd_peer_import": (ctypes.c_int, [ctypes.c_void_p, c_u8p]),
     "ivhd_peer_import_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "ivhd_peer_pull": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "ivhd_degenerate_pending": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_i64p, c_i32p, c_i32p]),
+    "ivhd_set_degenerate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_i32p, c_i32p, c_f64p]),
     "ivhd_peer_halo": (ctypes.c_int, [ctypes.c_void_p, c_i64p, c_i64p]),
     "ivhd_set_connections": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, c_u8p, c_f64p,
                                             c_f64p, ctypes.c_int64]),

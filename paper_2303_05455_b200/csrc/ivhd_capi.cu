@@ -87,8 +87,16 @@ struct ivhd_ctx {
   bool window_order = false;  // locality-ordered input: degree sort inside id windows, in-order schedule
 
   float* ybuf[2] = {nullptr, nullptr};  // 8 floats/vertex capacity
-  float* state = nullptr;               // state_fpv floats/vertex capacity
+  float* state = nullptr;               // 2 buffers x state_fpv floats/vertex (ctrl.scur = current)
   int state_fpv = 8;                    // 16 for fp64 Adam in 3-D
+  // degenerate random pairs (forces.py:167-174): host-drawn direction table + kernel misses
+  int2* dg_key = nullptr;
+  float4* dg_vec = nullptr;
+  int64_t dg_cap = 0;
+  int* miss_n = nullptr;
+  int2* miss = nullptr;
+  int miss_cap = 4096;
+  bool op_paused = false;  // an operator call (not the loop) is waiting for directions
   double4* partial = nullptr;  // per work unit (sharded / operator calls)
   double4* tpart = nullptr;    // per tile [n_tiles_cap]: the array ranks exchange (sharded)
   double4* bpart = nullptr;  // one per resident block of the step kernel
@@ -529,13 +537,24 @@ __global__ void k_tile_g(const uint32_t* __restrict__ rp, int64_t m, int n_tiles
 // Sharded mode: fold this rank's work-unit partials into one partial per tile
 // (units of a tile in unit order), so the exchanged array is indexed by tile
 // and every rank owns the contiguous chunk of its tile range.
+// (unit_base == nullptr: the fp64 kernel wrote tile partials already).  The
+// rank's first tile also carries 2^32 if this rank met degenerate pairs
+// without a direction (decide pauses every rank then).
 __global__ void k_fold_tiles(const double4* __restrict__ unit_part, const int* __restrict__ unit_base, int t0,
-                             int t1, double4* __restrict__ tpart) {
+                             int t1, double4* __restrict__ tpart, Ctrl* ctrl) {
   for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
     double4 s = make_double4(0, 0, 0, 0);
-    for (int u = unit_base[t]; u < unit_base[t + 1]; ++u) {
-      const double4 q = unit_part[u];
-      s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+    if (unit_base) {
+      for (int u = unit_base[t]; u < unit_base[t + 1]; ++u) {
+        const double4 q = unit_part[u];
+        s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+      }
+    } else {
+      s = tpart[t];
+    }
+    if (t == t0 && ctrl->need) {
+      s.w += kMissUnit;
+      ctrl->need = 0;
     }
     tpart[t] = s;
   }
@@ -641,6 +660,7 @@ void drop_graphs(ivhd_ctx* ctx) {
 
 int ys_now(ivhd_ctx* ctx);
 int ss_now(ivhd_ctx* ctx);
+float* state_buf(ivhd_ctx* ctx, int b);
 int pull_ctrl(ivhd_ctx* ctx);
 
 // Fix the vertex order from the degrees of the first CSR built: stable sort
@@ -733,8 +753,9 @@ int fix_permutation(ivhd_ctx* ctx, const uint32_t* rp_old, const int32_t* src, c
       if ((e = cudaMemcpyAsync(y, scratch, sizeof(float) * ys * m, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
         break;
       if (ss > 0) {
-        k_permute_rows<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(ctx->state, m, ss, perm, ctx->inv, scratch);
-        if ((e = cudaMemcpyAsync(ctx->state, scratch, sizeof(float) * ss * m, cudaMemcpyDeviceToDevice, st)) !=
+        float* sc = state_buf(ctx, ctx->ctrl_h->scur);
+        k_permute_rows<<<grid_for(m, ctx->sm_count), 256, 0, st>>>(sc, m, ss, perm, ctx->inv, scratch);
+        if ((e = cudaMemcpyAsync(sc, scratch, sizeof(float) * ss * m, cudaMemcpyDeviceToDevice, st)) !=
             cudaSuccess) break;
       }
     }
@@ -933,6 +954,12 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   A.ybuf0 = ctx->ybuf[0];
   A.ybuf1 = ctx->ybuf[1];
   A.state = ctx->state;
+  A.sstride = (long long)ctx->state_fpv * ctx->v_cap;
+  A.dg_key = ctx->dg_key;
+  A.dg_vec = ctx->dg_vec;
+  A.miss_n = ctx->miss_n;
+  A.miss = ctx->miss;
+  A.miss_cap = ctx->miss_cap;
   A.partial = ctx->partial;
   A.tpart = ctx->tpart;
   A.unit_base = S.d_unit_base;
@@ -1010,6 +1037,9 @@ int upload_stage(ivhd_ctx* ctx, const double* host, int64_t count) {
 }
 
 int vel_stride(int dim) { return dim == 2 ? 2 : 4; }
+
+// optimizer-state buffer b (0/1); ctrl.scur names the current one
+float* state_buf(ivhd_ctx* ctx, int b) { return ctx->state + (size_t)b * ctx->state_fpv * ctx->v_cap; }
 
 int ys_now(ivhd_ctx* ctx) { return ys_of(ctx->dim, ctx->opt.kind); }
 
@@ -1100,7 +1130,9 @@ int ivhd_create(ivhd_ctx** out, int device, int64_t m, int dim, uint64_t stream)
   };
   alloc((void**)&ctx->ybuf[0], sizeof(float) * 8 * vc);
   alloc((void**)&ctx->ybuf[1], sizeof(float) * 8 * vc);
-  alloc((void**)&ctx->state, sizeof(float) * 8 * vc);
+  alloc((void**)&ctx->state, sizeof(float) * 2 * 8 * vc);
+  alloc((void**)&ctx->miss_n, sizeof(int));
+  alloc((void**)&ctx->miss, sizeof(int2) * ctx->miss_cap);
   alloc((void**)&ctx->partial, sizeof(double4) * 32 * ctx->n_tiles_cap);  // <= 32 units per tile
   alloc((void**)&ctx->tpart, sizeof(double4) * ctx->n_tiles_cap);
   alloc((void**)&ctx->bpart, sizeof(double4) * 8 * ctx->sm_count);  // <= 2048/288 blocks per SM
@@ -1163,6 +1195,7 @@ int ivhd_destroy(ivhd_ctx* ctx) {
   dfree(ctx, ctx->trace); dfree(ctx, ctx->ctrl); dfree(ctx, ctx->opctrl); dfree(ctx, ctx->red_out);
   dfree(ctx, ctx->stage); dfree(ctx, ctx->op_y); dfree(ctx, ctx->op_force);
   dfree(ctx, ctx->snap_y); dfree(ctx, ctx->snap_state);
+  dfree(ctx, ctx->dg_key); dfree(ctx, ctx->dg_vec); dfree(ctx, ctx->miss_n); dfree(ctx, ctx->miss);
   if (ctx->ctrl_h) pinned_ctrl_put(ctx->ctrl_h);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1275,8 +1308,8 @@ int ivhd_init_positions(ivhd_ctx* ctx, uint64_t* rng, double lo, double hi) {
   const int ys = ys_of(ctx->dim, ctx->opt.kind);
   const bool nest = ctx->opt.kind == IVHD_OPT_NESTEROV;
   k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-      ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
-      (float)ctx->hyper.beta, ctx->ybuf[ctx->ctrl_h->cur], f64_of(ctx->opt.kind));
+      ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? state_buf(ctx, ctx->ctrl_h->scur) : nullptr,
+      vel_stride(ctx->dim), (float)ctx->hyper.beta, ctx->ybuf[ctx->ctrl_h->cur], f64_of(ctx->opt.kind));
   CU(ctx, cudaGetLastError());
   ctx->ctrl_h->status = 0;
   ctx->ctrl_h->last_commit = 0;
@@ -1483,8 +1516,8 @@ int ivhd_set_positions(ivhd_ctx* ctx, const double* y) {
   const bool nest = ctx->opt.kind == IVHD_OPT_NESTEROV;
   float* dst = ctx->ybuf[ctx->ctrl_h->cur];
   k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-      ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? ctx->state : nullptr, vel_stride(ctx->dim),
-      (float)ctx->hyper.beta, dst, f64_of(ctx->opt.kind));
+      ctx->stage, ctx->m, ctx->dim, ys, ctx->perm, nest ? state_buf(ctx, ctx->ctrl_h->scur) : nullptr,
+      vel_stride(ctx->dim), (float)ctx->hyper.beta, dst, f64_of(ctx->opt.kind));
   CU(ctx, cudaGetLastError());
   ctx->ctrl_h->status = 0;
   ctx->ctrl_h->last_commit = 0;
@@ -1536,7 +1569,7 @@ int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p) {
   const int need_fpv = (new_f64 && ctx->dim == 3) ? 16 : 8;
   if (need_fpv > ctx->state_fpv) {
     float* ns = nullptr;
-    CU(ctx, dalloc(ctx, &ns, sizeof(float) * need_fpv * ctx->v_cap));
+    CU(ctx, dalloc(ctx, &ns, sizeof(float) * 2 * need_fpv * ctx->v_cap));
     dfree(ctx, ctx->state);
     dfree(ctx, ctx->snap_state);
     ctx->snap_state = nullptr;
@@ -1551,13 +1584,14 @@ int ivhd_set_optimizer(ivhd_ctx* ctx, const ivhd_optimizer_params* p) {
     k_unpack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(cur, ctx->m, ctx->dim,
                                                                                 old_ys, ctx->perm, ctx->stage,
                                                                                 old_f64);
-    CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * ctx->state_fpv * ctx->v_cap, ctx->stream));
+    CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * 2 * ctx->state_fpv * ctx->v_cap, ctx->stream));
     k_pack_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
-        ctx->stage, ctx->m, ctx->dim, new_ys, ctx->perm, p->kind == IVHD_OPT_NESTEROV ? ctx->state : nullptr,
-        vel_stride(ctx->dim), (float)p->beta, cur, new_f64);
+        ctx->stage, ctx->m, ctx->dim, new_ys, ctx->perm,
+        p->kind == IVHD_OPT_NESTEROV ? state_buf(ctx, ctx->ctrl_h->scur) : nullptr, vel_stride(ctx->dim),
+        (float)p->beta, cur, new_f64);
     CU(ctx, cudaGetLastError());
   }
-  CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * ctx->state_fpv * ctx->v_cap, ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->state, 0, sizeof(float) * 2 * ctx->state_fpv * ctx->v_cap, ctx->stream));
   ctx->opt = *p;
   ctx->opt_set = true;
   Hyper h{};
@@ -1622,6 +1656,19 @@ static int read_trace(ivhd_ctx* ctx, double* stress_out, double* step_out, int64
   TRY(pull_ctrl(ctx));
   const Ctrl& C = *ctx->ctrl_h;
   if (C.status == 3) return fail(ctx, IVHD_ERR_PEER, "peer exchange: a rank did not arrive within the time limit");
+  if (C.status == 2) {  // paused before iteration C.iter: degenerate pairs need host-drawn directions
+    const int64_t done = C.iter;
+    if (done > 0 && (stress_out || step_out)) {
+      std::vector<double2> tr(done);
+      CU(ctx, cudaMemcpy(tr.data(), ctx->trace, sizeof(double2) * done, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < done; ++i) {
+        if (stress_out) stress_out[i] = tr[i].x;
+        if (step_out) step_out[i] = tr[i].y;
+      }
+    }
+    if (done_out) *done_out = done;
+    return IVHD_PAUSED_DEGENERATE;
+  }
   const bool diverged = C.status != 0;
   const int64_t done = diverged ? C.diverged_at : C.iter;
   const int64_t ntr = diverged ? done + 1 : done;
@@ -1649,12 +1696,15 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
     return fail(ctx, IVHD_ERR_STATE, "context is sharded; use ivhd_shard_* or the peer exchange (ivhd_peer_*)");
   TRY(ensure_trace(ctx, n_iter));
   TRY(pull_ctrl(ctx));
+  if (ctx->ctrl_h->status == 2)
+    return fail(ctx, IVHD_ERR_STATE, "paused at a degenerate pair: call ivhd_set_degenerate first");
   if (ctx->ctrl_h->status != 0) return fail(ctx, IVHD_ERR_DIVERGED, "context already diverged");
   ctx->ctrl_h->c = c;
   ctx->ctrl_h->iter = 0;
   ctx->ctrl_h->arrive = 0;
   ctx->ctrl_h->next_tile = 0;
   TRY(push_ctrl(ctx));
+  CU(ctx, cudaMemsetAsync(ctx->miss_n, 0, sizeof(int), ctx->stream));
   const CsrSlot& S = ctx->slots[slot];
   KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm);
   const bool peer = ctx->peer_on;
@@ -1721,7 +1771,10 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   Ctrl oc{};
   oc.c = c;
   oc.gstep = ctx->ctrl_h->gstep;
+  oc.dg_gstep = ctx->ctrl_h->dg_gstep;  // directions the host drew for this evaluation (forces.py:167-174)
+  oc.dg_n = ctx->ctrl_h->dg_n;
   CU(ctx, cudaMemcpyAsync(ctx->opctrl, &oc, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->miss_n, 0, sizeof(int), ctx->stream));
   const CsrSlot& S = ctx->slots[slot];
   StepArgs A{};
   A.row_ptr = S.row_ptr;
@@ -1732,6 +1785,11 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   A.partial = ctx->partial;
   A.ctrl = ctx->opctrl;
   A.force_out = ctx->op_force;
+  A.dg_key = ctx->dg_key;
+  A.dg_vec = ctx->dg_vec;
+  A.miss_n = ctx->miss_n;
+  A.miss = ctx->miss;
+  A.miss_cap = ctx->miss_cap;
   A.tile_g = S.tile_g;
   A.units = S.units;
   A.v_begin = 0;
@@ -1752,8 +1810,87 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
     CU(ctx, cudaMemcpyAsync(forces_out, ctx->stage, sizeof(double) * ctx->m * ctx->dim,
                             cudaMemcpyDeviceToHost, ctx->stream));
   }
+  int nmiss = 0;
+  CU(ctx, cudaMemcpyAsync(&nmiss, ctx->miss_n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (stress_out) *stress_out = 0.5 * red.x;
+  if (want_forces && nmiss > 0) {  // directions needed: ivhd_degenerate_pending, then call again
+    ctx->op_paused = true;
+    return IVHD_PAUSED_DEGENERATE;
+  }
+  if (ctx->ctrl_h->dg_n > 0) {  // the table served this evaluation only
+    ctx->ctrl_h->dg_n = 0;
+    TRY(push_ctrl(ctx));
+  }
+  return IVHD_OK;
+}
+
+// Degenerate pairs met by the paused iteration (or operator call): row in
+// the caller's ids and entry index in that row of the symmetrised CSR (out-
+// halves in connection order, then in-halves in connection order).
+int ivhd_degenerate_pending(ivhd_ctx* ctx, int64_t cap, int64_t* n_out, int32_t* rows_out, int32_t* entries_out) {
+  if (!ctx || !n_out) return fail(ctx, IVHD_ERR_INVALID_ARG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  int n = 0;
+  CU(ctx, cudaMemcpy(&n, ctx->miss_n, sizeof(int), cudaMemcpyDeviceToHost));
+  if (n > ctx->miss_cap)
+    return fail(ctx, IVHD_ERR_STATE, "%d degenerate pairs in one iteration (capacity %d)", n, ctx->miss_cap);
+  *n_out = n;
+  if (n == 0 || cap <= 0) return IVHD_OK;
+  const int k = (int)std::min<int64_t>(n, cap);
+  std::vector<int2> ms(k);
+  std::vector<int32_t> perm(1);
+  CU(ctx, cudaMemcpy(ms.data(), ctx->miss, sizeof(int2) * k, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < k; ++i) {
+    int32_t orig = 0;
+    CU(ctx, cudaMemcpy(&orig, ctx->perm + ms[i].x, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (rows_out) rows_out[i] = orig;
+    if (entries_out) entries_out[i] = ms[i].y;
+  }
+  return IVHD_OK;
+}
+
+// Directions for the paused iteration: (row, entry) as reported by
+// ivhd_degenerate_pending, vecs (n, dim) = w * t * unit direction with the
+// sign of the row's side (+ for the connection's source row, - for its
+// destination row).  Resumes the context; the table is valid for that one
+// iteration (or the next operator call).
+int ivhd_set_degenerate(ivhd_ctx* ctx, int64_t n, const int32_t* rows, const int32_t* entries, const double* vecs) {
+  if (!ctx || n < 0 || (n > 0 && (!rows || !entries || !vecs))) return fail(ctx, IVHD_ERR_INVALID_ARG, "bad arguments");
+  CU(ctx, cudaSetDevice(ctx->device));
+  TRY(pull_ctrl(ctx));
+  if (n > ctx->dg_cap) {
+    dfree(ctx, ctx->dg_key);
+    dfree(ctx, ctx->dg_vec);
+    ctx->dg_key = nullptr;
+    ctx->dg_vec = nullptr;
+    CU(ctx, dalloc(ctx, &ctx->dg_key, sizeof(int2) * n));
+    CU(ctx, dalloc(ctx, &ctx->dg_vec, sizeof(float4) * n));
+    ctx->dg_cap = n;
+    drop_graphs(ctx);  // captured launches hold the table pointers
+  }
+  std::vector<int32_t> inv(ctx->m);
+  if (n > 0) CU(ctx, cudaMemcpy(inv.data(), ctx->inv, sizeof(int32_t) * ctx->m, cudaMemcpyDeviceToHost));
+  std::vector<int2> key(n);
+  std::vector<float4> vec(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (rows[i] < 0 || rows[i] >= ctx->m) return fail(ctx, IVHD_ERR_INVALID_ARG, "row %d out of range", rows[i]);
+    key[i] = make_int2(inv[rows[i]], entries[i]);
+    const double* v = vecs + i * ctx->dim;
+    vec[i] = make_float4((float)v[0], (float)v[1], ctx->dim == 3 ? (float)v[2] : 0.f, 0.f);
+  }
+  if (n > 0) {
+    CU(ctx, cudaMemcpy(ctx->dg_key, key.data(), sizeof(int2) * n, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->dg_vec, vec.data(), sizeof(float4) * n, cudaMemcpyHostToDevice));
+  }
+  ctx->ctrl_h->dg_n = (int)n;
+  ctx->ctrl_h->dg_gstep = ctx->ctrl_h->gstep;
+  if (ctx->ctrl_h->status == 2) ctx->ctrl_h->status = 0;
+  ctx->ctrl_h->need = 0;
+  ctx->op_paused = false;
+  TRY(push_ctrl(ctx));
+  CU(ctx, cudaMemsetAsync(ctx->miss_n, 0, sizeof(int), ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
   return IVHD_OK;
 }
 
@@ -1776,7 +1913,7 @@ int ivhd_snapshot(ivhd_ctx* ctx) {
   TRY(pull_ctrl(ctx));
   const size_t used = sizeof(float) * 8 * ctx->m;
   CU(ctx, cudaMemcpyAsync(ctx->snap_y, ctx->ybuf[ctx->ctrl_h->cur], used, cudaMemcpyDeviceToDevice, ctx->stream));
-  CU(ctx, cudaMemcpyAsync(ctx->snap_state, ctx->state, sizeof(float) * ctx->state_fpv * ctx->m,
+  CU(ctx, cudaMemcpyAsync(ctx->snap_state, state_buf(ctx, ctx->ctrl_h->scur), sizeof(float) * ctx->state_fpv * ctx->m,
                           cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->snap_ctrl = *ctx->ctrl_h;
   ctx->snap_valid = true;
@@ -1791,7 +1928,7 @@ int ivhd_restore(ivhd_ctx* ctx) {
   const size_t used = sizeof(float) * 8 * ctx->m;
   *ctx->ctrl_h = ctx->snap_ctrl;
   CU(ctx, cudaMemcpyAsync(ctx->ybuf[ctx->snap_ctrl.cur], ctx->snap_y, used, cudaMemcpyDeviceToDevice, ctx->stream));
-  CU(ctx, cudaMemcpyAsync(ctx->state, ctx->snap_state, sizeof(float) * ctx->state_fpv * ctx->m,
+  CU(ctx, cudaMemcpyAsync(state_buf(ctx, ctx->snap_ctrl.scur), ctx->snap_state, sizeof(float) * ctx->state_fpv * ctx->m,
                           cudaMemcpyDeviceToDevice, ctx->stream));
   TRY(push_ctrl(ctx));
   return IVHD_OK;  // asynchronous: ordered before the next launch on the stream
@@ -1814,9 +1951,10 @@ int ivhd_synchronize(ivhd_ctx* ctx) {
 
 // unit partials of this rank's tiles -> tile partials (the fp64 kernel writes tiles directly)
 static int fold_tiles(ivhd_ctx* ctx, const CsrSlot& S) {
-  if (f64_of(ctx->opt.kind)) return IVHD_OK;
   const int t0 = (int)(ctx->shard_begin / ctx->tile_v), t1 = (int)(ctx->shard_end / ctx->tile_v);
-  if (t1 > t0) k_fold_tiles<<<(t1 - t0 + 255) / 256, 256, 0, ctx->stream>>>(ctx->partial, S.d_unit_base, t0, t1, ctx->tpart);
+  if (t1 > t0)
+    k_fold_tiles<<<(t1 - t0 + 255) / 256, 256, 0, ctx->stream>>>(
+        ctx->partial, f64_of(ctx->opt.kind) ? nullptr : S.d_unit_base, t0, t1, ctx->tpart, ctx->ctrl);
   CU(ctx, cudaGetLastError());
   return IVHD_OK;
 }

@@ -94,7 +94,10 @@ struct Ctrl {
   unsigned int arrive;  // blocks finished this launch
   unsigned int next_tile;
   unsigned int parrive; // peer mode: blocks that published this launch
-  unsigned int pad1;
+  int need;             // a degenerate random pair had no direction in the table (forces.py:167-174)
+  int scur;             // optimizer-state buffer holding the current state (double buffered)
+  int dg_n;             // directions in the degenerate-pair table ...
+  long long dg_gstep;   // ... valid for this global iteration only
 };
 
 constexpr int kMaxPeers = 7;  // up to 8 ranks (one node)
@@ -136,7 +139,13 @@ struct StepArgs {
   const float2* ew;       // nullptr in binary mode
   float* ybuf0;
   float* ybuf1;
-  float* state;
+  float* state;           // two buffers of sstride floats: ctrl->scur holds the current state
+  long long sstride;
+  const int2* dg_key;     // degenerate-pair table: (row, entry index in the row) -> direction
+  const float4* dg_vec;   //   x, y, z = w * t * unit direction drawn by the host from run.rng
+  int* miss_n;            // pairs with no table entry this iteration ...
+  int2* miss;             // ... (row, entry index), up to miss_cap of them
+  int miss_cap;
   double4* partial;       // per work unit (sharded / operator calls)
   double4* tpart;         // per tile: sharded mode's exchanged partials
   const int* unit_base;   // first unit of each tile
@@ -212,35 +221,37 @@ __device__ __forceinline__ void gather(const float* __restrict__ Y, uint32_t j, 
 }
 
 // ---------------------------------------------------- degenerate directions
-// forces.py:167-174 draws a random unit direction (magnitude w*t) for random
-// pairs at exactly zero distance.  On the device the direction comes from a
-// counter-based hash of (min id, max id, global step) so both endpoint rows
-// of the pair see the same direction with opposite signs (measure-zero path).
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
-  x ^= x >> 27; x *= 0x94d049bb133111ebull;
-  x ^= x >> 31;
-  return x;
-}
-
+// forces.py:167-174: a random pair at exactly zero distance gets a unit
+// direction drawn from run.rng (standard normals, in connection order,
+// magnitude w * t).  The draw needs the reference's generator, so it is made
+// on the host: the kernel looks the pair up in a small table the host filled
+// for this iteration (keyed by row and entry index, so both endpoint rows of
+// the connection get the same direction with opposite signs); a pair without
+// an entry is recorded and flags the iteration, which the decision then
+// turns into a pause (status 2, nothing committed, state not advanced).  The
+// host draws the directions in connection order, fills the table and the
+// iteration is re-run.  Measure-zero: after a random init it never happens.
 template <int DIM>
-__device__ __noinline__ void degenerate_dir(uint32_t i, uint32_t j, long long step, float (&u)[DIM]) {
-  const uint32_t lo = min(i, j), hi = max(i, j);
-  uint64_t h = mix64(((uint64_t)lo << 32 | hi) ^ mix64((uint64_t)step + 0x9e3779b97f4a7c15ull));
-  const float r0 = (float)(h >> 40) * (1.0f / 16777216.0f);
-  const float r1 = (float)((h >> 16) & 0xffffff) * (1.0f / 16777216.0f);
-  const float sgn = (i == lo) ? 1.f : -1.f;
-  float s, c;
-  sincospif(2.f * r0, &s, &c);
-  if constexpr (DIM == 2) {
-    u[0] = sgn * c; u[1] = sgn * s;
-  } else {
-    const float z = 2.f * r1 - 1.f, rho = sqrtf(fmaxf(0.f, 1.f - z * z));
-    u[0] = sgn * rho * c; u[1] = sgn * rho * s; u[2] = sgn * z;
+__device__ __noinline__ void degenerate_vec(const StepArgs& A, uint32_t v, int e, long long gstep,
+                                           float (&u)[DIM]) {
+  const Ctrl* c = A.ctrl;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) u[d] = 0.f;
+  if (c->dg_gstep == gstep) {
+    for (int i = 0; i < c->dg_n; ++i) {
+      const int2 k = A.dg_key[i];
+      if (k.x == (int)v && k.y == e) {
+        const float4 q = A.dg_vec[i];
+        u[0] = q.x;
+        u[1] = q.y;
+        if constexpr (DIM == 3) u[2] = q.z;
+        return;
+      }
+    }
   }
-  if (i == j) {
-    for (int d = 0; d < DIM; ++d) u[d] = 0.f;  // self pair: +comp and -comp cancel
-  }
+  const int slot = atomicAdd(A.miss_n, 1);
+  if (slot < A.miss_cap) A.miss[slot] = make_int2((int)v, e);
+  atomicExch(&A.ctrl->need, 1);
 }
 
 // ------------------------------------------------------------------ entries
@@ -359,9 +370,20 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double4* sm /*[kBlock/3
 
 // The iteration decision from the reduced partials {stress, sum|dnew|^2,
 // sum|dold|^2, #non-finite} (optim.py:80-92 + engine.py:373-384); one thread.
+constexpr double kMissUnit = 4294967296.0;  // sharded partials: .w = #non-finite + 2^32 * (rank had misses)
+
 template <int OPT>
 __device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
   Ctrl* ctrl = A.ctrl;
+  const double misses = floor(s.w / kMissUnit);
+  s.w -= misses * kMissUnit;
+  if (ctrl->need || misses > 0.0) {  // degenerate pairs without directions: pause, redo after the host draw
+    ctrl->status = 2;
+    ctrl->need = 0;
+    ctrl->next_tile = 0;
+    ctrl->arrive = 0;
+    return;
+  }
   const double E = 0.5 * s.x;
   double step = ctrl->step;
   bool commit = true;
@@ -388,6 +410,7 @@ __device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
     ctrl->iter = it + 1;
   }
   ctrl->gstep += 1;
+  ctrl->scur ^= 1;  // the state written this iteration is current (FD keeps new deltas on rollback)
   if (OPT == OPT_ADAM) ctrl->adam_t += 1;
   ctrl->next_tile = 0;
   ctrl->arrive = 0;  // the next launch is ordered after this grid completes
@@ -501,7 +524,8 @@ __device__ __forceinline__ void store_pos(float* base, long long v, const float 
 }
 
 template <int DIM, int OPT>
-__device__ __forceinline__ void apply_update(const StepArgs& A, float* __restrict__ Yout, long long v,
+__device__ __forceinline__ void apply_update(const StepArgs& A, float* __restrict__ Yout, float* __restrict__ Sout,
+                                             long long v,
                                              const float (&yi)[DIM], float (&sv)[Layout<DIM, OPT>::SS > 0 ? Layout<DIM, OPT>::SS : 1],
                                              const float (&f)[DIM], float step, float bc1, float bc2,
                                              float& acc_n, float& acc_o, float& acc_bad) {
@@ -547,7 +571,7 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
       yn[d] = yi[d] + dl;
     }
   }
-  if constexpr (L::SS > 0) st_state<L::SS>(A.state + (size_t)v * L::SS, sv);
+  if constexpr (L::SS > 0) st_state<L::SS>(Sout + (size_t)v * L::SS, sv);
   float la[DIM];
 #pragma unroll
   for (int d = 0; d < DIM; ++d) la[d] = OPT == OPT_NEST ? yn[d] + A.h.beta * sv[d] : yn[d];  // optim.py:174-175
@@ -658,9 +682,9 @@ constexpr int kUnitCache = IVHD_UNIT_CACHE;  // unit words cached per block
 // are issued first, then ~20 instructions per entry.  Slots past the lane's
 // last entry are self pairs (zero contribution).
 template <int D, bool GCOL>
-__device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G, int deg,
-                                         const float* __restrict__ Yin, uint32_t v, float y0, float y1, float c,
-                                         long long gstep, float (&f)[2], float& e) {
+__device__ __forceinline__ void fast_row(const StepArgs& A, const uint32_t* __restrict__ cb, int G, int deg,
+                                         int ebase, const float* __restrict__ Yin, uint32_t v, float y0, float y1,
+                                         float c, long long gstep, float (&f)[2], float& e) {
   uint32_t cw[D];
   float2 p[D];
 #pragma unroll
@@ -687,14 +711,14 @@ __device__ __forceinline__ void fast_row(const uint32_t* __restrict__ cb, int G,
     ee += rn ? c * r * r : d2;
     dmask |= (unsigned)(rn && z) << q;
   }
-  if (dmask) {  // degenerate random pairs (forces.py:167-174)
+  if (dmask) {  // degenerate random pairs (forces.py:167-174): slot q is entry ebase + q * G
 #pragma unroll
     for (int q = 0; q < D; ++q) {
       if ((dmask >> q) & 1u) {
         float u[2];
-        degenerate_dir<2>(v, cw[q] & kIdMask, gstep, u);
-        fx = fmaf(c, u[0], fx);
-        fy = fmaf(c, u[1], fy);
+        degenerate_vec<2>(A, v, ebase + q * G, gstep, u);
+        fx += u[0];
+        fy += u[1];
       }
     }
   }
@@ -776,6 +800,10 @@ __device__ __noinline__ void peer_publish(const StepArgs& A, int* scratch, bool 
       }
     } else {  // fp64 kernel: tile partials already in tpart
       s = A.tpart[t];
+    }
+    if (t == A.pe.t0 && A.ctrl->need) {  // this rank met degenerate pairs without directions
+      s.w += kMissUnit;
+      A.ctrl->need = 0;
     }
     A.pe.tp_local[par + t] = s;
     for (int q = 0; q < A.pe.n_peers; ++q) A.pe.tp[q][par + t] = s;
@@ -902,6 +930,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
           mbar_arrive(&bar_b[s]);
         }
       };
+      const float* Sin = nullptr;  // current optimizer state (set after the dependency wait)
       auto issue_ys = [&](int k, const float* Yin) {  // positions + optimizer state of unit k
         const int s = k % kStages;
         unsigned char* st = smem_raw + s * SL::BYTES;
@@ -913,7 +942,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
         if constexpr (L::SS > 0) s_copy = ((uint32_t)nv * L::SS * 4 + 15) / 16 * 16;
         mbar_expect_tx(&bar_a[s], y_copy + s_copy);
         bulk_g2s(st + SL::Y_OFF, Yin + va * YS, y_copy, &bar_a[s]);
-        if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, A.state + va * L::SS, s_copy, &bar_a[s]);
+        if constexpr (L::SS > 0) bulk_g2s(st + SL::S_OFF, Sin + va * L::SS, s_copy, &bar_a[s]);
       };
       const int pre = min(my_units, kStages);
       int nf = pre, nc = pre;
@@ -930,6 +959,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
         for (int k = 0; k < pre; ++k) mbar_wait(&bar_b[k], 0);
       } else {
         const float* Yin = (A.fixed_io || !ctrl->cur) ? A.ybuf0 : A.ybuf1;
+        Sin = A.state + (ctrl->scur ? A.sstride : 0);
         if (lane == 0)
           for (int k = 0; k < pre; ++k) issue_ys(k, Yin);
         // Event loop: stages are claimed as consumers free them; a unit's
@@ -971,6 +1001,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     const long long gstep = ctrl->gstep;
     const float* __restrict__ Yin = ycur ? A.ybuf1 : A.ybuf0;
     float* __restrict__ Yout = ycur ? A.ybuf0 : A.ybuf1;
+    float* __restrict__ Sout = A.state + (ctrl->scur ? 0 : A.sstride);
     float bc1 = 1.f, bc2 = 1.f;  // Adam bias corrections (optim.py:203-204)
     if constexpr (OPT == OPT_ADAM) {
       const double tt = (double)(ctrl->adam_t + 1);
@@ -1026,7 +1057,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
               if (slots <= 8) {
                 switch (slots) {
 #define IVHD_FAST_CASE(D) \
-  case D: fast_row<D, GC>(cb, G, nl, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+  case D: fast_row<D, GC>(A, cb, G, nl, lg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
                   IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
                   IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
 #undef IVHD_FAST_CASE
@@ -1034,7 +1065,8 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
                 }
               } else {
                 for (int c0 = 0; c0 < nl; c0 += 8)
-                  fast_row<8, GC>(cb + c0 * G, G, nl - c0, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e);
+                  fast_row<8, GC>(A, cb + c0 * G, G, nl - c0, lg + c0 * G, Yin, (uint32_t)v, yi[0], yi[1], c,
+                                  gstep, ff, e);
               }
             };
             if (staged) run(std::false_type{}, colst + (beg - e0 + coff) + lg);
@@ -1083,16 +1115,10 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
 #pragma unroll
             for (int q = 0; q < kUnroll; ++q) {
               if ((dmask >> q) & 1u) {
-                const bool rn = cw[q] & kRandBit;
-                float t = rn ? 1.f : 0.f, w = rn ? c : 1.f;
-                if constexpr (WEIGHTED) {
-                  t = tw[q].x;
-                  w *= tw[q].y;
-                }
                 float uvec[DIM];
-                degenerate_dir<DIM>((uint32_t)v, cw[q] & kIdMask, gstep, uvec);
+                degenerate_vec<DIM>(A, (uint32_t)v, (int)(k0 + (uint32_t)(q * G) - beg), gstep, uvec);
 #pragma unroll
-                for (int d = 0; d < DIM; ++d) f[d] = fmaf(w * t, uvec[d], f[d]);
+                for (int d = 0; d < DIM; ++d) f[d] += uvec[d];
               }
             }
           }
@@ -1116,7 +1142,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
             float sv[SSX];
 #pragma unroll
             for (int q = 0; q < SSX; ++q) sv[q] = L::SS > 0 ? ss[grp * SSX + q] : 0.f;
-            apply_update<DIM, OPT>(A, Yout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
+            apply_update<DIM, OPT>(A, Yout, Sout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
           }
         }
       }

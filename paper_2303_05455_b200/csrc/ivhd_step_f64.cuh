@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
   const int ycur = A.fixed_io ? 0 : ctrl->cur;
   const double* __restrict__ Yin = reinterpret_cast<const double*>(ycur ? A.ybuf1 : A.ybuf0);
   double* __restrict__ Yout = reinterpret_cast<double*>(ycur ? A.ybuf0 : A.ybuf1);
-  double* __restrict__ S = reinterpret_cast<double*>(A.state);
+  const double* __restrict__ Sin = reinterpret_cast<const double*>(A.state + (ctrl->scur ? A.sstride : 0));
+  double* __restrict__ Sout = reinterpret_cast<double*>(A.state + (ctrl->scur ? 0 : A.sstride));
   const double c = ctrl->c, alpha = ctrl->step;
   const long long gstep = ctrl->gstep;
   const double tt = (double)(ctrl->adam_t + 1);
@@ -109,15 +110,16 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
         double yo[DIM];
 #pragma unroll
         for (int d = 0; d < DIM; ++d) yo[d] = Yin[(size_t)o * FL::DP + d];
-        if (entry_f64<DIM, NORM>(yi, yo, t_, w, f, e)) {  // forces.py:167-174
+        if (entry_f64<DIM, NORM>(yi, yo, t_, w, f, e)) {  // forces.py:167-174 (host-drawn direction)
           float u[DIM];
-          degenerate_dir<DIM>((uint32_t)v, o, gstep, u);
+          degenerate_vec<DIM>(A, (uint32_t)v, (int)(k - beg), gstep, u);
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) f[d] += w * t_ * (double)u[d];
+          for (int d = 0; d < DIM; ++d) f[d] += (double)u[d];
         }
       }
       // Adam (optim.py:195-205) with grad = -2 f (optim.py:259-263)
-      double* sv = S + (size_t)v * FL::SD;
+      const double* sv = Sin + (size_t)v * FL::SD;
+      double* so = Sout + (size_t)v * FL::SD;
       double yn[DIM];
       bool ok = true;
 #pragma unroll
@@ -125,8 +127,8 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
         const double g = -2.0 * f[d];
         const double vv = A.h.gv_d * sv[d] + (1.0 - A.h.gv_d) * g;
         const double ss = A.h.gs_d * sv[FL::DP + d] + (1.0 - A.h.gs_d) * g * g;
-        sv[d] = vv;
-        sv[FL::DP + d] = ss;
+        so[d] = vv;
+        so[FL::DP + d] = ss;
         yn[d] = yi[d] - alpha * (vv / bc1) / (A.h.eps_d + sqrt(ss / bc2));
         Yout[v * FL::DP + d] = yn[d];
         ok &= isfinite(yn[d]);

@@ -156,27 +156,72 @@ class DeviceEmbedding:
         return v.value
 
     # ---------------------------------------------------------------- loops
+    # Resolves the directions of degenerate random pairs when the device
+    # pauses (degenerate.py): callable(slot, rows, entries) -> (rows,
+    # entries, vecs) drawn from the run's generator; set by run_embedding's
+    # session, which owns the connection lists and the generator.
+    degenerate_resolver = None
+
+    def _resolve(self, slot):
+        n = ctypes.c_int64()
+        self._check(self.lib.ivhd_degenerate_pending(self.h, 0, ctypes.byref(n), None, None))
+        rows = np.empty(n.value, dtype=np.int32)
+        ent = np.empty(n.value, dtype=np.int32)
+        self._check(self.lib.ivhd_degenerate_pending(self.h, n.value, ctypes.byref(n),
+                                                     rows.ctypes.data_as(c_i32p), ent.ctypes.data_as(c_i32p)))
+        if self.degenerate_resolver is None:
+            from .errors import DeviceError
+
+            raise DeviceError("random pairs at zero distance need directions from the run's generator "
+                              "(forces.py:167-174): use run_embedding / compute_forces, or set "
+                              "DeviceEmbedding.degenerate_resolver")
+        t_rows, t_ent, t_vec = self.degenerate_resolver(slot, rows, ent)
+        t_rows, t_ent, t_vec = i32(t_rows), i32(t_ent), f64(t_vec)
+        self._check(self.lib.ivhd_set_degenerate(self.h, len(t_rows), t_rows.ctypes.data_as(c_i32p),
+                                                 t_ent.ctypes.data_as(c_i32p), t_vec.ctypes.data_as(c_f64p)))
+
     def run(self, slot, norm, c, n_iter):
-        """Run n_iter iterations; returns (stress[], step[], done, diverged)."""
-        stress = np.empty(max(int(n_iter), 1))
-        step = np.empty(max(int(n_iter), 1))
-        done = ctypes.c_int64(0)
-        code = self.lib.ivhd_run(self.h, int(slot), _lib.NORM[norm], float(c), int(n_iter),
-                                 stress.ctypes.data_as(c_f64p), step.ctypes.data_as(c_f64p),
-                                 ctypes.byref(done))
-        if code == _lib.ERR_DIVERGED:
+        """Run n_iter iterations; returns (stress[], step[], done, diverged).
+        An iteration that meets degenerate random pairs pauses on the device;
+        the directions are drawn on the host and the iteration re-runs."""
+        n_iter = int(n_iter)
+        parts_s, parts_b, total = [], [], 0
+        while True:
+            left = n_iter - total
+            stress = np.empty(max(left, 1))
+            step = np.empty(max(left, 1))
+            done = ctypes.c_int64(0)
+            code = self.lib.ivhd_run(self.h, int(slot), _lib.NORM[norm], float(c), left,
+                                     stress.ctypes.data_as(c_f64p), step.ctypes.data_as(c_f64p),
+                                     ctypes.byref(done))
             d = done.value
-            return stress[: d + 1], step[: d + 1], d, True
-        self._check(code)
-        return stress[: done.value], step[: done.value], done.value, False
+            if code == _lib.PAUSED_DEGENERATE:
+                parts_s.append(stress[:d])
+                parts_b.append(step[:d])
+                total += d
+                self._resolve(slot)
+                continue
+            if code == _lib.ERR_DIVERGED:
+                parts_s.append(stress[: d + 1])
+                parts_b.append(step[: d + 1])
+                return np.concatenate(parts_s), np.concatenate(parts_b), total + d, True
+            self._check(code)
+            parts_s.append(stress[:d])
+            parts_b.append(step[:d])
+            return np.concatenate(parts_s), np.concatenate(parts_b), total + d, False
 
     def compute_forces(self, slot, norm, c, y):
         y = f64(y)
         f = np.empty((self.m, self.dim))
         e = ctypes.c_double()
-        self._check(self.lib.ivhd_compute_forces(self.h, int(slot), _lib.NORM[norm], float(c),
-                                                 y.ctypes.data_as(c_f64p), f.ctypes.data_as(c_f64p),
-                                                 ctypes.byref(e)))
+        for _ in range(2):
+            code = self.lib.ivhd_compute_forces(self.h, int(slot), _lib.NORM[norm], float(c),
+                                                y.ctypes.data_as(c_f64p), f.ctypes.data_as(c_f64p),
+                                                ctypes.byref(e))
+            if code != _lib.PAUSED_DEGENERATE:
+                break
+            self._resolve(slot)  # directions drawn on the host, then evaluate again
+        self._check(code)
         return f, e.value
 
     def stress(self, slot, norm, c, y):

@@ -244,6 +244,9 @@ class _Session:
 
         # one GPU (DeviceEmbedding) or this rank's shard (sharded.ShardedEmbedding)
         self.dev = (make_device or DeviceEmbedding)(m, config.target_dim, device=device)
+        # degenerate random pairs draw their directions from this run's
+        # generator on the host (degenerate.py, forces.py:167-174)
+        getattr(self.dev, "device_embedding", self.dev).degenerate_resolver = self.degenerate_directions
         self.dev.set_optimizer(resolve_optimizer(config.optimizer, m, config.integrator, config.opt))
         # one PCG64 stream, reference order (engine.py:165, 214-215): the
         # layout, then the random partners — drawn on the device (numpy's
@@ -333,6 +336,32 @@ class _Session:
             np.concatenate([nn_t[keep], rn_t]),
             np.concatenate([scale, np.ones(len(rn_edges))]))
         self.filtered_ready = True
+
+    def connection_arrays(self, slot):
+        """(src, dst, w * t) of connection set `slot` in the reference's
+        connection order (engine.py:225-262; slot 1 = rnn_filtered, 270-286)."""
+        nn_edges, rn_edges = self._edge_arrays()
+        if self.euclid:
+            nn_t, rn_t = self._targets()
+        else:
+            nn_t, rn_t = np.zeros(len(nn_edges)), np.ones(len(rn_edges))
+        nn_w = np.ones(len(nn_edges))
+        if slot == 1:
+            keep = rnn_edge_filter(nn_edges, self.nn_sets, self.helper)
+            ncols = self.nn_sets.shape[1]
+            kept_per = keep.reshape(-1, ncols).sum(axis=1)
+            nn_edges, nn_t = nn_edges[keep], nn_t[keep]
+            nn_w = (ncols / kept_per)[nn_edges[:, 0]]
+        src = np.concatenate([nn_edges[:, 0], rn_edges[:, 0]])
+        dst = np.concatenate([nn_edges[:, 1], rn_edges[:, 1]])
+        wt = np.concatenate([nn_w * nn_t, self.c * rn_t])
+        return src, dst, wt
+
+    def degenerate_directions(self, slot, rows, entries):
+        from . import degenerate
+
+        src, dst, wt = self.connection_arrays(slot)
+        return degenerate.table(rows, entries, src, dst, wt, self.rng, self.dim)
 
     def resample(self):
         """engine.py:264-268: new random partners from the same stream."""

@@ -5,8 +5,8 @@ Differences from the reference, by design:
 * arithmetic is float32 per connection with float64 reductions (the kernel's
   contract; normwise relative agreement ~1e-7);
 * the degenerate random-pair fallback (d == 0, t != 0; forces.py:167-174)
-  draws its unit direction from a device counter hash instead of `rng`, so
-  `rng` is accepted and ignored (the magnitude w*t is the same).
+  draws from `rng` (default_rng(0) when None) on the host, exactly as the
+  reference does (degenerate.py); the kernel then applies the directions.
 """
 
 import threading
@@ -104,11 +104,21 @@ def _check_norm(norm):
 def compute_forces(positions, conn, c, norm=NORM_L2, rng=None, threads=1, with_stress=False,
                    device=0):
     """Force = -1/2 grad E (forces.py:139-181) on the GPU."""
-    del rng, threads
+    del threads
     _check_norm(norm)
     y = np.asarray(positions, dtype=np.float64)
     m, dim = y.shape
     dev = _device_for(m, dim, conn, device)
+
+    def directions(slot, rows, entries):  # forces.py:167-171 (rng None -> default_rng(0))
+        from . import degenerate
+
+        gen = rng if rng is not None else np.random.default_rng(0)
+        wt = conn.weights(c) * np.asarray(conn.targets, dtype=np.float64)
+        e_ = np.asarray(conn.edges)
+        return degenerate.table(rows, entries, e_[:, 0], e_[:, 1], wt, gen, dim)
+
+    dev.degenerate_resolver = directions
     f, e = dev.compute_forces(0, norm, c, y)
     return (f, e) if with_stress else f
 

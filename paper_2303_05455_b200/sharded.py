@@ -135,6 +135,11 @@ class ShardedEmbedding:
             raise AttributeError(name)
         return getattr(self.backend, name)
 
+    @property
+    def device_embedding(self):
+        """The rank's DeviceEmbedding (None for a custom backend)."""
+        return getattr(self.backend, "dev", None)
+
     def launches_per_iteration(self):
         """Kernels per iteration: p2p = the step kernel (it publishes to the
         peers itself) + the finalizer; nccl = local update, tile fold,
@@ -249,4 +254,12 @@ def run_embedding_distributed(graph=None, config=None, dataset=None, helper_grap
 
     with torch.cuda.stream(stream):
         sess = _Session(graph, config, dataset, helper_graph, device, make_device=make)
+        if world > 1:  # every rank draws the directions of all ranks' degenerate pairs, in one order
+            def gathered(slot, rows, entries):
+                parts = [None] * world
+                dist.all_gather_object(parts, (np.asarray(rows).tolist(), np.asarray(entries).tolist()), group=group)
+                return sess.degenerate_directions(slot, sum((p[0] for p in parts), []),
+                                                  sum((p[1] for p in parts), []))
+
+            sess.dev.device_embedding.degenerate_resolver = gathered
         return _drive(sess, config, None)

@@ -75,11 +75,12 @@ def test_hand_values():
     np.testing.assert_allclose(f, 0.0, atol=1e-7)
     f = P.compute_forces(np.array([[0.0, 0.0], [0.5, 0.0]]), pair(1.0, True), c=0.1)
     assert f[0, 0] < 0 < f[1, 0]
-    # degenerate random pair: unit direction of magnitude w*t, opposite on the partner
+    # degenerate random pair: the reference's default_rng(0) direction, magnitude w*t
     f = P.compute_forces(np.zeros((2, 2)), pair(1.0, True), c=0.1)
-    assert np.isfinite(f).all()
-    assert np.linalg.norm(f[0]) == pytest.approx(0.1, rel=1e-6)
-    np.testing.assert_allclose(f[0], -f[1], rtol=1e-6)
+    u = np.random.default_rng(0).standard_normal((1, 2))
+    u /= np.linalg.norm(u)
+    np.testing.assert_allclose(f[0], 0.1 * u[0], rtol=1e-6)
+    np.testing.assert_allclose(f[1], -0.1 * u[0], rtol=1e-6)
     assert P.stress(np.zeros((2, 2)), pair(1.0, True), c=0.1) == pytest.approx(0.1, rel=1e-6)
     assert P.stress(np.array([[0.0, 0.0], [2.0, 0.0]]), pair(0.0, False), c=0.5) == pytest.approx(4.0)
 
@@ -285,3 +286,74 @@ def test_switch_force_directed_to_adam_mid_run():
         ref.step()
     assert normwise(res.embedding.points, ref.Y) < 1e-5
     np.testing.assert_allclose(res.trace.stress, ref.trace_stress, rtol=1e-5)
+
+
+# ---------------------------------------- degenerate random pairs (a8)
+
+DEG = load("degenerate_cases.npz")
+
+
+@pytest.mark.parametrize("k", range(int(DEG["n_cases"])))
+def test_degenerate_pairs_match_reference_golden(k):
+    """forces.py:158-174 through the CUDA operator: the kernel reports the
+    zero-distance random pairs, the host draws their directions from `rng`
+    (default_rng(0) when None) in connection order, the kernel applies them."""
+    p = f"d{k}_"
+    sc = DEG[p + "scale"]
+    conn = P.ConnectionSet(DEG[p + "edges"], DEG[p + "targets"], DEG[p + "is_random"],
+                           None if sc.size == 0 else sc)
+    seed = int(DEG[p + "seed"])
+    gen = None if seed < 0 else np.random.default_rng(seed)
+    f, e = P.compute_forces(DEG[p + "Y"], conn, float(DEG[p + "c"]), rng=gen, with_stress=True)
+    assert normwise(f, DEG[p + "force"]) < 1e-5
+    assert e == pytest.approx(float(DEG[p + "stress"]), rel=1e-5)
+    if gen is not None:  # the draw consumed the caller's generator like the reference's
+        ref = np.random.default_rng(seed)
+        n_bad = 0
+        y = DEG[p + "Y"]
+        ed = DEG[p + "edges"]
+        t = DEG[p + "targets"]
+        n_bad = int(((np.abs(y[ed[:, 0]] - y[ed[:, 1]]).sum(1) == 0) & (t != 0)).sum())
+        ref.standard_normal((n_bad, y.shape[1]))
+        assert gen.bit_generator.state == ref.bit_generator.state
+
+
+@pytest.mark.parametrize("opt", ["force-directed", "nesterov", "adam"])
+def test_loop_pauses_for_degenerate_pairs_and_follows_the_oracle(opt):
+    """The loop meets random pairs at zero distance (several rn partners
+    placed on their source vertex): the iteration pauses on the device
+    (nothing committed, state double buffer not advanced), the host draws the
+    directions from the run's generator in connection order, the iteration is
+    re-run — positions, stress and the generator state then follow the
+    oracle (the reference's draw) step by step."""
+    from paper_2303_05455_b200 import degenerate
+    from paper_2303_05455_b200.config import resolve_optimizer
+    from paper_2303_05455_b200.device import DeviceEmbedding
+
+    nb = planted_graph(5000, 2, seed=4)
+    orc = OracleRun(nb, nn=2, rn=1, c=0.1, iterations=6, seed=9, optimizer=opt)
+    y0 = orc.Y.copy()
+    src = np.arange(0, 5000, 97)
+    y0[orc.rn_assign[src, 0]] = y0[src]  # coincident random pairs
+    orc.Y = y0.copy()
+    gen = np.random.Generator(np.random.PCG64())
+    gen.bit_generator.state = orc.rng.bit_generator.state
+    conn = orc.full
+    dev = DeviceEmbedding(5000, 2)
+    dev.set_optimizer(resolve_optimizer(opt, 5000))
+    dev.set_positions(y0)
+    dev.set_graph(0, nb, orc.rn_assign)
+    calls = []
+
+    def resolver(slot, rows, entries):
+        calls.append(len(rows))
+        return degenerate.table(rows, entries, conn.src, conn.dst, conn.weights(0.1) * conn.target, gen, 2)
+
+    dev.degenerate_resolver = resolver
+    st, bb, done, div = dev.run(0, "l2", 0.1, 6)
+    assert done == 6 and not div and calls and calls[0] >= 2 * len(src) - 4
+    orc.run(6)
+    assert normwise(dev.positions(), orc.Y) < 1e-5
+    np.testing.assert_allclose(st, orc.trace_stress, rtol=1e-5)
+    assert gen.bit_generator.state == orc.rng.bit_generator.state
+    dev.close()
