@@ -17,8 +17,7 @@
 #include <vector>
 
 #include "../../include/ivhd_b200.h"
-#include "ivhd_step.cuh"
-#include "ivhd_step_f64.cuh"
+#include "ivhd_kernels.h"
 #include "ivhd_rng.cuh"
 
 using namespace ivhd;
@@ -47,13 +46,6 @@ struct CsrSlot {
   bool valid = false;
 };
 
-using KernelFn = void (*)(StepArgs);
-
-struct KernelInfo {
-  KernelFn fn;
-  int smem;
-  int threads = kThreads;
-};
 
 struct GraphKey {
   int slot, norm, opt, G;
@@ -222,35 +214,6 @@ inline int ys_of(int dim, int opt) {
 inline bool f64_of(int opt) { return opt == OPT_ADAM; }
 
 // ------------------------------------------------------------ kernel table
-
-template <int DIM, int OPT, bool W, int N>
-KernelInfo kinfo() {
-  return KernelInfo{step_kernel<DIM, OPT, W, N>, step_smem_bytes<DIM, OPT, W, N>()};
-}
-
-template <int DIM, bool W, int N>
-KernelInfo pick_opt(int opt) {
-  switch (opt) {
-    case OPT_ADAM: return KernelInfo{step_kernel_f64<DIM, W, N>, 0, kBlock};
-    case OPT_FD: return kinfo<DIM, OPT_FD, W, N>();
-    case OPT_SGD: return kinfo<DIM, OPT_SGD, W, N>();
-    case OPT_MOM: return kinfo<DIM, OPT_MOM, W, N>();
-    case OPT_NEST: return kinfo<DIM, OPT_NEST, W, N>();
-    case OPT_ADADELTA: return kinfo<DIM, OPT_ADADELTA, W, N>();
-    default: return kinfo<DIM, OPT_NONE, W, N>();
-  }
-}
-
-template <int DIM, bool W>
-KernelInfo pick_norm(int opt, int norm) {
-  return norm == 0 ? pick_opt<DIM, W, 0>(opt) : pick_opt<DIM, W, 1>(opt);
-}
-
-// weighted = per-entry {target, scale} stream present (euclidean / RNN sets)
-KernelInfo pick_kernel(int dim, int opt, bool weighted, int norm) {
-  if (dim == 2) return weighted ? pick_norm<2, true>(opt, norm) : pick_norm<2, false>(opt, norm);
-  return weighted ? pick_norm<3, true>(opt, norm) : pick_norm<3, false>(opt, norm);
-}
 
 KernelFn pick_finalize_peer(int opt) {
   switch (opt) {
@@ -611,6 +574,46 @@ __global__ void k_peer_barrier(PeerArgs pe, Ctrl* ctrl) {
   if (threadIdx.x == 0) pe.stamp[1] = s;
 }
 
+// Positions a paused iteration evaluated its forces at, in the operator
+// layout (ys_out floats per vertex): y itself, or Nesterov's y + beta v (at
+// float offset `off` of the record).
+__global__ void k_eval_positions(const float* __restrict__ y, int64_t m, int ys_in, int off, int dim, int ys_out,
+                                 float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < ys_out; ++d) out[i * ys_out + d] = d < dim ? y[i * ys_in + off + d] : 0.f;
+}
+
+// Undo the in-place fp32 state update of a paused iteration from the forces
+// it used (optim.py:95-236 solved for the old state; recovered to rounding).
+template <int DIM, int OPT>
+__global__ void k_unstep(float* __restrict__ state, const double* __restrict__ force, int64_t m, float step, Hyper h) {
+  using L = Layout<DIM, OPT>;
+  constexpr int V = DIM == 2 ? 2 : 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    float* sv = state + i * L::SS;
+    for (int d = 0; d < DIM; ++d) {
+      const double f = force[i * DIM + d], g = -2.0 * f;
+      if constexpr (OPT == OPT_FD) {  // dn = a d + b f
+        sv[d] = (float)(((double)sv[d] - (double)(step * (float)f)) / (double)h.a);
+      } else if constexpr (OPT == OPT_MOM || OPT == OPT_NEST) {  // v' = beta v - alpha g
+        sv[d] = (float)(((double)sv[d] + (double)step * g) / (double)h.beta);
+      } else if constexpr (OPT == OPT_ADADELTA) {
+        const double rho = h.rho, eps = h.eps, sg_new = sv[d], sd_new = sv[V + d];
+        const double k = (double)step * step * g * g / (sg_new + eps);
+        sv[d] = (float)((sg_new - (1.0 - rho) * g * g) / rho);
+        sv[V + d] = (float)((sd_new - (1.0 - rho) * k * eps) / (rho + (1.0 - rho) * k));
+      }
+    }
+  }
+}
+
+// {target, scale} per entry of a binary connection set (rn -> 1, nn -> 0;
+// scale 1): lets the weighted kernel instantiation re-run a paused iteration.
+__global__ void k_binary_ew(const uint32_t* __restrict__ col, int64_t n, float2* __restrict__ ew) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    ew[k] = make_float2((col[k] & kRandBit) ? 1.f : 0.f, 1.f);
+}
+
 // fixed-order reduction of partial tiles into one double4 (operator calls)
 __global__ void __launch_bounds__(kBlock) k_reduce_partials(const double4* __restrict__ p, int n,
                                                             double4* __restrict__ out) {
@@ -660,6 +663,7 @@ void drop_graphs(ivhd_ctx* ctx) {
 
 int ys_now(ivhd_ctx* ctx);
 int ss_now(ivhd_ctx* ctx);
+int64_t state_stride(ivhd_ctx* ctx);
 float* state_buf(ivhd_ctx* ctx, int b);
 int pull_ctrl(ivhd_ctx* ctx);
 
@@ -954,7 +958,7 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   A.ybuf0 = ctx->ybuf[0];
   A.ybuf1 = ctx->ybuf[1];
   A.state = ctx->state;
-  A.sstride = (long long)ctx->state_fpv * ctx->v_cap;
+  A.sstride = state_stride(ctx);
   A.dg_key = ctx->dg_key;
   A.dg_vec = ctx->dg_vec;
   A.miss_n = ctx->miss_n;
@@ -1038,8 +1042,12 @@ int upload_stage(ivhd_ctx* ctx, const double* host, int64_t count) {
 
 int vel_stride(int dim) { return dim == 2 ? 2 : 4; }
 
-// optimizer-state buffer b (0/1); ctrl.scur names the current one
-float* state_buf(ivhd_ctx* ctx, int b) { return ctx->state + (size_t)b * ctx->state_fpv * ctx->v_cap; }
+// Optimizer-state buffer b (0/1); ctrl.scur names the current one.  Only the
+// fp64 Adam kernel double-buffers (stride > 0); the fp32 kernels update in
+// place (stride 0: both indices name buffer 0) — a paused iteration's state is
+// recovered by inverting the update instead (resume_degenerate).
+int64_t state_stride(ivhd_ctx* ctx) { return f64_of(ctx->opt.kind) ? (int64_t)ctx->state_fpv * ctx->v_cap : 0; }
+float* state_buf(ivhd_ctx* ctx, int b) { return ctx->state + (size_t)b * state_stride(ctx); }
 
 int ys_now(ivhd_ctx* ctx) { return ys_of(ctx->dim, ctx->opt.kind); }
 
@@ -1651,6 +1659,97 @@ static int ensure_trace(ivhd_ctx* ctx, int64_t n) {
 static int peer_masks(ivhd_ctx* ctx);
 static int peer_pull(ivhd_ctx* ctx, bool barrier);
 
+static void launch_unstep(ivhd_ctx* ctx, float* state, float step) {
+  const int g = grid_for(ctx->m, ctx->sm_count);
+  cudaStream_t st = ctx->stream;
+  const double* f = ctx->op_force;
+  const int64_t m = ctx->m;
+  const Hyper h = ctx->hyper;
+  const bool d2 = ctx->dim == 2;
+  switch (ctx->opt.kind) {  // SGD keeps no state
+    case OPT_FD:
+      if (d2) k_unstep<2, OPT_FD><<<g, 256, 0, st>>>(state, f, m, step, h);
+      else k_unstep<3, OPT_FD><<<g, 256, 0, st>>>(state, f, m, step, h);
+      break;
+    case OPT_MOM:
+      if (d2) k_unstep<2, OPT_MOM><<<g, 256, 0, st>>>(state, f, m, step, h);
+      else k_unstep<3, OPT_MOM><<<g, 256, 0, st>>>(state, f, m, step, h);
+      break;
+    case OPT_NEST:
+      if (d2) k_unstep<2, OPT_NEST><<<g, 256, 0, st>>>(state, f, m, step, h);
+      else k_unstep<3, OPT_NEST><<<g, 256, 0, st>>>(state, f, m, step, h);
+      break;
+    case OPT_ADADELTA:
+      if (d2) k_unstep<2, OPT_ADADELTA><<<g, 256, 0, st>>>(state, f, m, step, h);
+      else k_unstep<3, OPT_ADADELTA><<<g, 256, 0, st>>>(state, f, m, step, h);
+      break;
+    default: break;
+  }
+}
+
+// Before re-running an iteration that paused at degenerate pairs (forces.py:
+// 167-174): the fp32 kernels updated the optimizer state in place, so recover
+// the old state by inverting that update with the forces the paused
+// iteration used (the same kernel family at the same positions, without the
+// missing directions); then choose the re-run kernel: the 2-D binary fast
+// path only records degenerate pairs, so a binary set re-runs through the
+// weighted instantiation (general path, applies the table) with {t, 1}
+// entry weights built here.  The fp64 Adam kernel double-buffers its state
+// and re-runs as is.
+static int resume_degenerate(ivhd_ctx* ctx, int slot, int norm, StepArgs& R, KernelInfo& k, float2** tmp_ew) {
+  const CsrSlot& S = ctx->slots[slot];
+  const int opt = ctx->opt.kind, dim = ctx->dim;
+  if (f64_of(opt)) return IVHD_OK;
+  if (!ctx->op_y) CU(ctx, dalloc(ctx, &ctx->op_y, sizeof(float) * 4 * ctx->v_cap));
+  if (!ctx->op_force) CU(ctx, dalloc(ctx, &ctx->op_force, sizeof(double) * 3 * ctx->v_cap));
+  const int ys = ys_now(ctx), ys_op = dim == 2 ? 2 : 4, off = opt == OPT_NEST ? (dim == 2 ? 2 : 4) : 0;
+  k_eval_positions<<<grid_for(ctx->m, ctx->sm_count), 256, 0, ctx->stream>>>(
+      ctx->ybuf[ctx->ctrl_h->cur], ctx->m, ys, off, dim, ys_op, ctx->op_y);
+  Ctrl oc{};
+  oc.c = ctx->ctrl_h->c;
+  oc.gstep = ctx->ctrl_h->gstep;
+  CU(ctx, cudaMemcpyAsync(ctx->opctrl, &oc, sizeof(Ctrl), cudaMemcpyHostToDevice, ctx->stream));
+  StepArgs O{};
+  O.row_ptr = S.row_ptr;
+  O.col = S.col;
+  O.ew = S.ew;
+  O.ybuf0 = O.ybuf1 = ctx->op_y;
+  O.partial = ctx->partial;
+  O.ctrl = ctx->opctrl;
+  O.force_out = ctx->op_force;
+  O.dg_key = ctx->dg_key;
+  O.dg_vec = ctx->dg_vec;
+  O.miss_n = ctx->miss_n;
+  O.miss = ctx->miss;
+  O.miss_cap = ctx->miss_cap;
+  O.tile_g = S.tile_g;
+  O.units = S.units;
+  O.v_begin = 0;
+  O.v_end = ctx->m;
+  O.tile_v = ctx->tile_v;
+  O.n_tiles = S.unit_base[ctx->n_tiles];
+  O.n_tiles_global = O.n_tiles;
+  O.norm = norm;
+  TRY(launch_step(ctx, pick_kernel(dim, OPT_NONE, S.ew != nullptr, norm), O));
+  float* st = state_buf(ctx, 0);
+  launch_unstep(ctx, st, (float)ctx->ctrl_h->step);
+  CU(ctx, cudaGetLastError());
+  CU(ctx, cudaMemsetAsync(ctx->miss_n, 0, sizeof(int), ctx->stream));
+  const bool fast = dim == 2 && S.ew == nullptr && norm == IVHD_NORM_L2 && opt != OPT_NEST;
+  if (fast) {
+    CU(ctx, dalloc(ctx, tmp_ew, sizeof(float2) * std::max<int64_t>(S.n, 1)));
+    k_binary_ew<<<grid_for(S.n, ctx->sm_count), 256, 0, ctx->stream>>>(S.col, S.n, *tmp_ew);
+    CU(ctx, cudaGetLastError());
+    R.ew = *tmp_ew;
+    k = pick_kernel(dim, opt, true, norm, ctx->peer_on);
+    if (R.boff) {  // the cost-balanced schedule was built for the fast kernel's grid: plain round robin
+      R.units = S.units;
+      R.boff = nullptr;
+    }
+  }
+  return IVHD_OK;
+}
+
 // After a run segment: status, trace and done count (engine.py:373-377 contract).
 static int read_trace(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t* done_out) {
   TRY(pull_ctrl(ctx));
@@ -1706,8 +1805,8 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   TRY(push_ctrl(ctx));
   CU(ctx, cudaMemsetAsync(ctx->miss_n, 0, sizeof(int), ctx->stream));
   const CsrSlot& S = ctx->slots[slot];
-  KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm);
   const bool peer = ctx->peer_on;
+  KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm, peer);
   if (peer && ctx->masks_stale) TRY(peer_masks(ctx));
   StepArgs A = make_args(ctx, slot, norm, peer ? 0 : 1);
   if (!peer) {
@@ -1725,6 +1824,18 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
     return IVHD_OK;
   };
   int64_t left = n_iter;
+  if (left > 0 && ctx->ctrl_h->dg_n > 0 && ctx->ctrl_h->dg_gstep == ctx->ctrl_h->gstep) {
+    // re-run of the iteration that paused at degenerate pairs, with the
+    // host-drawn directions (one launch, outside the graphs)
+    StepArgs R = A;
+    KernelInfo k = fn;
+    float2* tmp_ew = nullptr;
+    TRY(resume_degenerate(ctx, slot, norm, R, k, &tmp_ew));
+    const int rc = launch_step(ctx, k, R);
+    dfree(ctx, tmp_ew);  // stream-ordered after the launch
+    TRY(rc);
+    --left;
+  }
   const int chunk = ctx->graph_chunk;
   if (left >= chunk) {
     const GraphKey key{slot, norm, ctx->opt.kind, (S.ew != nullptr ? 1 : 0) | (peer ? 2 : 0)};
@@ -1799,7 +1910,19 @@ static int op_launch(ivhd_ctx* ctx, int slot, int norm, double c, const double* 
   A.n_tiles_global = A.n_tiles;
   A.norm = norm;
   A.fuse_finalize = 0;
-  TRY(launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, S.ew != nullptr, norm), A));
+  // with host-drawn directions for this evaluation, a binary 2-D L2 set runs
+  // through the weighted instantiation (the fast path only records pairs)
+  float2* tmp_ew = nullptr;
+  bool weighted = S.ew != nullptr;
+  if (oc.dg_n > 0 && oc.dg_gstep == oc.gstep && !weighted && ctx->dim == 2 && norm == IVHD_NORM_L2) {
+    CU(ctx, dalloc(ctx, &tmp_ew, sizeof(float2) * std::max<int64_t>(S.n, 1)));
+    k_binary_ew<<<grid_for(S.n, ctx->sm_count), 256, 0, ctx->stream>>>(S.col, S.n, tmp_ew);
+    A.ew = tmp_ew;
+    weighted = true;
+  }
+  const int lrc = launch_step(ctx, pick_kernel(ctx->dim, OPT_NONE, weighted, norm), A);
+  dfree(ctx, tmp_ew);
+  TRY(lrc);
   k_reduce_partials<<<1, kBlock, 0, ctx->stream>>>(ctx->partial, A.n_tiles, ctx->red_out);
   CU(ctx, cudaGetLastError());
   double4 red;
@@ -2076,7 +2199,7 @@ int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out) {
       TRY(peer_masks(ctx));
       A.pe = ctx->pe;
     }
-    if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm), A));
+    if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm, true), A));
     if (exchange_out) *exchange_out = 0;
     return IVHD_OK;
   }

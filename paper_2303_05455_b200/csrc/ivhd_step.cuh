@@ -231,27 +231,35 @@ __device__ __forceinline__ void gather(const float* __restrict__ Y, uint32_t j, 
 // turns into a pause (status 2, nothing committed, state not advanced).  The
 // host draws the directions in connection order, fills the table and the
 // iteration is re-run.  Measure-zero: after a random init it never happens.
-template <int DIM>
-__device__ __noinline__ void degenerate_vec(const StepArgs& A, uint32_t v, int e, long long gstep,
-                                           float (&u)[DIM]) {
-  const Ctrl* c = A.ctrl;
-#pragma unroll
-  for (int d = 0; d < DIM; ++d) u[d] = 0.f;
+__device__ __forceinline__ void record_degenerate(Ctrl* c, int* miss_n, int2* miss, int miss_cap, uint32_t v, int e) {
+  const int slot = atomicAdd(miss_n, 1);
+  if (slot < miss_cap) miss[slot] = make_int2((int)v, e);
+  atomicExch(&c->need, 1);
+}
+
+// (out of line, rare path: plain pointers only, so the caller keeps the
+// kernel parameters in the constant bank instead of copying them to a stack)
+static __device__ __noinline__ float4 degenerate_lookup(Ctrl* c, const int2* key, const float4* vec, int* miss_n,
+                                                int2* miss, int miss_cap, uint32_t v, int e, long long gstep) {
   if (c->dg_gstep == gstep) {
     for (int i = 0; i < c->dg_n; ++i) {
-      const int2 k = A.dg_key[i];
-      if (k.x == (int)v && k.y == e) {
-        const float4 q = A.dg_vec[i];
-        u[0] = q.x;
-        u[1] = q.y;
-        if constexpr (DIM == 3) u[2] = q.z;
-        return;
-      }
+      const int2 k = key[i];
+      if (k.x == (int)v && k.y == e) return vec[i];
     }
   }
-  const int slot = atomicAdd(A.miss_n, 1);
-  if (slot < A.miss_cap) A.miss[slot] = make_int2((int)v, e);
-  atomicExch(&A.ctrl->need, 1);
+  const int slot = atomicAdd(miss_n, 1);
+  if (slot < miss_cap) miss[slot] = make_int2((int)v, e);
+  atomicExch(&c->need, 1);
+  return make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+template <int DIM>
+__device__ __forceinline__ void degenerate_vec(const StepArgs& A, uint32_t v, int e, long long gstep,
+                                               float (&u)[DIM]) {
+  const float4 q = degenerate_lookup(A.ctrl, A.dg_key, A.dg_vec, A.miss_n, A.miss, A.miss_cap, v, e, gstep);
+  u[0] = q.x;
+  u[1] = q.y;
+  if constexpr (DIM == 3) u[2] = q.z;
 }
 
 // ------------------------------------------------------------------ entries
@@ -523,7 +531,7 @@ __device__ __forceinline__ void store_pos(float* base, long long v, const float 
   }
 }
 
-template <int DIM, int OPT>
+template <int DIM, int OPT, bool PEER>
 __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restrict__ Yout, float* __restrict__ Sout,
                                              long long v,
                                              const float (&yi)[DIM], float (&sv)[Layout<DIM, OPT>::SS > 0 ? Layout<DIM, OPT>::SS : 1],
@@ -576,7 +584,7 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
 #pragma unroll
   for (int d = 0; d < DIM; ++d) la[d] = OPT == OPT_NEST ? yn[d] + A.h.beta * sv[d] : yn[d];  // optim.py:174-175
   store_pos<DIM, OPT>(Yout, v, yn, la);
-  if (A.pe.on) {  // fused exchange: the same record into the replica of every peer that gathers it
+  if constexpr (PEER) {  // fused exchange: the same record into the replica of every peer that gathers it
     const bool out1 = Yout == A.ybuf1;
     const unsigned mk = A.pe.mask[v];
     for (int q = 0; q < A.pe.n_peers; ++q)
@@ -711,16 +719,13 @@ __device__ __forceinline__ void fast_row(const StepArgs& A, const uint32_t* __re
     ee += rn ? c * r * r : d2;
     dmask |= (unsigned)(rn && z) << q;
   }
-  if (dmask) {  // degenerate random pairs (forces.py:167-174): slot q is entry ebase + q * G
+  if (dmask) {  // degenerate random pairs (forces.py:167-174): slot q is entry ebase + q * G.
+    // Only recorded here (the iteration pauses); the re-run with the host's
+    // directions launches the weighted instantiation, whose general path
+    // applies them (ivhd_capi.cu resume_degenerate).
 #pragma unroll
-    for (int q = 0; q < D; ++q) {
-      if ((dmask >> q) & 1u) {
-        float u[2];
-        degenerate_vec<2>(A, v, ebase + q * G, gstep, u);
-        fx += u[0];
-        fy += u[1];
-      }
-    }
+    for (int q = 0; q < D; ++q)
+      if ((dmask >> q) & 1u) record_degenerate(A.ctrl, A.miss_n, A.miss, A.miss_cap, v, ebase + q * G);
   }
   f[0] = fx;
   f[1] = fy;
@@ -778,7 +783,7 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 // unit partials into tile partials, stores them into its own and every peer's
 // partial array (slot = stamp parity), and raises flag[rank] = stamp on every
 // rank.  `scratch` is >= 1 int of shared memory.
-__device__ __noinline__ void peer_publish(const StepArgs& A, int* scratch, bool from_units) {
+__device__ __forceinline__ void peer_publish(const StepArgs& A, int* scratch, bool from_units) {
   block_sync();
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -829,7 +834,9 @@ __device__ __noinline__ void peer_publish(const StepArgs& A, int* scratch, bool 
 constexpr int kThreads = kBlock + 32;  // 8 consumer warps + 1 TMA producer warp
 constexpr int kConsumerWarps = kBlock / 32;
 
-template <int DIM, int OPT, bool WEIGHTED, int NORM>
+// PEER: sharded mode with the fused NVLink exchange (separate instantiation,
+// so the single-GPU kernel carries none of its code).
+template <int DIM, int OPT, bool WEIGHTED, int NORM, bool PEER>
 __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, NORM>()) step_kernel(StepArgs A) {
   using L = Layout<DIM, OPT>;
   using SL = StageLayout<DIM, OPT>;
@@ -842,7 +849,6 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   __shared__ StageMeta meta[kStages];
   __shared__ double4 sm_wp[kStages][kConsumerWarps];
   __shared__ int sm_cnt[kStages];
-  __shared__ double4 sm_red[kBlock / 32];
   __shared__ int sm_units[kUnitCache];  // this block's unit words (static schedule)
 
   Ctrl* ctrl = A.ctrl;
@@ -889,10 +895,30 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     nv = (int)max(0LL, min((long long)groups, A.v_end - va));
   };
 
-  // fused mode: this thread's running partials, in fp64 (the auto-adapt test
-  // compares the cancelling difference sum|dnew|^2 - sum|dold|^2 with tau)
-  double te = 0.0, tn = 0.0, to = 0.0;
-  float tb = 0.f;
+  // fused mode: this thread's running partials in fp32 over at most 64 units,
+  // then folded (fixed fp64 warp butterfly) into its warp's fp64 sums — the
+  // auto-adapt test compares the cancelling difference sum|dnew|^2 -
+  // sum|dold|^2 with tau, so long sums (C4/C5: ~900 vertices per thread) stay
+  // fp64 without fp64 registers in the unit loop
+  float te = 0.f, tn = 0.f, to = 0.f, tb = 0.f;
+  __shared__ double4 sm_wacc[kConsumerWarps];
+  if (tid < kConsumerWarps) sm_wacc[tid] = make_double4(0, 0, 0, 0);
+  auto flush_partials = [&]() {
+    double a = te, b = tn, c2 = to, d = tb;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+    if (lane == 0) {
+      double4 w = sm_wacc[warp];
+      w.x += a; w.y += b; w.z += c2; w.w += d;
+      sm_wacc[warp] = w;
+    }
+    te = tn = to = tb = 0.f;
+  };
   if (warp == kConsumerWarps) {
     // ---------------------------------------------------- TMA producer warp
     // Lane 0 issues the bulk copies (the whole warp runs the loop).
@@ -1142,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
             float sv[SSX];
 #pragma unroll
             for (int q = 0; q < SSX; ++q) sv[q] = L::SS > 0 ? ss[grp * SSX + q] : 0.f;
-            apply_update<DIM, OPT>(A, Yout, Sout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
+            apply_update<DIM, OPT, PEER>(A, Yout, Sout, v, yi, sv, f, step, bc1, bc2, acc_n, acc_o, acc_bad);
           }
         }
       }
@@ -1150,6 +1176,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
         // single GPU: running per-thread sums (fixed vertex order); the block
         // reduces them once after its last unit
         te += acc_e; tn += acc_n; to += acc_o; tb += acc_bad;
+        if ((k & 63) == 63) flush_partials();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_e[s]);  // this warp is done with stage s
         if (k < 34) IVHD_TL(2 + k);
@@ -1188,23 +1215,14 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   }
 
   if (!A.fuse_finalize) {
-    if (A.pe.on) peer_publish(A, sm_units, true);
+    if constexpr (PEER) peer_publish(A, sm_units, true);
     return;
   }
   IVHD_TL(38);
   // block partial: warp sums in a fixed butterfly, then warps in order
   block_sync();
   IVHD_TL(36);
-  if (warp < kConsumerWarps) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {  // fp64 butterfly, then warps in order
-      te += __shfl_xor_sync(0xffffffffu, te, o);
-      tn += __shfl_xor_sync(0xffffffffu, tn, o);
-      to += __shfl_xor_sync(0xffffffffu, to, o);
-      tb += __shfl_xor_sync(0xffffffffu, tb, o);
-    }
-    if (lane == 0) sm_red[warp] = make_double4(te, tn, to, tb);
-  }
+  if (warp < kConsumerWarps) flush_partials();  // the last (partial) group of units
   block_sync();
   if (warp != 0) return;
   // last-block-done: lane 0 publishes the block partial with a release
@@ -1214,7 +1232,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     double4 t = make_double4(0, 0, 0, 0);
 #pragma unroll
     for (int w = 0; w < kConsumerWarps; ++w) {
-      t.x += sm_red[w].x; t.y += sm_red[w].y; t.z += sm_red[w].z; t.w += sm_red[w].w;
+      t.x += sm_wacc[w].x; t.y += sm_wacc[w].y; t.z += sm_wacc[w].z; t.w += sm_wacc[w].w;
     }
     A.bpart[blockIdx.x] = t;
     unsigned old;

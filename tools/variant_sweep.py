@@ -6,6 +6,7 @@ on the C3 fixture and a planted 10^7 graph: us per iteration, steady state.
 import json, os, subprocess, sys, time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+C3 = os.path.join(ROOT, "tests", "golden", "c3_graph.npz")
 CHILD = r'''
 import os, sys, time, json
 import numpy as np
@@ -20,7 +21,7 @@ from paper_2303_05455_b200.embed import init_layout, sample_random_neighbors
 out = {}
 for name in GRAPHS:
     if name == "c3":
-        nb = np.load(os.path.join(ROOT, "tests/golden/c3_graph.npz"))["neighbors"]
+        nb = np.load(C3)["neighbors"]
     else:
         nb = synth.planted_graph(int(name.split(":")[1]), 2, seed=0)
     m = nb.shape[0]
@@ -45,7 +46,11 @@ def main():
     graphs = os.environ.get("GRAPHS", "c3,planted:10000000").split(",")
     iters = int(os.environ.get("ITERS", "500"))
     for lib in libs:
-        code = f"ROOT={ROOT!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
+        root = ROOT
+        if lib.endswith("/"):  # a package tree (another revision): its own python + library
+            root = os.path.abspath(lib)
+            lib = os.path.join(root, "paper_2303_05455_b200", "libivhd_b200.so")
+        code = f"C3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         print(os.path.basename(lib), r.stdout.strip() or r.stderr[-800:], flush=True)
 
