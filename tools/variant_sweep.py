@@ -22,6 +22,8 @@ out = {}
 for name in GRAPHS:
     if name == "c3":
         nb = np.load(C3)["neighbors"]
+    elif name.startswith("npz:"):
+        nb = np.load(os.path.join(os.path.dirname(C3), name[4:]))["neighbors"][:, :2]
     else:
         nb = synth.planted_graph(int(name.split(":")[1]), 2, seed=0)
     m = nb.shape[0]
@@ -29,6 +31,8 @@ for name in GRAPHS:
     y0 = init_layout(m, 2, rng); rn = sample_random_neighbors(m, nb, 1, rng)
     dev = DeviceEmbedding(m, 2)
     dev.set_optimizer(resolve_optimizer("force-directed", m)); dev.set_positions(y0); dev.set_graph(0, nb, rn)
+    if MODE and hasattr(dev, "set_launch_mode"):
+        dev.set_launch_mode(MODE)
     dev.snapshot()
     best = []
     for rep in range(4):
@@ -50,7 +54,7 @@ def main():
         if lib.endswith("/"):  # a package tree (another revision): its own python + library
             root = os.path.abspath(lib)
             lib = os.path.join(root, "paper_2303_05455_b200", "libivhd_b200.so")
-        code = f"C3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
+        code = f"MODE={os.environ.get('MODE', '')!r}\nC3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         print(os.path.basename(lib), r.stdout.strip() or r.stderr[-800:], flush=True)
 
