@@ -959,6 +959,12 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
   A.ybuf1 = ctx->ybuf[1];
   A.state = ctx->state;
   A.sstride = state_stride(ctx);
+  {  // streamed graph bytes + positions + state per iteration vs the L2 size
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+    const int64_t ws = 4 * S.n + 4 * ctx->m + (int64_t)4 * ctx->m * (2 * ys_now(ctx) + ss_now(ctx));
+    A.stream_hint = ws > (int64_t)l2 ? 1 : 0;
+  }
   A.dg_key = ctx->dg_key;
   A.dg_vec = ctx->dg_vec;
   A.miss_n = ctx->miss_n;

@@ -146,6 +146,7 @@ struct StepArgs {
   int* miss_n;            // pairs with no table entry this iteration ...
   int2* miss;             // ... (row, entry index), up to miss_cap of them
   int miss_cap;
+  int stream_hint;        // evict-first L2 policy on the streamed graph data (working set > L2)
   double4* partial;       // per work unit (sharded / operator calls)
   double4* tpart;         // per tile: sharded mode's exchanged partials
   const int* unit_base;   // first unit of each tile
@@ -656,6 +657,23 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // global -> shared bulk copy (TMA, non-tensor); 16-byte aligned, size % 16 == 0
+// L2 eviction policy for the streamed graph data (row pointers, columns) when
+// the working set exceeds L2 (A.stream_hint): first out, so the randomly
+// gathered positions stay (planted 10^7: 263 -> 252 µs; C3 fits L2 and runs
+// without it, profiles/r02_kernel_experiments.md)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -934,7 +952,8 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
         meta[s].nv = nv;
         const uint32_t rp_bytes = (uint32_t)((nv + 1) * 4 + 15) / 16 * 16;
         mbar_expect_tx(&bar_r[s], rp_bytes);
-        bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_r[s]);
+        if (A.stream_hint) bulk_g2s_hint(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_r[s], policy_evict_first());
+        else bulk_g2s(st + SL::RP_OFF, A.row_ptr + va, rp_bytes, &bar_r[s]);
       };
       auto issue_cols = [&](int k) {  // column segment of local unit k (its row pointers have landed)
         const int s = k % kStages;
@@ -949,7 +968,8 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
           meta[s].col_off = (int)(e0 - a0);
           meta[s].staged = 1;
           mbar_expect_tx(&bar_b[s], (a1 - a0) * 4);
-          bulk_g2s(st + SL::COL_OFF, A.col + a0, (a1 - a0) * 4, &bar_b[s]);
+          if (A.stream_hint) bulk_g2s_hint(st + SL::COL_OFF, A.col + a0, (a1 - a0) * 4, &bar_b[s], policy_evict_first());
+          else bulk_g2s(st + SL::COL_OFF, A.col + a0, (a1 - a0) * 4, &bar_b[s]);
         } else {
           meta[s].col_off = 0;
           meta[s].staged = 0;
