@@ -441,6 +441,21 @@ def gpu_arm(args, w):
     value = L * iters * args.steps / tot
     s_iter = tot / (args.steps * iters)
     dev_launches = dev.launches_per_iteration() if hasattr(dev, "launches_per_iteration") else 1
+    nvlink = None
+    if sharded and getattr(dev, "exchange", None) == "p2p":
+        # fused exchange: position records this rank stores into peers per
+        # iteration (halo masks) -> NVLink bytes; max over ranks
+        recs, nbytes_pe = dev.device_embedding.peer_halo()
+        t = torch.tensor([float(nbytes_pe), float(recs)], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allgather_bytes = (world - 1) * (m // world) * 8
+        nvlink = {"exchange": "fused P2P stores from the step kernel (halo masks), no NCCL",
+                  "bytes_per_iteration_per_rank_max": float(t[0]), "records_per_iteration_per_rank_max": float(t[1]),
+                  "allgather_bytes_per_rank": allgather_bytes,
+                  "achieved_gbs": float(t[0]) / s_iter / 1e9,
+                  "peak_gbs": 770.0,
+                  "note": "bytes each rank writes over NVLink per iteration / device time per iteration; "
+                          "peak = measured peer copy per direction (B200_PROFILING.md)"}
     dev.close() if hasattr(dev, "close") else None
 
     # ---------------- e2e: public API from pinned host arrays
@@ -523,7 +538,7 @@ def gpu_arm(args, w):
                          "note": f"algorithmic bytes {nbytes} per iteration (8L+36M for FD) / device time "
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * iters * dev_launches, "clocks": clk.summary(),
+            "gpu_launches": args.steps * iters * dev_launches, "clocks": clk.summary(), "nvlink": nvlink,
             "final_stress_e2e": final_stress,
             "knn": knn, "quality": quality,
         }
