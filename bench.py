@@ -30,7 +30,9 @@ baseline/_ref (`ivhd.engine.run_embedding`, threads = all host cores) on the
 same graph and config, rank 0 only; it never imports this package.
 
 N > 1: `python bench.py --gpus N` starts N ranks itself (one process per
-GPU, NCCL) when it is not already running under torchrun.
+GPU) when it is not already running under torchrun; the ranks exchange
+positions and partials through the fused NVLink path (sharded.py, no NCCL),
+the gloo process group is the control plane only.
 """
 
 import argparse
@@ -384,7 +386,9 @@ def gpu_arm(args, w):
             with socket.socket() as so:
                 so.bind(("127.0.0.1", 0))
                 os.environ["MASTER_PORT"] = str(so.getsockname()[1])
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # control plane only (IPC handles, barriers, max over ranks): the fused
+        # exchange moves the data itself, so the process group is gloo on the host
+        dist.init_process_group("gloo")
     nb = make_graph(w)
     m, L, iters = w["m"], (w["nn"] + w["rn"]) * w["m"], w["iterations"]
 
@@ -434,7 +438,7 @@ def gpu_arm(args, w):
     torch.cuda.synchronize()
     tot = sum(times)
     if sharded:
-        t = torch.tensor([tot], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([tot], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot = float(t.item())
         dist.barrier()
@@ -446,7 +450,7 @@ def gpu_arm(args, w):
         # fused exchange: position records this rank stores into peers per
         # iteration (halo masks) -> NVLink bytes; max over ranks
         recs, nbytes_pe = dev.device_embedding.peer_halo()
-        t = torch.tensor([float(nbytes_pe), float(recs)], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([float(nbytes_pe), float(recs)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         allgather_bytes = (world - 1) * (m // world) * 8
         nvlink = {"exchange": "fused P2P stores from the step kernel (halo masks), no NCCL",
@@ -484,7 +488,7 @@ def gpu_arm(args, w):
             torch.cuda.synchronize()
             wall = time.perf_counter() - t0
             if sharded:
-                t = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+                t = torch.tensor([wall], dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 wall = float(t.item())
             if i >= 2:  # two warm-up calls (allocator pools, pinned result buffers)

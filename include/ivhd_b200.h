@@ -210,8 +210,10 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
  * all-gather: the step kernel stores every updated position straight into
  * each peer's replica and its tile partials into each peer's partial array
  * (P2P stores overlap the update tile by tile), raises its arrival flag on
- * every rank, and a one-block finalizer waits for all ranks' flags and takes
- * the same decision on every rank.  Set-up, after ivhd_shard_set_range:
+ * every rank; the last block of each rank's step kernel then reduces its
+ * blocks' partials, publishes the rank partial to every rank, waits for all
+ * ranks' flags and takes the same decision on every rank (one launch per
+ * iteration).  Set-up, after ivhd_shard_set_range:
  *   ivhd_peer_export(ctx, world, rank, h)   moves the exchanged buffers to
  *       cudaMalloc memory and writes their CUDA IPC handles
  *       (IVHD_PEER_HANDLE_BYTES bytes) into h;
@@ -220,9 +222,10 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
  * In-process (several contexts of one process, tests): ivhd_peer_export on
  * each, then ivhd_peer_import_local(ctx, ctxs) with the contexts in rank order.
  * Afterwards ivhd_run drives the whole exchange on the device (CUDA graphs of
- * step + finalizer launches, no host work per iteration); ivhd_shard_step /
- * ivhd_shard_finalize launch the two kernels one at a time (the in-process
- * emulation interleaves them over ranks).  A rank that does not arrive within
+ * one step launch per iteration, no host work per iteration).  In-process
+ * peers (ivhd_peer_import_local) decide in a separate finalizer kernel instead:
+ * ivhd_shard_step / ivhd_shard_finalize launch the two one at a time, so the
+ * emulation can run every rank's step before any finalizer.  A rank that does not arrive within
  * 10 s makes the others fail with IVHD_ERR_PEER instead of hanging. */
 #define IVHD_PEER_HANDLE_BYTES 256
 int ivhd_peer_export(ivhd_ctx* ctx, int world, int rank, uint8_t* handle_out);

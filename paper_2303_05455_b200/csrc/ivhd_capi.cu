@@ -39,6 +39,7 @@ struct CsrSlot {
   std::vector<int> unit_words;  // host copy of units
   std::vector<int> unit_cost;   // host: modelled cost of each unit (slot rounds per lane)
   int sched_grid = 0;           // grid the cost-balanced schedule below was built for
+  int sched_u0 = 0, sched_u1 = 0;  // ... and its unit range
   int* sched_units = nullptr;   // units regrouped per block (fused mode)
   int* sched_off = nullptr;     // [sched_grid + 1]
   int64_t n = 0;                // entries (2 * connections)
@@ -123,7 +124,8 @@ struct ivhd_ctx {
   bool peer_on = false;
   int world = 1, rank = 0;
   bool ybuf_malloc = false;            // ybuf[0..1] are cudaMalloc (not pool) memory
-  double4* tp2 = nullptr;              // [2][n_tiles_cap] tile partials by stamp parity
+  double4* tp2 = nullptr;              // [2][world][8 * SMs] block partials by stamp parity
+  int64_t tp2_slots = 0;
   unsigned long long* flags = nullptr; // [8] arrival flags, one slot per rank
   unsigned long long* stamp = nullptr; // iterations exchanged
   PeerArgs pe{};
@@ -866,6 +868,7 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
       S.unit_cost[u] = (dm[t] + G - 1) / G;  // slots per lane
     }
     S.sched_grid = 0;
+    S.sched_u1 = -1;
     S.n_units = (int)units.size();
     if (S.units) dfree(ctx, S.units);
     S.units = nullptr;
@@ -895,26 +898,28 @@ int build_csr(ivhd_ctx* ctx, int slot, const int32_t* src, const int32_t* dst, c
 // per-unit overhead), ties to the lowest block; each block then runs its
 // units heavy first.  Deterministic for a given graph and grid, so the
 // per-thread partial sums keep a fixed order.
-int build_schedule(ivhd_ctx* ctx, CsrSlot& S, int grid) {
-  if (S.sched_grid == grid) return IVHD_OK;
+// Units [u0, u1) (a sharded rank's range; the whole graph by default).
+int build_schedule(ivhd_ctx* ctx, CsrSlot& S, int grid, int u0 = 0, int u1 = -1) {
+  if (u1 < 0) u1 = S.n_units;
+  if (S.sched_grid == grid && S.sched_u0 == u0 && S.sched_u1 == u1) return IVHD_OK;
   constexpr int c0 = 3;  // modelled fixed cost of a unit, in slot rounds (profiles/r01_c0_sweep.txt)
-  const int n = S.n_units;
+  const int n = u1 - u0;
   std::vector<std::vector<int>> per(grid);
   if (ctx->window_order) {
     // id-local input: contiguous unit ranges of equal modelled cost, so one
     // block sweeps a window's tiles back to back and its nn partners are
     // still in L2 (and L1) when the neighbouring tiles gather them
     int64_t total = 0, acc = 0;
-    for (int u = 0; u < n; ++u) total += S.unit_cost[u] + c0;
+    for (int u = u0; u < u1; ++u) total += S.unit_cost[u] + c0;
     int b = 0;
-    for (int u = 0; u < n; ++u) {
+    for (int u = u0; u < u1; ++u) {
       per[b].push_back(u);
       acc += S.unit_cost[u] + c0;
       while (b < grid - 1 && acc * grid >= (int64_t)(b + 1) * total) ++b;
     }
   } else {
     std::vector<int> order(n);
-    for (int i = 0; i < n; ++i) order[i] = i;
+    for (int i = 0; i < n; ++i) order[i] = u0 + i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return S.unit_cost[a] > S.unit_cost[b]; });
     std::vector<std::pair<int64_t, int>> heap;  // (load, block), min-heap
     for (int b = 0; b < grid; ++b) heap.push_back({0, b});
@@ -946,6 +951,8 @@ int build_schedule(ivhd_ctx* ctx, CsrSlot& S, int grid) {
   CU(ctx, cudaMemcpyAsync(S.sched_off, off.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
   S.sched_grid = grid;
+  S.sched_u0 = u0;
+  S.sched_u1 = u1;
   return IVHD_OK;
 }
 
@@ -1001,6 +1008,22 @@ StepArgs make_args(ivhd_ctx* ctx, int slot, int norm, int fuse) {
     A.n_tiles_global = A.n_tiles;
   }
   return A;
+}
+
+// The peer finalizer, also programmatically dependent: it becomes resident
+// while the step drains and waits (griddepcontrol.wait) for it.
+int launch_finalize_peer(ivhd_ctx* ctx, const StepArgs& A) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU(ctx, cudaLaunchKernelEx(&cfg, pick_finalize_peer(ctx->opt.kind), A));
+  return IVHD_OK;
 }
 
 int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
@@ -1814,20 +1837,19 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   const bool peer = ctx->peer_on;
   KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm, peer);
   if (peer && ctx->masks_stale) TRY(peer_masks(ctx));
-  StepArgs A = make_args(ctx, slot, norm, peer ? 0 : 1);
-  if (!peer) {
+  StepArgs A = make_args(ctx, slot, norm, 1);  // peer mode too: running sums, one partial per block
+  if (A.n_tiles > 0) {  // cost-balanced static schedule over this context's (rank's) units
     const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
-    TRY(build_schedule(ctx, ctx->slots[slot], grid));
+    TRY(build_schedule(ctx, ctx->slots[slot], grid, A.tile0, A.tile0 + A.n_tiles));
     A.units = S.sched_units;
     A.boff = S.sched_off;
   }
   // one iteration: the fused kernel (one GPU), or step + peer finalizer
+  // peer mode: the step kernel's last block waits for the peers and decides
+  // (one process per GPU); in-process contexts use the finalizer kernel
   auto launch_step = [&](ivhd_ctx* c, KernelInfo k, const StepArgs& a) -> int {
-    if (!peer) return ::launch_step(c, k, a);
-    if (a.n_tiles > 0) TRY(::launch_step(c, k, a));
-    pick_finalize_peer(c->opt.kind)<<<1, kBlock, 0, c->stream>>>(a);
-    CU(c, cudaGetLastError());
-    return IVHD_OK;
+    TRY(::launch_step(c, k, a));
+    return (peer && !c->pe.decide_here) ? launch_finalize_peer(c, a) : IVHD_OK;
   };
   int64_t left = n_iter;
   if (left > 0 && ctx->ctrl_h->dg_n > 0 && ctx->ctrl_h->dg_gstep == ctx->ctrl_h->gstep) {
@@ -2205,6 +2227,7 @@ int ivhd_shard_step(ivhd_ctx* ctx, int slot, int norm, uint64_t* exchange_out) {
       TRY(peer_masks(ctx));
       A.pe = ctx->pe;
     }
+    A.fuse_finalize = 1;  // running sums, one partial per block (round-robin units here)
     if (A.n_tiles > 0) TRY(launch_step(ctx, pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm, true), A));
     if (exchange_out) *exchange_out = 0;
     return IVHD_OK;
@@ -2220,11 +2243,7 @@ int ivhd_shard_finalize(ivhd_ctx* ctx) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
   CU(ctx, cudaSetDevice(ctx->device));
   StepArgs A = make_args(ctx, ctx->shard_slot, 0, 0);
-  if (ctx->peer_on) {
-    pick_finalize_peer(ctx->opt.kind)<<<1, kBlock, 0, ctx->stream>>>(A);
-    CU(ctx, cudaGetLastError());
-    return IVHD_OK;
-  }
+  if (ctx->peer_on) return launch_finalize_peer(ctx, A);
   shard_io(ctx, A);
   pick_finalize(ctx->opt.kind)<<<1, kBlock, 0, ctx->stream>>>(A);
   CU(ctx, cudaGetLastError());
@@ -2261,11 +2280,20 @@ static int peer_alloc(ivhd_ctx* ctx, int world, int rank) {
     }
     ctx->ybuf_malloc = true;
   }
-  if (!ctx->tp2) CU(ctx, cudaMalloc(&ctx->tp2, sizeof(double4) * 2 * ctx->n_tiles_cap));
+  // rank-partial slots: [2 parities][world ranks]
+  const int64_t n_slots = world;
+  if (ctx->tp2 && ctx->tp2_slots < n_slots) {
+    cudaFree(ctx->tp2);
+    ctx->tp2 = nullptr;
+  }
+  if (!ctx->tp2) {
+    CU(ctx, cudaMalloc(&ctx->tp2, sizeof(double4) * 2 * n_slots));
+    ctx->tp2_slots = n_slots;
+  }
   // flags: [0, 8) iteration arrivals, [8, 16) end-of-run barrier; stamp: [0] iterations, [1] barriers
   if (!ctx->flags) CU(ctx, cudaMalloc(&ctx->flags, sizeof(unsigned long long) * 16));
   if (!ctx->stamp) CU(ctx, cudaMalloc(&ctx->stamp, sizeof(unsigned long long) * 2));
-  CU(ctx, cudaMemset(ctx->tp2, 0, sizeof(double4) * 2 * ctx->n_tiles_cap));
+  CU(ctx, cudaMemset(ctx->tp2, 0, sizeof(double4) * 2 * ctx->tp2_slots));
   CU(ctx, cudaMemset(ctx->flags, 0, sizeof(unsigned long long) * 16));
   CU(ctx, cudaMemset(ctx->stamp, 0, sizeof(unsigned long long) * 2));
   CU(ctx, cudaDeviceSynchronize());
@@ -2282,6 +2310,7 @@ static int peer_alloc(ivhd_ctx* ctx, int world, int rank) {
   pe.fl_local = ctx->flags;
   pe.stamp = ctx->stamp;
   pe.n_tiles_cap = ctx->n_tiles_cap;
+  pe.decide_here = 1;
   pe.timeout_ns = 10LL * 1000 * 1000 * 1000;
   drop_graphs(ctx);
   return IVHD_OK;
@@ -2402,6 +2431,7 @@ int ivhd_peer_import_local(ivhd_ctx* ctx, ivhd_ctx* const* ctxs) {
   if (!ctx->tp2) return fail(ctx, IVHD_ERR_STATE, "call ivhd_peer_export first");
   PeerArgs& pe = ctx->pe;
   pe.n_peers = 0;
+  pe.decide_here = 0;  // ranks share this process (and GPU): a separate finalizer decides
   for (int q = 0; q < ctx->world; ++q) {
     if (q == ctx->rank) continue;
     const ivhd_ctx* o = ctxs[q];

@@ -119,6 +119,8 @@ struct PeerArgs {
   unsigned long long* fl_local;   // own arrival flags [world]
   unsigned long long* stamp;      // iterations exchanged so far (device word; survives ivhd_restore)
   int n_tiles_cap;
+  int decide_here;                // 1: the step kernel's last block waits for the peers and decides
+                                  // (one process per GPU); 0: finalize_peer_kernel does (emulation)
   long long timeout_ns;           // finalizer wait limit before it reports a peer failure
   int prank[kMaxPeers];           // rank of peer slot k
   const uint8_t* mask;            // halo: bit r of mask[v] = rank r has a row that gathers v
@@ -795,49 +797,84 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// End of a peer-mode step launch, called by every thread of every block:
-// the block's P2P position stores are ordered before its arrival (system-scope
-// fence after the block barrier); the last block to arrive folds this rank's
-// unit partials into tile partials, stores them into its own and every peer's
-// partial array (slot = stamp parity), and raises flag[rank] = stamp on every
-// rank.  `scratch` is >= 1 int of shared memory.
-__device__ __forceinline__ void peer_publish(const StepArgs& A, int* scratch, bool from_units) {
-  block_sync();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    unsigned old;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&A.ctrl->parrive) : "memory");
-    scratch[0] = old == gridDim.x - 1;
-  }
-  block_sync();
-  if (!scratch[0]) return;
-  __threadfence();
-  const unsigned long long stamp = *A.pe.stamp + 1;
-  const size_t par = (size_t)(stamp & 1) * A.pe.n_tiles_cap;
-  for (int t = A.pe.t0 + threadIdx.x; t < A.pe.t1; t += blockDim.x) {
-    double4 s = make_double4(0, 0, 0, 0);
-    if (from_units) {  // fp32 kernel: fold the tile's unit partials in unit order
-      for (int u = A.unit_base[t]; u < A.unit_base[t + 1]; ++u) {
-        const double4 q = A.partial[u];
-        s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
-      }
-    } else {  // fp64 kernel: tile partials already in tpart
-      s = A.tpart[t];
+__device__ __forceinline__ double4 ldcg4(const double4* p) {  // L2 (coherent) load of a double4
+  const double2 a = __ldcg(reinterpret_cast<const double2*>(p)), b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// Peer mode, last block of a rank, one warp: the rank's partial (its block
+// partials reduced in block order, plus 2^32 if it met degenerate pairs
+// without directions) goes into slot `rank` of every rank's partial array
+// (half = stamp parity), then flag[rank] = stamp is raised on every rank
+// (system-scope release: every block fenced its P2P stores before arriving).
+// The ranks' partials are reduced in rank order — deterministic for a given
+// rank count; positions and decisions do not depend on it.
+__device__ __forceinline__ void peer_rank_publish(const StepArgs& A, int n_blocks) {
+  const int lane = threadIdx.x & 31;
+  double4 s = make_double4(0, 0, 0, 0);
+  for (int t0 = lane; t0 < n_blocks; t0 += 32 * 16) {
+    double4 a[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = t0 + 32 * j < n_blocks ? ldcg4(A.bpart + t0 + 32 * j) : make_double4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      s.x += a[j].x; s.y += a[j].y; s.z += a[j].z; s.w += a[j].w;
     }
-    if (t == A.pe.t0 && A.ctrl->need) {  // this rank met degenerate pairs without directions
+  }
+  s.x = warp_dsum(s.x); s.y = warp_dsum(s.y); s.z = warp_dsum(s.z); s.w = warp_dsum(s.w);
+  if (lane == 0) {
+    if (A.ctrl->need) {
       s.w += kMissUnit;
       A.ctrl->need = 0;
     }
-    A.pe.tp_local[par + t] = s;
-    for (int q = 0; q < A.pe.n_peers; ++q) A.pe.tp[q][par + t] = s;
-  }
-  block_sync();
-  if (threadIdx.x == 0) {
+    const unsigned long long stamp = *A.pe.stamp + 1;
+    const size_t slot = (size_t)(stamp & 1) * A.pe.world + A.pe.rank;
+    A.pe.tp_local[slot] = s;
+    for (int q = 0; q < A.pe.n_peers; ++q) A.pe.tp[q][slot] = s;
     __threadfence_system();
     st_release_sys(A.pe.fl_local + A.pe.rank, stamp);
     for (int q = 0; q < A.pe.n_peers; ++q) st_release_sys(A.pe.fl[q] + A.pe.rank, stamp);
-    A.ctrl->parrive = 0;  // every block of this launch has arrived
   }
+  __syncwarp();
+}
+
+// Wait until every rank raised its flag for this iteration (system-scope
+// acquire), then reduce the ranks' partials in rank order and decide.  One
+// warp (lanes < world wait).  A rank that does not arrive within
+// pe.timeout_ns sets status 3 (peer failure) instead of hanging.
+template <int OPT>
+__device__ __forceinline__ void peer_decide(const StepArgs& A) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long stamp = *A.pe.stamp + 1;
+  int fail = 0;
+  if (lane < A.pe.world) {
+    const unsigned long long* f = A.pe.fl_local + lane;
+    long long t0 = 0, t1 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys(f) < stamp) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > A.pe.timeout_ns) {
+        fail = 1;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  fail = __any_sync(0xffffffffu, fail);
+  if (lane != 0) return;
+  if (fail) {
+    A.ctrl->status = 3;
+    return;
+  }
+  __threadfence();
+  const double4* tp = A.pe.tp_local + (size_t)(stamp & 1) * A.pe.world;
+  double4 s = make_double4(0, 0, 0, 0);
+  for (int r = 0; r < A.pe.world; ++r) {
+    const double4 q = ldcg4(tp + r);
+    s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+  }
+  decide<OPT>(A, s);
+  *A.pe.stamp = stamp;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -1234,10 +1271,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     }
   }
 
-  if (!A.fuse_finalize) {
-    if constexpr (PEER) peer_publish(A, sm_units, true);
-    return;
-  }
+  if (!A.fuse_finalize) return;
   IVHD_TL(38);
   // block partial: warp sums in a fixed butterfly, then warps in order
   block_sync();
@@ -1255,6 +1289,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       t.x += sm_wacc[w].x; t.y += sm_wacc[w].y; t.z += sm_wacc[w].z; t.w += sm_wacc[w].w;
     }
     A.bpart[blockIdx.x] = t;
+    if constexpr (PEER) __threadfence_system();  // this block's P2P position stores first
     unsigned old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&ctrl->arrive) : "memory");
     last = old == gridDim.x - 1;
@@ -1262,48 +1297,25 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   IVHD_TL(37);
   if (!__shfl_sync(0xffffffffu, last, 0)) return;
   __syncwarp();
+  if constexpr (PEER) {
+    peer_rank_publish(A, (int)gridDim.x);
+    if (A.pe.decide_here) peer_decide<OPT>(A);  // ranks on separate GPUs: no finalizer launch
+    else if (lane == 0) ctrl->arrive = 0;       // the finalizer kernel decides (in-process emulation)
+    return;
+  }
   finalize_warp<OPT>(A, A.bpart, (int)gridDim.x);
   IVHD_TL(39);
 }
 
-// Peer-mode finalizer: one block.  Waits until every rank has raised its
-// flag for this iteration (system-scope acquire; a rank that does not arrive
-// within pe.timeout_ns sets status 3 = peer failure instead of hanging), then
-// reduces all tile partials of the iteration in tile order and decides.
+// Peer-mode finalizer for ranks that share one GPU (in-process emulation:
+// every rank's step kernel runs before any finalizer, so nothing waits on a
+// kernel that has not run).  One warp: peer_decide.
 template <int OPT>
-__global__ void __launch_bounds__(kBlock) finalize_peer_kernel(StepArgs A) {
-  __shared__ double4 sm_red[kBlock / 32];
-  __shared__ int s_fail;
+__global__ void __launch_bounds__(32) finalize_peer_kernel(StepArgs A) {
+  if (threadIdx.x == 0) griddep_launch_dependents();  // the next step may stage its graph constants
   griddep_wait();
   if (A.ctrl->status != 0) return;
-  const unsigned long long stamp = *A.pe.stamp + 1;
-  if (threadIdx.x == 0) s_fail = 0;
-  block_sync();
-  if (threadIdx.x < A.pe.world) {
-    const unsigned long long* f = A.pe.fl_local + threadIdx.x;
-    long long t0 = 0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    int fail = 0;
-    while (ld_acquire_sys(f) < stamp) {
-      long long t1;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      if (t1 - t0 > A.pe.timeout_ns) {
-        fail = 1;
-        break;
-      }
-      __nanosleep(100);
-    }
-    if (fail) atomicExch(&s_fail, 1);
-  }
-  block_sync();
-  if (s_fail) {
-    if (threadIdx.x == 0) A.ctrl->status = 3;
-    return;
-  }
-  __threadfence();
-  const double4* tp = A.pe.tp_local + (size_t)(stamp & 1) * A.pe.n_tiles_cap;
-  finalize_block<OPT>(A, sm_red, tp, A.pe.n_tiles_cap);
-  if (threadIdx.x == 0) *A.pe.stamp = stamp;
+  peer_decide<OPT>(A);
 }
 
 // Standalone finalizer (sharded mode, after the exchange): one block.

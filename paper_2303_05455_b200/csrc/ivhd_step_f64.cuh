@@ -154,25 +154,27 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
       if (tid == 0) A.tpart[t] = r;
     }
   }
-  if (!A.fuse_finalize) {
-    if (A.pe.on) {
-      __shared__ int scratch;
-      peer_publish(A, &scratch, false);
-    }
-    return;
-  }
+  if (!A.fuse_finalize) return;
   // block partial in fixed order, then the last block to arrive decides
+  // (peer mode: into every rank's partial array, then the arrival flags)
   const double4 r = block_sum4(make_double4(te, 0.0, 0.0, tb), sm_red);
   if (warp != 0) return;
   int last = 0;
   if (lane == 0) {
     A.bpart[blockIdx.x] = r;
+    if (A.pe.on) __threadfence_system();  // this block's P2P position stores first
     unsigned old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&ctrl->arrive) : "memory");
     last = old == gridDim.x - 1;
   }
   if (!__shfl_sync(0xffffffffu, last, 0)) return;
   __syncwarp();
+  if (A.pe.on) {  // peer mode (see ivhd_step.cuh peer_rank_publish / peer_decide)
+    peer_rank_publish(A, (int)gridDim.x);
+    if (A.pe.decide_here) peer_decide<OPT_ADAM>(A);
+    else if (lane == 0) ctrl->arrive = 0;
+    return;
+  }
   finalize_warp<OPT_ADAM>(A, A.bpart, (int)gridDim.x);
 }
 

@@ -173,9 +173,12 @@ def test_peer_exchange_emulated_matches_nccl_path_and_oracle(world):
     for y, st, bb in many:
         np.testing.assert_array_equal(y, many[0][0])
         np.testing.assert_array_equal(st, many[0][1])
-    # same tiles, same fold order, same decisions: bit-identical to the NCCL path
+    # same per-vertex updates and decisions as the NCCL path: positions and the
+    # step-size trace bit-identical; the fp64 stress is summed per block here
+    # (per tile there), so it agrees to rounding
     np.testing.assert_array_equal(many[0][0], ref[0])
-    np.testing.assert_array_equal(many[0][1], ref[1])
+    np.testing.assert_array_equal(many[0][2], ref[2])
+    np.testing.assert_allclose(many[0][1], ref[1], rtol=1e-12)
     orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0)
     orc.run()
     assert normwise(many[0][0], orc.Y) < 1e-5

@@ -30,8 +30,12 @@ for name in GRAPHS:
     rng = np.random.default_rng(0)
     y0 = init_layout(m, 2, rng); rn = sample_random_neighbors(m, nb, 1, rng)
     dev = DeviceEmbedding(m, 2)
+    if MODE == "peer1":  # the fused peer exchange with one rank (sharded kernels + finalizer)
+        tv, nt = dev.tiles()
+        dev.shard_set_range(0, tv * nt)
+        dev.peer_import([dev.peer_export(1, 0)])
     dev.set_optimizer(resolve_optimizer("force-directed", m)); dev.set_positions(y0); dev.set_graph(0, nb, rn)
-    if MODE and hasattr(dev, "set_launch_mode"):
+    if MODE in ("graphs", "persistent") and hasattr(dev, "set_launch_mode"):
         dev.set_launch_mode(MODE)
     dev.snapshot()
     best = []
