@@ -208,12 +208,11 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
 /* Fused peer exchange over NVLink (sharded mode, one process per GPU on one
  * node, up to 8 ranks).  Replaces the per-iteration NCCL
  * all-gather: the step kernel stores every updated position straight into
- * each peer's replica and its tile partials into each peer's partial array
- * (P2P stores overlap the update tile by tile), raises its arrival flag on
- * every rank; the last block of each rank's step kernel then reduces its
- * blocks' partials, publishes the rank partial to every rank, waits for all
- * ranks' flags and takes the same decision on every rank (one launch per
- * iteration).  Set-up, after ivhd_shard_set_range:
+ * the replica of each peer that gathers it (P2P stores overlap the update
+ * tile by tile); the last block of each rank's step kernel reduces its
+ * blocks' partials, stores the rank partial into every rank's partial array,
+ * raises its arrival flag on every rank, waits for all ranks' flags and takes
+ * the same decision on every rank (one launch per iteration).  Set-up, after ivhd_shard_set_range:
  *   ivhd_peer_export(ctx, world, rank, h)   moves the exchanged buffers to
  *       cudaMalloc memory and writes their CUDA IPC handles
  *       (IVHD_PEER_HANDLE_BYTES bytes) into h;
@@ -225,8 +224,9 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
  * one step launch per iteration, no host work per iteration).  In-process
  * peers (ivhd_peer_import_local) decide in a separate finalizer kernel instead:
  * ivhd_shard_step / ivhd_shard_finalize launch the two one at a time, so the
- * emulation can run every rank's step before any finalizer.  A rank that does not arrive within
- * 10 s makes the others fail with IVHD_ERR_PEER instead of hanging. */
+ * emulation can run every rank's step before any finalizer.  A rank that
+ * does not arrive within 10 s makes the others fail with IVHD_ERR_PEER
+ * instead of hanging. */
 #define IVHD_PEER_HANDLE_BYTES 256
 int ivhd_peer_export(ivhd_ctx* ctx, int world, int rank, uint8_t* handle_out);
 int ivhd_peer_import(ivhd_ctx* ctx, const uint8_t* all_handles);
