@@ -15,6 +15,8 @@ if kind == "mixture":
     if not os.path.exists(cache):
         np.save(cache, synth.mixture_knn_graph(1_400_000, 100, k=2, seed=0)[0])
     nb = np.load(cache)
+elif kind.endswith(".npz"):
+    nb = np.load(kind)["neighbors"]
 else:
     nb = synth.planted_graph(m, 2, seed=0)
 m = nb.shape[0]
@@ -24,7 +26,7 @@ dev.set_optimizer(resolve_optimizer("force-directed", m))
 dev.init_positions(g)
 dev.set_graph_sampled(0, nb[:, :2], 1, g)
 dev.run(0, "l2", 0.1, 20)
-lib = ctypes.CDLL(os.environ["IVHD_B200_LIB"])
+lib = ctypes.CDLL(os.environ.get("IVHD_B200_LIB", os.path.join(os.path.dirname(__file__), "..", "paper_2303_05455_b200", "libivhd_b200.so")))
 buf = np.zeros(2 * 1024 * 40, np.int64)
 lib.ivhd_timeline_dump(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)))
 t = buf.reshape(2, 1024, 40).astype(np.float64)

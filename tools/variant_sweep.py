@@ -35,7 +35,7 @@ for name in GRAPHS:
         dev.shard_set_range(0, tv * nt)
         dev.peer_import([dev.peer_export(1, 0)])
     dev.set_optimizer(resolve_optimizer("force-directed", m)); dev.set_positions(y0); dev.set_graph(0, nb, rn)
-    if MODE in ("graphs", "persistent") and hasattr(dev, "set_launch_mode"):
+    if MODE in ("auto", "grid") and hasattr(dev, "set_launch_mode"):
         dev.set_launch_mode(MODE)
     dev.snapshot()
     best = []
