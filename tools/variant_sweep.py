@@ -24,8 +24,9 @@ for name in GRAPHS:
         nb = np.load(C3)["neighbors"]
     elif name.startswith("npz:"):
         nb = np.load(os.path.join(os.path.dirname(C3), name[4:]))["neighbors"][:, :2]
-    else:
-        nb = synth.planted_graph(int(name.split(":")[1]), 2, seed=0)
+    else:  # planted:M (nn=2) or plantedK:M (nn=K)
+        kind, mm = name.split(":")
+        nb = synth.planted_graph(int(mm), int(kind[7:] or 2), seed=0)
     m = nb.shape[0]
     rng = np.random.default_rng(0)
     y0 = init_layout(m, 2, rng); rn = sample_random_neighbors(m, nb, 1, rng)
@@ -37,6 +38,12 @@ for name in GRAPHS:
     dev.set_optimizer(resolve_optimizer("force-directed", m)); dev.set_positions(y0); dev.set_graph(0, nb, rn)
     if MODE in ("auto", "grid") and hasattr(dev, "set_launch_mode"):
         dev.set_launch_mode(MODE)
+    if L2G:  # driver-level L2 fetch granularity limit (CU_LIMIT_MAX_L2_FETCH_GRANULARITY)
+        import ctypes
+        cu = ctypes.CDLL("libcuda.so.1"); val = ctypes.c_size_t(0)
+        cu.cuCtxGetLimit(ctypes.byref(val), 5); before = val.value
+        rc = cu.cuCtxSetLimit(5, ctypes.c_size_t(L2G)); cu.cuCtxGetLimit(ctypes.byref(val), 5)
+        out[name + ":l2g"] = [before, rc, val.value]
     dev.snapshot()
     best = []
     for rep in range(4):
@@ -58,7 +65,7 @@ def main():
         if lib.endswith("/"):  # a package tree (another revision): its own python + library
             root = os.path.abspath(lib)
             lib = os.path.join(root, "paper_2303_05455_b200", "libivhd_b200.so")
-        code = f"MODE={os.environ.get('MODE', '')!r}\nC3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
+        code = f"L2G={int(os.environ.get('L2G', '0'))}\nMODE={os.environ.get('MODE', '')!r}\nC3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         print(os.path.basename(lib), r.stdout.strip() or r.stderr[-800:], flush=True)
 
