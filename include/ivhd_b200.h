@@ -225,7 +225,7 @@ int ivhd_shard_end(ivhd_ctx* ctx, double* stress_out, double* step_out, int64_t*
  * peers (ivhd_peer_import_local) decide in a separate finalizer kernel instead:
  * ivhd_shard_step / ivhd_shard_finalize launch the two one at a time, so the
  * emulation can run every rank's step before any finalizer.  A rank that
- * does not arrive within 10 s makes the others fail with IVHD_ERR_PEER
+ * does not arrive within 60 s makes the others fail with IVHD_ERR_PEER
  * instead of hanging. */
 #define IVHD_PEER_HANDLE_BYTES 256
 int ivhd_peer_export(ivhd_ctx* ctx, int world, int rank, uint8_t* handle_out);
@@ -242,6 +242,10 @@ int ivhd_peer_pull(ivhd_ctx* ctx, int barrier);
 /* Position records this rank stores into peers per iteration (sum over its
  * vertices of the ranks that gather them) and their bytes. */
 int ivhd_peer_halo(ivhd_ctx* ctx, int64_t* records_out, int64_t* bytes_out);
+/* Peer failure detection: how long a rank waits for the others' arrival
+ * flags (each iteration and at the segment-end barrier) before it gives up
+ * with IVHD_ERR_PEER; default 60 s.  Call after ivhd_peer_import*. */
+int ivhd_peer_set_timeout(ivhd_ctx* ctx, double seconds);
 
 /* Exact kNN graph of the rows of a host (m, n) float64 matrix, computed on
  * `device` (knng.build_exact_knn, knng.py:158-194): row i lists its k nearest

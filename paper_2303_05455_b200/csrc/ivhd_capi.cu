@@ -2085,11 +2085,6 @@ int ivhd_restore(ivhd_ctx* ctx) {
   return IVHD_OK;  // asynchronous: ordered before the next launch on the stream
 }
 
-#ifdef IVHD_TIMELINE
-int ivhd_timeline_dump(long long* out) {
-  return cudaMemcpyFromSymbol(out, ivhd::g_tl, sizeof(ivhd::g_tl)) == cudaSuccess ? 0 : 2;
-}
-#endif
 
 int ivhd_synchronize(ivhd_ctx* ctx) {
   if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
@@ -2311,7 +2306,7 @@ static int peer_alloc(ivhd_ctx* ctx, int world, int rank) {
   pe.stamp = ctx->stamp;
   pe.n_tiles_cap = ctx->n_tiles_cap;
   pe.decide_here = 1;
-  pe.timeout_ns = 10LL * 1000 * 1000 * 1000;
+  pe.timeout_ns = 60LL * 1000 * 1000 * 1000;  // peer failure detection (ranks start segments with skew)
   drop_graphs(ctx);
   return IVHD_OK;
 }
@@ -2389,6 +2384,15 @@ int ivhd_peer_halo(ivhd_ctx* ctx, int64_t* records_out, int64_t* bytes_out) {
   for (uint8_t b : mk) n += __builtin_popcount(b);
   if (records_out) *records_out = n;
   if (bytes_out) *bytes_out = n * (int64_t)sizeof(float) * ys_of(ctx->dim, ctx->opt.kind);
+  return IVHD_OK;
+}
+
+int ivhd_peer_set_timeout(ivhd_ctx* ctx, double seconds) {
+  if (!ctx) return fail(nullptr, IVHD_ERR_INVALID_ARG, "null context");
+  if (!ctx->peer_on) return fail(ctx, IVHD_ERR_STATE, "peer exchange not set up");
+  if (!(seconds > 0.0) || seconds > 3600.0) return fail(ctx, IVHD_ERR_INVALID_ARG, "timeout must be in (0, 3600] s");
+  ctx->pe.timeout_ns = (long long)(seconds * 1e9);
+  drop_graphs(ctx);  // captured launches hold the old arguments
   return IVHD_OK;
 }
 

@@ -37,3 +37,11 @@ KernelInfo kernel_d2(int opt, bool weighted, int norm, bool peer) {
 }
 
 }  // namespace ivhd
+
+#ifdef IVHD_TIMELINE
+// debug builds (tools/timeline.py): the 2-D step kernels live in this unit,
+// so its copy of the timeline buffer is the one they write
+extern "C" int ivhd_timeline_dump(long long* out) {
+  return cudaMemcpyFromSymbol(out, ivhd::g_tl, sizeof(ivhd::g_tl)) == cudaSuccess ? 0 : 2;
+}
+#endif

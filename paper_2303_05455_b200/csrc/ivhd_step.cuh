@@ -588,10 +588,12 @@ __device__ __forceinline__ void apply_update(const StepArgs& A, float* __restric
   for (int d = 0; d < DIM; ++d) la[d] = OPT == OPT_NEST ? yn[d] + A.h.beta * sv[d] : yn[d];  // optim.py:174-175
   store_pos<DIM, OPT>(Yout, v, yn, la);
   if constexpr (PEER) {  // fused exchange: the same record into the replica of every peer that gathers it
-    const bool out1 = Yout == A.ybuf1;
-    const unsigned mk = A.pe.mask[v];
-    for (int q = 0; q < A.pe.n_peers; ++q)
-      if ((mk >> A.pe.prank[q]) & 1u) store_pos<DIM, OPT>(out1 ? A.pe.y1[q] : A.pe.y0[q], v, yn, la);
+    if (A.pe.n_peers > 0) {
+      const bool out1 = Yout == A.ybuf1;
+      const unsigned mk = A.pe.mask[v];
+      for (int q = 0; q < A.pe.n_peers; ++q)
+        if ((mk >> A.pe.prank[q]) & 1u) store_pos<DIM, OPT>(out1 ? A.pe.y1[q] : A.pe.y0[q], v, yn, la);
+    }
   }
   acc_bad += all_finite(yn, DIM) ? 0.f : 1.f;
 }
@@ -793,6 +795,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// release fence at system scope (orders this thread's earlier stores, P2P
+// ones included, before its later flag stores; lighter than fence.sc.sys)
+__device__ __forceinline__ void fence_release_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -831,9 +841,14 @@ __device__ __forceinline__ void peer_rank_publish(const StepArgs& A, int n_block
     const size_t slot = (size_t)(stamp & 1) * A.pe.world + A.pe.rank;
     A.pe.tp_local[slot] = s;
     for (int q = 0; q < A.pe.n_peers; ++q) A.pe.tp[q][slot] = s;
-    __threadfence_system();
-    st_release_sys(A.pe.fl_local + A.pe.rank, stamp);
-    for (int q = 0; q < A.pe.n_peers; ++q) st_release_sys(A.pe.fl[q] + A.pe.rank, stamp);
+    if (A.pe.n_peers > 0) {
+      fence_release_sys();
+      st_release_sys(A.pe.fl_local + A.pe.rank, stamp);
+      for (int q = 0; q < A.pe.n_peers; ++q) st_release_sys(A.pe.fl[q] + A.pe.rank, stamp);
+    } else {  // one rank: nothing leaves this GPU, GPU scope is enough
+      __threadfence();
+      *reinterpret_cast<volatile unsigned long long*>(A.pe.fl_local + A.pe.rank) = stamp;
+    }
   }
   __syncwarp();
 }
@@ -851,7 +866,8 @@ __device__ __forceinline__ void peer_decide(const StepArgs& A) {
     const unsigned long long* f = A.pe.fl_local + lane;
     long long t0 = 0, t1 = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (ld_acquire_sys(f) < stamp) {
+    // own flag: written by this GPU (GPU scope); the peers' over NVLink (system)
+    while ((lane == A.pe.rank ? ld_acquire_gpu(f) : ld_acquire_sys(f)) < stamp) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       if (t1 - t0 > A.pe.timeout_ns) {
         fail = 1;
@@ -1289,7 +1305,9 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       t.x += sm_wacc[w].x; t.y += sm_wacc[w].y; t.z += sm_wacc[w].z; t.w += sm_wacc[w].w;
     }
     A.bpart[blockIdx.x] = t;
-    if constexpr (PEER) __threadfence_system();  // this block's P2P position stores first
+    if constexpr (PEER) {  // this block's P2P position stores first (none with one rank)
+      if (A.pe.n_peers > 0) fence_release_sys();
+    }
     unsigned old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&ctrl->arrive) : "memory");
     last = old == gridDim.x - 1;
@@ -1301,6 +1319,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     peer_rank_publish(A, (int)gridDim.x);
     if (A.pe.decide_here) peer_decide<OPT>(A);  // ranks on separate GPUs: no finalizer launch
     else if (lane == 0) ctrl->arrive = 0;       // the finalizer kernel decides (in-process emulation)
+    IVHD_TL(39);
     return;
   }
   finalize_warp<OPT>(A, A.bpart, (int)gridDim.x);

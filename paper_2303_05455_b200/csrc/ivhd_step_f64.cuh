@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
   int last = 0;
   if (lane == 0) {
     A.bpart[blockIdx.x] = r;
-    if (A.pe.on) __threadfence_system();  // this block's P2P position stores first
+    if (A.pe.on && A.pe.n_peers > 0) fence_release_sys();  // this block's P2P position stores first
     unsigned old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&ctrl->arrive) : "memory");
     last = old == gridDim.x - 1;

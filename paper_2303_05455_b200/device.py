@@ -299,6 +299,11 @@ class DeviceEmbedding:
         self._check(self.lib.ivhd_peer_halo(self.h, ctypes.byref(n), ctypes.byref(b)))
         return n.value, b.value
 
+    def peer_set_timeout(self, seconds):
+        """Peer failure detection: wait at most `seconds` for the other ranks'
+        arrival flags, then fail with IVHD_ERR_PEER (DeviceError, status 5) instead of hanging."""
+        self._check(self.lib.ivhd_peer_set_timeout(self.h, float(seconds)))
+
     # asynchronous sharded loop (include/ivhd_b200.h, ivhd_shard_*)
     def shard_begin(self, slot, c, n_iter):
         """Returns (index of the buffer holding the current positions, graph

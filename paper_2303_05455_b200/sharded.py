@@ -96,6 +96,25 @@ def _allgather_inplace(buf, rank, world, group=None):
         buf.copy_(torch.cat(parts))
 
 
+def _peer_capable(device, group=None):
+    """True on every rank iff all ranks share one host and every pair of
+    their GPUs can access each other's memory (collective over `group`)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    me = (socket.gethostname(), int(device))
+    ranks = [None] * world
+    dist.all_gather_object(ranks, me, group=group)
+    ok = all(h == me[0] for h, _ in ranks) and all(
+        d == me[1] or torch.cuda.can_device_access_peer(me[1], d) for _, d in ranks)
+    oks = [None] * world
+    dist.all_gather_object(oks, bool(ok), group=group)
+    return all(oks)
+
+
 class ShardedEmbedding:
     """One rank's share of a distributed IVHD run (same surface as
     DeviceEmbedding for set-up; `run` drives the per-iteration exchange)."""
@@ -116,6 +135,14 @@ class ShardedEmbedding:
         self.ranges = shard_ranges(n_tiles_cap, tile_v, self.world)
         self.v0, self.v1 = self.ranges[self.rank]
         backend.shard_set_range(self.v0, self.v1)
+        if self.exchange == "p2p" and self.world > 1 and not _peer_capable(device, group):
+            # some pair of ranks cannot map each other's memory (another node,
+            # no P2P path): every rank falls back to the NCCL all-gather
+            import torch.distributed as dist
+
+            self.exchange = "nccl"
+            if dist.get_backend(group) != "nccl":
+                self.group = group = dist.new_group(backend="nccl")
         if self.exchange == "p2p":
             # fused NVLink exchange (include/ivhd_b200.h ivhd_peer_*): every
             # rank publishes its buffers' CUDA IPC handles, opens the others'

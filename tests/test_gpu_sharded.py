@@ -258,3 +258,35 @@ def test_halo_masks_cut_the_exchanged_records():
     expect = sum(1 for v, r in pairs if v // range_v != r)
     assert sum(recs) == expect
     assert sum(recs) < 0.45 * (world - 1) * m
+
+
+def test_peer_exchange_missing_rank_fails_instead_of_hanging():
+    """Failure detection: a rank whose peer never arrives gives up after the
+    peer timeout with IVHD_ERR_PEER (status 3 on the device), no hang."""
+    import time
+
+    from paper_2303_05455_b200.errors import DeviceError
+
+    nb = hub_graph(seed=3)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ranks = [_setup(nb, 2, r, stream, iters=3)[0] for r in range(2)]
+        devs = [sh.backend.dev for sh in ranks]
+        for r, d in enumerate(devs):
+            d.peer_export(2, r)
+        for d in devs:
+            d.peer_import_local(devs)
+        d0 = devs[0]
+        d0.peer_set_timeout(0.25)
+        d0.shard_begin(0, 0.1, 3)
+        t0 = time.time()
+        for _ in range(3):  # rank 1 never steps
+            d0.shard_step(0, "l2")
+            d0.shard_finalize()
+        with pytest.raises(DeviceError, match="status 5"):
+            d0.shard_end()
+        assert time.time() - t0 < 20
+        with pytest.raises(P.InvalidArgumentError):
+            d0.peer_set_timeout(0.0)
+        for d in devs:
+            d.close()

@@ -1,4 +1,5 @@
-"""Block timeline of two consecutive step-kernel launches (iterations 10, 11)
+"""(PEER=1: the one-rank peer-exchange instantiation.)
+Block timeline of two consecutive step-kernel launches (iterations 10, 11)
 at C3, from a debug build:  python tools/build_variant.py tl -DIVHD_TIMELINE
 then on the GPU box:  IVHD_B200_LIB=sweep/lib_tl.so python tools/timeline.py"""
 import ctypes, os, sys
@@ -22,6 +23,10 @@ else:
 m = nb.shape[0]
 g = np.random.default_rng(0)
 dev = DeviceEmbedding(m, 2)
+if os.environ.get("PEER"):  # sharded kernels with the fused peer exchange, one rank
+    tv, nt = dev.tiles()
+    dev.shard_set_range(0, tv * nt)
+    dev.peer_import([dev.peer_export(1, 0)])
 dev.set_optimizer(resolve_optimizer("force-directed", m))
 dev.init_positions(g)
 dev.set_graph_sampled(0, nb[:, :2], 1, g)

@@ -29,7 +29,7 @@ for name in GRAPHS:
         nb = synth.planted_graph(int(mm), int(kind[7:] or 2), seed=0)
     m = nb.shape[0]
     rng = np.random.default_rng(0)
-    y0 = init_layout(m, 2, rng); rn = sample_random_neighbors(m, nb, 1, rng)
+    y0 = init_layout(m, 2, rng); rn = sample_random_neighbors(m, nb, RN, rng)
     dev = DeviceEmbedding(m, 2)
     if MODE == "peer1":  # the fused peer exchange with one rank (sharded kernels + finalizer)
         tv, nt = dev.tiles()
@@ -65,7 +65,7 @@ def main():
         if lib.endswith("/"):  # a package tree (another revision): its own python + library
             root = os.path.abspath(lib)
             lib = os.path.join(root, "paper_2303_05455_b200", "libivhd_b200.so")
-        code = f"L2G={int(os.environ.get('L2G', '0'))}\nMODE={os.environ.get('MODE', '')!r}\nC3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
+        code = f"RN={int(os.environ.get('RN', '1'))}\nL2G={int(os.environ.get('L2G', '0'))}\nMODE={os.environ.get('MODE', '')!r}\nC3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         print(os.path.basename(lib), r.stdout.strip() or r.stderr[-800:], flush=True)
 
