@@ -445,6 +445,16 @@ def gpu_arm(args, w):
     value = L * iters * args.steps / tot
     s_iter = tot / (args.steps * iters)
     dev_launches = dev.launches_per_iteration() if hasattr(dev, "launches_per_iteration") else 1
+    gfloor = None
+    if not sharded:
+        # the same neighbour gathers with nothing else (ivhd_gather_floor): the
+        # memory-system floor of an iteration on this graph, beside the HBM roofline
+        g_us = dev.gather_floor(0)
+        gfloor = {"us_per_pass": g_us, "us_per_iteration": s_iter * 1e6, "frac": g_us / (s_iter * 1e6),
+                  "entries_per_pass": n_entries,
+                  "note": "one pass streaming the column ids and gathering every neighbour position "
+                          "(no arithmetic, update or decision), CUDA events, warm L2, best of 10; "
+                          "frac = that floor / the step kernel's time per iteration"}
     nvlink = None
     if sharded and getattr(dev, "exchange", None) == "p2p":
         # fused exchange: position records this rank stores into peers per
@@ -541,6 +551,7 @@ def gpu_arm(args, w):
                          "algorithmic_bytes_per_launch": nbytes,
                          "note": f"algorithmic bytes {nbytes} per iteration (8L+36M for FD) / device time "
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
+            "gather_floor": gfloor,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps * iters * dev_launches, "clocks": clk.summary(), "nvlink": nvlink,
             "final_stress_e2e": final_stress,

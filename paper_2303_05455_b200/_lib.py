@@ -66,6 +66,7 @@ SIGNATURES = {
     "ivhd_set_degenerate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_i32p, c_i32p, c_f64p]),
     "ivhd_peer_halo": (ctypes.c_int, [ctypes.c_void_p, c_i64p, c_i64p]),
     "ivhd_peer_set_timeout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double]),
+    "ivhd_gather_floor": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_f64p]),
     "ivhd_set_connections": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i32p, c_u8p, c_f64p,
                                             c_f64p, ctypes.c_int64]),
     "ivhd_set_positions": (ctypes.c_int, [ctypes.c_void_p, c_f64p]),

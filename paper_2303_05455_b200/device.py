@@ -299,6 +299,14 @@ class DeviceEmbedding:
         self._check(self.lib.ivhd_peer_halo(self.h, ctypes.byref(n), ctypes.byref(b)))
         return n.value, b.value
 
+    def gather_floor(self, slot=0, reps=10):
+        """Device time (us) of one gather-only pass over the slot's connections:
+        the column ids streamed and every neighbour position gathered, nothing
+        else (ivhd_gather_floor) — the memory-system floor of one iteration."""
+        us = ctypes.c_double()
+        self._check(self.lib.ivhd_gather_floor(self.h, int(slot), int(reps), ctypes.byref(us)))
+        return us.value
+
     def peer_set_timeout(self, seconds):
         """Peer failure detection: wait at most `seconds` for the other ranks'
         arrival flags, then fail with IVHD_ERR_PEER (DeviceError, status 5) instead of hanging."""

@@ -362,3 +362,36 @@ def test_run_embedding_distributed_world1_matches_run_embedding():
     np.testing.assert_allclose(b.trace.stress, a.trace.stress, rtol=1e-5)
     assert b.trace.step_size == a.trace.step_size
     np.testing.assert_array_equal(b.state.rn_assignments, a.state.rn_assignments)
+
+
+def test_gather_floor_is_below_the_step_time():
+    """ivhd_gather_floor: the gather-only pass over the CSR takes less device
+    time than a full iteration on the same graph (positive, finite)."""
+    import time
+
+    from paper_2303_05455_b200.config import resolve_optimizer
+    from paper_2303_05455_b200.device import DeviceEmbedding
+    from paper_2303_05455_b200.embed import init_layout, sample_random_neighbors
+
+    nb = _problem(200_000)
+    m = nb.shape[0]
+    rng = np.random.default_rng(0)
+    dev = DeviceEmbedding(m, 2)
+    dev.set_optimizer(resolve_optimizer("force-directed", m))
+    dev.set_positions(init_layout(m, 2, rng))
+    dev.set_graph(0, nb[:, :3], sample_random_neighbors(m, nb[:, :3], 1, rng))
+    g = dev.gather_floor(0, reps=5)
+    dev.run(0, "l2", 0.1, 50)
+    dev.synchronize()
+    t0 = time.perf_counter()
+    dev.run(0, "l2", 0.1, 200)
+    dev.synchronize()
+    per_iter = (time.perf_counter() - t0) / 200 * 1e6
+    dev.close()
+    assert 0.0 < g < per_iter
+    fresh = DeviceEmbedding(m, 2)
+    with pytest.raises(P.DeviceError, match="not set"):
+        fresh.gather_floor(0)  # no connection set yet
+    with pytest.raises(P.InvalidArgumentError):
+        fresh.gather_floor(2)
+    fresh.close()
