@@ -453,7 +453,7 @@ def gpu_arm(args, w):
         gfloor = {"us_per_pass": g_us, "us_per_iteration": s_iter * 1e6, "frac": g_us / (s_iter * 1e6),
                   "entries_per_pass": n_entries,
                   "note": "one pass streaming the column ids and gathering every neighbour position "
-                          "(no arithmetic, update or decision), CUDA events, warm L2, best of 10; "
+                          "(no arithmetic, update or decision), CUDA events, warm L2, best of 10 in each of three sweeps (per-block slices at 8 and 3 blocks per SM, whole grid front to back); "
                           "frac = that floor / the step kernel's time per iteration"}
     nvlink = None
     if sharded and getattr(dev, "exchange", None) == "p2p":

@@ -248,12 +248,13 @@ int ivhd_peer_halo(ivhd_ctx* ctx, int64_t* records_out, int64_t* bytes_out);
 int ivhd_peer_set_timeout(ivhd_ctx* ctx, double seconds);
 
 /* ---- diagnostics (new; no reference counterpart) ----------------------
- * Gather floor of a connection set: one pass that streams the slot's column
+ * Gather floor of a connection set: a pass that streams the slot's column
  * ids and gathers every neighbour position (the step kernel's only random
- * traffic) with nothing else — no arithmetic, no update, no decision.  Its
- * device time per pass (CUDA events, warm L2, best of `reps`) is the
- * memory-system floor of one iteration on this graph; bench.py reports the
- * step kernel's time against it. */
+ * traffic) with nothing else — no arithmetic, no update, no decision — in
+ * three sweep orders (per-block slices at 8 and 3 blocks per SM, the whole
+ * grid front to back).  The best device time per pass (CUDA events, warm L2,
+ * `reps` passes of each) is the memory-system floor of one iteration on this
+ * graph; bench.py reports the step kernel's time against it. */
 int ivhd_gather_floor(ivhd_ctx* ctx, int slot, int reps, double* us_out);
 
 /* Exact kNN graph of the rows of a host (m, n) float64 matrix, computed on

@@ -2088,29 +2088,53 @@ int ivhd_restore(ivhd_ctx* ctx) {
 
 }  // extern "C"
 
-// gather-only pass over a CSR (ivhd_gather_floor): 8 column ids and 8
-// position gathers in flight per thread, the same load instructions as the
-// step kernel (streamed ids, L1-allocating position loads)
-template <int YS>
+// gather-only pass over a CSR (ivhd_gather_floor), in one of two orders:
+// BLOCKED (8 or, like the step kernel, 3 blocks per SM) — every block sweeps
+// one contiguous slice of the column ids, as the
+// step kernel's blocks sweep contiguous unit ranges (id-local neighbourhoods
+// are reused in L1); STRIDED — the whole grid sweeps the ids front to back
+// (no per-SM locality, all SMs on one region of L2).  8 column ids and 8
+// position gathers in flight per thread, the step kernel's load instructions
+// (streamed ids, evict-first in L2 when the working set exceeds it;
+// L1-allocating position loads).
+__device__ __forceinline__ uint32_t ld_col_first(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <int YS, bool BLOCKED>
 __global__ void k_gather_floor(const uint32_t* __restrict__ col, int64_t n, const float* __restrict__ Y,
-                               float* __restrict__ sink) {
+                               int stream_hint, float* __restrict__ sink) {
   using V = typename std::conditional<YS == 2, float2, float4>::type;
+  constexpr int kStride = YS / (int)(sizeof(V) / 4);
   const V* Yv = reinterpret_cast<const V*>(Y);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t b0 = 0, b1 = n, i, stride;
+  if (BLOCKED) {
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    b0 = blockIdx.x * per;
+    b1 = min(n, b0 + per);
+    i = b0 + threadIdx.x;
+    stride = blockDim.x;
+  } else {
+    i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    stride = (int64_t)gridDim.x * blockDim.x;
+  }
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   float acc = 0.f;
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  for (; i + 7 * stride < n; i += 8 * stride) {
+  for (; i + 7 * stride < b1; i += 8 * stride) {
     uint32_t j[8];
     V p[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) j[q] = ld_col(col + i + q * stride) & kIdMask;
+    for (int q = 0; q < 8; ++q)
+      j[q] = (stream_hint ? ld_col_first(col + i + q * stride, pol) : ld_col(col + i + q * stride)) & kIdMask;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) p[q] = __ldg(Yv + (size_t)j[q] * (YS / (sizeof(V) / 4)));
+    for (int q = 0; q < 8; ++q) p[q] = __ldg(Yv + (size_t)j[q] * kStride);
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc += p[q].x * p[q].y;
   }
-  for (; i < n; i += stride) {
-    const V p = __ldg(Yv + (size_t)(ld_col(col + i) & kIdMask) * (YS / (sizeof(V) / 4)));
+  for (; i < b1; i += stride) {
+    const V p = __ldg(Yv + (size_t)(ld_col(col + i) & kIdMask) * kStride);
     acc += p.x * p.y;
   }
   if (acc == 1.2345e-30f) *sink = acc;  // keeps the loads
@@ -2126,25 +2150,32 @@ int ivhd_gather_floor(ivhd_ctx* ctx, int slot, int reps, double* us_out) {
   const int ys = ys_now(ctx);
   const float* y = ctx->ybuf[ctx->ctrl_h->cur];
   float* sink = reinterpret_cast<float*>(ctx->stage);
-  const int grid = ctx->sm_count * 8;
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+  const int hint = 4 * S.n + (int64_t)4 * ctx->m * ys > (int64_t)l2 ? 1 : 0;
+  int which = 0;  // launch order: blocked (8 and 3 blocks per SM), strided; the best is the floor
   auto launch = [&] {
-    if (ys == 2) k_gather_floor<2><<<grid, 256, 0, ctx->stream>>>(S.col, S.n, y, sink);
-    else if (ys == 4) k_gather_floor<4><<<grid, 256, 0, ctx->stream>>>(S.col, S.n, y, sink);
-    else k_gather_floor<8><<<grid, 256, 0, ctx->stream>>>(S.col, S.n, y, sink);
+    const int grid = ctx->sm_count * (which == 1 ? 3 : 8);
+#define IVHD_GF(Y)                                                                                   \
+  if (which < 2) k_gather_floor<Y, true><<<grid, 256, 0, ctx->stream>>>(S.col, S.n, y, hint, sink); \
+  else k_gather_floor<Y, false><<<grid, 256, 0, ctx->stream>>>(S.col, S.n, y, hint, sink);
+    if (ys == 2) { IVHD_GF(2) } else if (ys == 4) { IVHD_GF(4) } else { IVHD_GF(8) }
+#undef IVHD_GF
   };
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   CU(ctx, cudaEventCreate(&e0));
   CU(ctx, cudaEventCreate(&e1));
   double best = 1e30;
   cudaError_t e = cudaSuccess;
-  for (int r = 0; r < reps + 2 && e == cudaSuccess; ++r) {
+  for (int r = 0; r < 3 * (reps + 2) && e == cudaSuccess; ++r) {
+    which = r % 3;
     cudaEventRecord(e0, ctx->stream);
     launch();
     cudaEventRecord(e1, ctx->stream);
     if ((e = cudaEventSynchronize(e1)) != cudaSuccess) break;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    if (r >= 2) best = std::min(best, (double)ms * 1e3);  // two warm-up passes (L2 warm like the loop's)
+    if (r >= 6) best = std::min(best, (double)ms * 1e3);  // two warm-up passes each (L2 warm like the loop's)
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

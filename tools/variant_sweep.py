@@ -51,6 +51,8 @@ for name in GRAPHS:
         dev.run(0, "l2", 0.1, ITERS); torch.cuda.synchronize()
         best.append((time.perf_counter() - t0) / ITERS * 1e6)
     out[name] = round(min(best[1:]), 2)
+    if FLOOR:  # the gather-only pass over the same connections (ivhd_gather_floor)
+        out[name + ":floor"] = round(dev.gather_floor(0), 2)
     dev.close()
 print(json.dumps(out))
 '''
@@ -65,7 +67,7 @@ def main():
         if lib.endswith("/"):  # a package tree (another revision): its own python + library
             root = os.path.abspath(lib)
             lib = os.path.join(root, "paper_2303_05455_b200", "libivhd_b200.so")
-        code = f"RN={int(os.environ.get('RN', '1'))}\nL2G={int(os.environ.get('L2G', '0'))}\nMODE={os.environ.get('MODE', '')!r}\nC3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
+        code = f"FLOOR={int(os.environ.get('FLOOR', '0'))}\nRN={int(os.environ.get('RN', '1'))}\nL2G={int(os.environ.get('L2G', '0'))}\nMODE={os.environ.get('MODE', '')!r}\nC3={C3!r}\nROOT={root!r}\nLIB={os.path.abspath(lib)!r}\nGRAPHS={graphs!r}\nITERS={iters}\n" + CHILD
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         print(os.path.basename(lib), r.stdout.strip() or r.stderr[-800:], flush=True)
 
