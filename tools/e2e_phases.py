@@ -7,8 +7,8 @@ import torch
 from paper_2303_05455_b200 import EmbeddingConfig, KnnGraph, run_embedding, synth
 from paper_2303_05455_b200 import device as D
 
-cache = "/tmp/ivhd_graph_v2_mixture_1400000_100_2.npy"
-nb = np.load(cache) if os.path.exists(cache) else synth.mixture_knn_graph(1_400_000, 100, k=2, seed=0)[0]
+nb = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                          "c3_graph.npz"))["neighbors"]  # the C3 bench fixture
 T = {}
 def wrap(cls, name):
     f = getattr(cls, name)
