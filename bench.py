@@ -223,20 +223,21 @@ class ReferenceTimer:
             self.kind = "port"
             self.nb = nb
 
-    def call(self, n):
+    def call(self, n, threads=None):
         w = self.w
+        threads = threads or self.threads
         t0 = time.perf_counter()
         if self.kind == "reference":
             E = self.ivhd.engine
             cfg = E.EmbeddingConfig(nn=w["nn"], rn=w["rn"], c=w["c"], iterations=n, seed=0,
                                     optimizer=w["optimizer"])
-            E.run_embedding(graph=self.graph, config=cfg, threads=self.threads)
+            E.run_embedding(graph=self.graph, config=cfg, threads=threads)
         else:
             sys.path.insert(0, ROOT)
             from oracle.ivhd_oracle import OracleRun
 
             OracleRun(self.nb, nn=w["nn"], rn=w["rn"], c=w["c"], iterations=n, seed=0,
-                      optimizer=w["optimizer"], threads=self.threads).run()
+                      optimizer=w["optimizer"], threads=threads).run()
         return time.perf_counter() - t0
 
     def pick_n(self, budget_s):
@@ -524,6 +525,9 @@ def gpu_arm(args, w):
         n = rt.pick_n(args.cpu_budget / 3)
         ts = [rt.call(n) for _ in range(2)]
         cpu = rt.describe(n, rt.L * n * len(ts) / sum(ts))
+        n1 = max(1, n // 4)  # the same on one thread (T=1 and T=all cores)
+        cpu["value_1_thread"] = rt.L * n1 / rt.call(n1, threads=1)
+        cpu["sample_1_thread"] = f"run_embedding(iterations={n1}), threads=1"
     knn = None
     if world == 1 and rank == 0 and not args.no_knn:
         knn = knn_leg(w, local, peaks, nb)
