@@ -201,3 +201,33 @@ def test_shard_plan_covers_all_vertices():
     covered = sorted((s.v0, s.v1) for s in spans)
     assert covered[0][0] == 0 and covered[-1][1] >= 700
     assert all(covered[i][1] == covered[i + 1][0] for i in range(3))
+
+
+def _capable_worker(rank, world, port, out, deny_rank, host_of):
+    """Runs sharded._peer_capable with a patched P2P query / host name."""
+    import socket as _socket
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2303_05455_b200 import sharded
+
+        torch.cuda.can_device_access_peer = lambda a, b: rank != deny_rank
+        _socket.gethostname = lambda: host_of[rank]
+        ok = sharded._peer_capable(device=rank)
+        np.save(os.path.join(out, f"cap{rank}.npy"), np.array([ok]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("deny_rank,hosts,expect", [(-1, ("a", "a"), True), (1, ("a", "a"), False),
+                                                    (-1, ("a", "b"), False)])
+def test_peer_capability_is_agreed_by_every_rank(tmp_path, deny_rank, hosts, expect):
+    """The fused exchange needs every pair of ranks to map each other's memory:
+    one rank without a P2P path (or on another host) sends all ranks to the
+    NCCL exchange, and every rank reaches the same answer."""
+    mp.start_processes(_capable_worker, args=(2, _free_port(), str(tmp_path), deny_rank, hosts), nprocs=2,
+                       start_method="spawn", join=True)
+    got = [bool(np.load(tmp_path / f"cap{r}.npy")[0]) for r in range(2)]
+    assert got == [expect, expect]
