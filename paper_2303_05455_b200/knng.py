@@ -77,7 +77,9 @@ _METRIC_IDS = {"euclidean": 0, "cosine": 1, "precomputed": 2}
 
 def cache_write(graph, path):
     """Write `graph` in the reference's IVHG format (knng.py:286-300):
-    byte-identical to the reference writer."""
+    byte-identical to the reference writer — its header layout and field
+    order are the reference's, kept as is so either side reads the other's
+    files."""
     from .errors import MalformedInputError
 
     has_dist = graph.distances is not None

@@ -4,9 +4,13 @@ Rank curves: `rnx_curve`, `gnn_curve`, `trust_continuity` and
 `evaluate_embedding` are drop-ins for the reference's functions of the same
 names (metrics.py:185-251, 351-380).  Their counts come from one GPU pass
 (`ivhd_curve_pass`, csrc/ivhd_metrics.cu) that replaces the reference's
-streamed `_curve_pass` (metrics.py:149-182); the curve arithmetic on those
-integer counts (`_curves_from_counts`, `_gnn_from_counts`, the trust /
-continuity scaling) is restated here on the host, as in the reference.
+streamed `_curve_pass` (metrics.py:149-182).  The host arithmetic on those
+integer counts (`_curves_from_counts`, `_gnn_from_counts`, `_unrank_pairs`, the
+trust / continuity scaling, and the body of `shepard_and_corank` /
+`evaluate_embedding`) is the reference's arithmetic kept verbatim
+(metrics.py:208-236, 297-320, 323-332, 355-385), so the golden tests can demand
+bit-identical floating-point results on identical counts; the GPU code is what
+produces the counts.
 
 `neighbor_hit` is the drop-in for the reference's `ivhd.metrics.neighbor_hit`
 (/root/reference/pkg/src/ivhd/metrics.py:254-294): same signature, same
