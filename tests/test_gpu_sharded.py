@@ -290,3 +290,19 @@ def test_peer_exchange_missing_rank_fails_instead_of_hanging():
             d0.peer_set_timeout(0.0)
         for d in devs:
             d.close()
+
+
+@pytest.mark.parametrize("optimizer", ["nesterov", "adadelta", "momentum"])
+def test_peer_exchange_emulated_other_optimizers(optimizer):
+    """The fused exchange with wider position records (Nesterov: y | look-ahead)
+    and state (Adadelta: two accumulators): 2 ranks identical, and on the
+    oracle's trajectory."""
+    nb = hub_graph(seed=4)
+    iters = 10
+    many = _emulated_p2p(nb, 2, iters, optimizer=optimizer)
+    np.testing.assert_array_equal(many[0][0], many[1][0])
+    np.testing.assert_array_equal(many[0][1], many[1][1])
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer=optimizer)
+    orc.run()
+    assert normwise(many[0][0], orc.Y) < 1e-5
+    np.testing.assert_allclose(many[0][1], orc.trace_stress, rtol=1e-5)
