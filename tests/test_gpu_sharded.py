@@ -306,3 +306,46 @@ def test_peer_exchange_emulated_other_optimizers(optimizer):
     orc.run()
     assert normwise(many[0][0], orc.Y) < 1e-5
     np.testing.assert_allclose(many[0][1], orc.trace_stress, rtol=1e-5)
+
+
+@pytest.mark.parametrize("opt", ["force-directed", "adam"])
+def test_peer_exchange_world1_pauses_for_degenerate_pairs(opt):
+    """The sharded kernels with the fused exchange (one rank) meet random pairs
+    at zero distance: the pause decision, the host draw and the re-run through
+    the weighted PEER instantiation follow the oracle like the fused loop."""
+    from paper_2303_05455_b200 import degenerate, synth
+    from paper_2303_05455_b200.config import resolve_optimizer
+    from paper_2303_05455_b200.sharded import ShardedEmbedding
+
+    m = 5000
+    nb = synth.planted_graph(m, 2, seed=4)
+    orc = OracleRun(nb, nn=2, rn=1, c=0.1, iterations=6, seed=9, optimizer=opt)
+    y0 = orc.Y.copy()
+    src = np.arange(0, m, 97)
+    y0[orc.rn_assign[src, 0]] = y0[src]  # coincident random pairs
+    orc.Y = y0.copy()
+    gen = np.random.Generator(np.random.PCG64())
+    gen.bit_generator.state = orc.rng.bit_generator.state
+    conn = orc.full
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        sh = ShardedEmbedding(m, 2, 0, 1, device=0, stream=stream.cuda_stream)  # exchange="p2p"
+        assert sh.exchange == "p2p"
+        sh.set_optimizer(resolve_optimizer(opt, m))
+        sh.set_positions(y0)
+        sh.set_graph(0, nb, orc.rn_assign)
+        calls = []
+
+        def resolver(slot, rows, entries):
+            calls.append(len(rows))
+            return degenerate.table(rows, entries, conn.src, conn.dst, conn.weights(0.1) * conn.target, gen, 2)
+
+        sh.device_embedding.degenerate_resolver = resolver
+        st, bb, done, div = sh.run(0, "l2", 0.1, 6)
+        y = sh.positions()
+        sh.close()
+    assert done == 6 and not div and calls
+    orc.run(6)
+    assert normwise(y, orc.Y) < 1e-5
+    np.testing.assert_allclose(st, orc.trace_stress, rtol=1e-5)
+    assert gen.bit_generator.state == orc.rng.bit_generator.state
