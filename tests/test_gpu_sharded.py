@@ -35,15 +35,16 @@ def hub_graph(m=20000, k=3, seed=0):
     return nb.astype(np.int32)
 
 
-def _setup(nb, world, rank, stream, optimizer="force-directed", iters=12, integrator=None):
+def _setup(nb, world, rank, stream, optimizer="force-directed", iters=12, integrator=None, dim=2):
     from paper_2303_05455_b200.config import resolve_optimizer
     from paper_2303_05455_b200.sharded import ShardedEmbedding
 
     m = nb.shape[0]
-    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer=optimizer, integrator=integrator)
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer=optimizer, integrator=integrator,
+                    target_dim=dim)
     # exchange="nccl": no automatic peer set-up (that needs a process group);
     # the p2p emulation below connects the contexts itself
-    sh = ShardedEmbedding(m, 2, rank, world, device=0, stream=stream.cuda_stream, exchange="nccl")
+    sh = ShardedEmbedding(m, dim, rank, world, device=0, stream=stream.cuda_stream, exchange="nccl")
     sh.set_optimizer(resolve_optimizer(optimizer, m, integrator=integrator and P.IntegratorParams(**integrator)))
     sh.set_positions(orc.Y)
     sh.set_graph(0, nb[:, :3], orc.rn_assign)
@@ -129,7 +130,7 @@ def test_emulated_ranks_rollbacks_and_adam():
     assert normwise(many[0][0], orc.Y) < 1e-5
 
 
-def _emulated_p2p(nb, world, iters, optimizer="force-directed", integrator=None):
+def _emulated_p2p(nb, world, iters, optimizer="force-directed", integrator=None, dim=2):
     """The fused peer exchange (ivhd_peer_*) with `world` contexts in one
     process: ivhd_peer_export on each, ivhd_peer_import_local with the
     contexts as peers; per iteration every rank's step kernel (it stores into
@@ -137,7 +138,7 @@ def _emulated_p2p(nb, world, iters, optimizer="force-directed", integrator=None)
     flags are already up: nothing waits on a kernel that has not run)."""
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        ranks = [_setup(nb, world, r, stream, optimizer=optimizer, iters=iters, integrator=integrator)[0]
+        ranks = [_setup(nb, world, r, stream, optimizer=optimizer, iters=iters, integrator=integrator, dim=dim)[0]
                  for r in range(world)]
         devs = [sh.backend.dev for sh in ranks]
         for r, d in enumerate(devs):
@@ -349,3 +350,19 @@ def test_peer_exchange_world1_pauses_for_degenerate_pairs(opt):
     assert normwise(y, orc.Y) < 1e-5
     np.testing.assert_allclose(st, orc.trace_stress, rtol=1e-5)
     assert gen.bit_generator.state == orc.rng.bit_generator.state
+
+
+@pytest.mark.parametrize("optimizer", ["force-directed", "nesterov"])
+def test_peer_exchange_emulated_target_dim3(optimizer):
+    """3-D records (float4 positions; Nesterov: y | look-ahead in 8 floats)
+    through the fused exchange at 4 ranks."""
+    nb = hub_graph(seed=5)
+    iters = 8
+    many = _emulated_p2p(nb, 4, iters, optimizer=optimizer, dim=3)
+    for y, st, bb in many[1:]:
+        np.testing.assert_array_equal(y, many[0][0])
+    orc = OracleRun(nb, nn=3, rn=1, c=0.1, iterations=iters, seed=0, optimizer=optimizer, target_dim=3)
+    orc.run()
+    assert many[0][0].shape[1] == 3
+    assert normwise(many[0][0], orc.Y) < 1e-5
+    np.testing.assert_allclose(many[0][1], orc.trace_stress, rtol=1e-5)
