@@ -337,19 +337,23 @@ def test_pinned_pool_cap_releases_pooled_buffers():
     assert float(e.sum()) == e.size and float(c.sum()) == 2 * c.size
 
 
-def test_run_embedding_distributed_world1_matches_run_embedding():
+@pytest.mark.parametrize("phased", [False, True])
+def test_run_embedding_distributed_world1_matches_run_embedding(phased):
     """The public multi-GPU entry point (sharded.run_embedding_distributed) on
     a one-rank NCCL group: same RunResult contract and trajectory as
     run_embedding on a hub-heavy mixture kNN graph (snake-dealt rank groups:
-    a different vertex order, so equal to fp32 summation order)."""
+    a different vertex order, so equal to fp32 summation order).  phased: rn
+    resampling, the RNN-filtered phase (weighted connection set) and the L1
+    phase through the sharded (peer) kernels."""
     import torch
     import torch.distributed as dist
 
     from paper_2303_05455_b200 import synth
     from paper_2303_05455_b200.sharded import run_embedding_distributed
 
-    nb, _, _ = synth.mixture_knn_graph(30000, 50, k=3, seed=3, spread=0.5)
-    cfg = P.EmbeddingConfig(nn=3, rn=1, c=0.1, iterations=50, seed=5)
+    nb, _, _ = synth.mixture_knn_graph(30000, 50, k=12, seed=3, spread=0.5)  # k = 4 nn: its own RNN helper
+    extra = dict(rn_resample_period=7, rnn_final_steps=10, l1_final_steps=8) if phased else {}
+    cfg = P.EmbeddingConfig(nn=3, rn=1, c=0.1, iterations=50, seed=5, **extra)
     a = P.run_embedding(graph=P.KnnGraph(nb), config=cfg)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
