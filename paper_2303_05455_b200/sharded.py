@@ -11,12 +11,14 @@ the positions and updates the vertices of its tile-aligned range [v0, v1)
 
 * "p2p" (default on GPUs) — the fused exchange of ivhd_peer_* (one process
   per GPU, one node): the step kernel stores each updated position straight
-  into every peer's replica over NVLink (CUDA IPC mappings) as it is
-  computed, so the transfer overlaps the update tile by tile; its last block
-  stores the rank's tile partials into every peer and raises an arrival flag
-  on every rank; a one-block finalizer waits for all flags and reduces the
-  tile partials in tile order.  No NCCL, no host work per iteration: the
-  iterations run as CUDA-graph replays of (step, finalizer).
+  into the replica of every peer whose rows gather it (halo masks) over
+  NVLink (CUDA IPC mappings) as it is computed, so the transfer overlaps the
+  update tile by tile; its last block stores the rank's partial into every
+  peer, raises an arrival flag on every rank, waits for all ranks' flags and
+  reduces the rank partials in rank order to the same decision everywhere.
+  No NCCL, no host work per iteration: one launch per iteration, replayed
+  from CUDA graphs.  Ranks that cannot map each other's memory fall back to
+  "nccl".
 * "nccl" — the step writes its slice locally, then the slice and the
   rank's tile partials are all-gathered in place through torch.distributed
   (NCCL; gloo in the CPU tests) and ivhd_shard_finalize reduces them.  Kept
@@ -168,10 +170,11 @@ class ShardedEmbedding:
         return getattr(self.backend, "dev", None)
 
     def launches_per_iteration(self):
-        """Kernels per iteration: p2p = the step kernel (it publishes to the
-        peers itself) + the finalizer; nccl = local update, tile fold,
-        finalizer (NCCL's all-gathers come on top)."""
-        return 2 if self.exchange == "p2p" else 3
+        """Kernels per iteration: p2p = the step kernel alone (it publishes to
+        the peers, waits for their flags and decides in its last block; the
+        finalizer kernel only exists for in-process emulated ranks); nccl =
+        local update, tile fold, finalizer (NCCL's all-gathers come on top)."""
+        return 1 if self.exchange == "p2p" else 3
 
     def step(self, slot, norm, c):
         """One synchronous iteration: local update, exchange, fixed-order
