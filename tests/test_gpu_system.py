@@ -368,9 +368,12 @@ def test_run_embedding_distributed_world1_matches_run_embedding(phased):
     np.testing.assert_array_equal(b.state.rn_assignments, a.state.rn_assignments)
 
 
-def test_gather_floor_is_below_the_step_time():
+@pytest.mark.parametrize("dim,opt", [(2, "force-directed"), (2, "nesterov"), (3, "force-directed"),
+                                     (3, "nesterov")])
+def test_gather_floor_is_below_the_step_time(dim, opt):
     """ivhd_gather_floor: the gather-only pass over the CSR takes less device
-    time than a full iteration on the same graph (positive, finite)."""
+    time than a full iteration on the same graph (positive, finite), for every
+    position record width (2-D / 3-D, with Nesterov's look-ahead: 2, 4, 8 floats)."""
     import time
 
     from paper_2303_05455_b200.config import resolve_optimizer
@@ -380,9 +383,9 @@ def test_gather_floor_is_below_the_step_time():
     nb = _problem(200_000)
     m = nb.shape[0]
     rng = np.random.default_rng(0)
-    dev = DeviceEmbedding(m, 2)
-    dev.set_optimizer(resolve_optimizer("force-directed", m))
-    dev.set_positions(init_layout(m, 2, rng))
+    dev = DeviceEmbedding(m, dim)
+    dev.set_optimizer(resolve_optimizer(opt, m))
+    dev.set_positions(init_layout(m, dim, rng))
     dev.set_graph(0, nb[:, :3], sample_random_neighbors(m, nb[:, :3], 1, rng))
     g = dev.gather_floor(0, reps=5)
     dev.run(0, "l2", 0.1, 50)
@@ -393,7 +396,7 @@ def test_gather_floor_is_below_the_step_time():
     per_iter = (time.perf_counter() - t0) / 200 * 1e6
     dev.close()
     assert 0.0 < g < per_iter
-    fresh = DeviceEmbedding(m, 2)
+    fresh = DeviceEmbedding(m, dim)
     with pytest.raises(P.DeviceError, match="not set"):
         fresh.gather_floor(0)  # no connection set yet
     with pytest.raises(P.InvalidArgumentError):
