@@ -1026,6 +1026,27 @@ int launch_finalize_peer(ivhd_ctx* ctx, const StepArgs& A) {
   return IVHD_OK;
 }
 
+// Deferred decisions: decide the last launch's iteration at the end of a run
+// segment (the launches of the segment each decided their predecessor's).
+template <int OPT>
+__global__ void k_defer_finalize(StepArgs A) {
+  Ctrl* c = A.ctrl;
+  if (!c->pend || threadIdx.x != 0) return;
+  DState d = dstate_load(c);
+  const long long it = d.iter;
+  double2 tr;
+  if (d.status == 0 && decide_core<OPT>(A, fix_read(c, c->pslot), c->needw[c->pslot], d, tr) && A.trace)
+    A.trace[it] = tr;
+  dstate_store(c, d);
+  c->needw[c->pslot] = 0;
+  c->fnf[c->pslot] = 0;
+  for (int q = 0; q < 4; ++q) c->facc[c->pslot][q] = 0ull;
+  c->pend = 0;
+  c->readers = 0;
+  c->next_tile = 0;
+  c->arrive = 0;
+}
+
 int launch_step(ivhd_ctx* ctx, KernelInfo k, const StepArgs& A) {
   const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, k) * ctx->sm_count));
   // Programmatic dependent launch: this grid may become resident while the
@@ -1831,6 +1852,11 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   ctx->ctrl_h->iter = 0;
   ctx->ctrl_h->arrive = 0;
   ctx->ctrl_h->next_tile = 0;
+  ctx->ctrl_h->pend = 0;
+  ctx->ctrl_h->readers = 0;
+  ctx->ctrl_h->needw[0] = ctx->ctrl_h->needw[1] = 0;
+  ctx->ctrl_h->fnf[0] = ctx->ctrl_h->fnf[1] = 0;
+  for (int q = 0; q < 4; ++q) ctx->ctrl_h->facc[0][q] = ctx->ctrl_h->facc[1][q] = 0ull;
   TRY(push_ctrl(ctx));
   CU(ctx, cudaMemsetAsync(ctx->miss_n, 0, sizeof(int), ctx->stream));
   const CsrSlot& S = ctx->slots[slot];
@@ -1838,6 +1864,10 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
   KernelInfo fn = pick_kernel(ctx->dim, ctx->opt.kind, S.ew != nullptr, norm, peer);
   if (peer && ctx->masks_stale) TRY(peer_masks(ctx));
   StepArgs A = make_args(ctx, slot, norm, 1);  // peer mode too: running sums, one partial per block
+  // one GPU, fp32 kernels: each launch decides its predecessor's iteration
+  // (off the critical path of the launch boundary); k_defer_finalize decides
+  // the segment's last one
+  A.defer = (!peer && fn.smem > 0) ? 1 : 0;
   if (A.n_tiles > 0) {  // cost-balanced static schedule over this context's (rank's) units
     const int grid = std::max(1, std::min(A.n_tiles, occupancy(ctx, fn) * ctx->sm_count));
     TRY(build_schedule(ctx, ctx->slots[slot], grid, A.tile0, A.tile0 + A.n_tiles));
@@ -1891,6 +1921,11 @@ int ivhd_run(ivhd_ctx* ctx, int slot, int norm, double c, int64_t n_iter, double
     }
   }
   for (; left > 0; --left) TRY(launch_step(ctx, fn, A));
+  if (A.defer) {
+    if (ctx->opt.kind == OPT_FD) k_defer_finalize<OPT_FD><<<1, 32, 0, ctx->stream>>>(A);
+    else k_defer_finalize<OPT_SGD><<<1, 32, 0, ctx->stream>>>(A);
+    CU(ctx, cudaGetLastError());
+  }
   if (peer && n_iter > 0) TRY(peer_pull(ctx, true));
   return read_trace(ctx, stress_out, step_out, done_out);
 }

@@ -98,6 +98,14 @@ struct Ctrl {
   int scur;             // optimizer-state buffer holding the current state (double buffered)
   int dg_n;             // directions in the degenerate-pair table ...
   long long dg_gstep;   // ... valid for this global iteration only
+  // deferred decisions (single-GPU loop): launch t+1 decides iteration t from
+  // t's block partials before its own work; block 0 persists the decided state
+  int pend;             // the partial sums in slot `pslot` await their decision
+  int pslot;
+  int needw[2];         // per slot: a degenerate pair had no direction
+  unsigned int readers; // blocks of this launch that have read the control block
+  int fnf[2];           // per slot: bit 2q component q was +-inf / out of range, bit 2q+1 NaN
+  unsigned long long facc[2][4];  // per slot: the launch's partials in fixed point (2^-24), summed by atomics
 };
 
 constexpr int kMaxPeers = 7;  // up to 8 ranks (one node)
@@ -167,6 +175,7 @@ struct StepArgs {
   int n_tiles_global;     // work-unit partials reduced by the finalizer
   int norm;               // 0 = L2, 1 = L1
   int fuse_finalize;      // last block reduces + decides (single GPU)
+  int defer;              // fuse_finalize with deferred decisions (Ctrl::pend): the next launch decides
   int fixed_io;           // sharded async mode: read ybuf0, write ybuf1 (host-chosen parity)
   int out_index;          // fixed_io: which context buffer ybuf1 is (becomes ctrl->cur)
   long long v_cap_floats; // fixed_io: floats per position buffer (rollback copy)
@@ -234,16 +243,17 @@ __device__ __forceinline__ void gather(const float* __restrict__ Y, uint32_t j, 
 // turns into a pause (status 2, nothing committed, state not advanced).  The
 // host draws the directions in connection order, fills the table and the
 // iteration is re-run.  Measure-zero: after a random init it never happens.
-__device__ __forceinline__ void record_degenerate(Ctrl* c, int* miss_n, int2* miss, int miss_cap, uint32_t v, int e) {
+__device__ __forceinline__ void record_degenerate(int* need, int* miss_n, int2* miss, int miss_cap, uint32_t v, int e) {
   const int slot = atomicAdd(miss_n, 1);
   if (slot < miss_cap) miss[slot] = make_int2((int)v, e);
-  atomicExch(&c->need, 1);
+  atomicExch(need, 1);
 }
 
 // (out of line, rare path: plain pointers only, so the caller keeps the
 // kernel parameters in the constant bank instead of copying them to a stack)
-static __device__ __noinline__ float4 degenerate_lookup(Ctrl* c, const int2* key, const float4* vec, int* miss_n,
-                                                int2* miss, int miss_cap, uint32_t v, int e, long long gstep) {
+static __device__ __noinline__ float4 degenerate_lookup(Ctrl* c, int* need, const int2* key, const float4* vec,
+                                                int* miss_n, int2* miss, int miss_cap, uint32_t v, int e,
+                                                long long gstep) {
   if (c->dg_gstep == gstep) {
     for (int i = 0; i < c->dg_n; ++i) {
       const int2 k = key[i];
@@ -252,14 +262,14 @@ static __device__ __noinline__ float4 degenerate_lookup(Ctrl* c, const int2* key
   }
   const int slot = atomicAdd(miss_n, 1);
   if (slot < miss_cap) miss[slot] = make_int2((int)v, e);
-  atomicExch(&c->need, 1);
+  atomicExch(need, 1);
   return make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 template <int DIM>
-__device__ __forceinline__ void degenerate_vec(const StepArgs& A, uint32_t v, int e, long long gstep,
+__device__ __forceinline__ void degenerate_vec(const StepArgs& A, int* need, uint32_t v, int e, long long gstep,
                                                float (&u)[DIM]) {
-  const float4 q = degenerate_lookup(A.ctrl, A.dg_key, A.dg_vec, A.miss_n, A.miss, A.miss_cap, v, e, gstep);
+  const float4 q = degenerate_lookup(A.ctrl, need, A.dg_key, A.dg_vec, A.miss_n, A.miss, A.miss_cap, v, e, gstep);
   u[0] = q.x;
   u[1] = q.y;
   if constexpr (DIM == 3) u[2] = q.z;
@@ -383,20 +393,37 @@ __device__ __forceinline__ double4 block_sum4(double4 v, double4* sm /*[kBlock/3
 // sum|dold|^2, #non-finite} (optim.py:80-92 + engine.py:373-384); one thread.
 constexpr double kMissUnit = 4294967296.0;  // sharded partials: .w = #non-finite + 2^32 * (rank had misses)
 
+// The decided part of the control block.
+struct DState {
+  int cur, status, last_commit, scur;
+  long long iter, gstep, diverged_at, adam_t;
+  double step;
+};
+__device__ __forceinline__ DState dstate_load(const Ctrl* c) {
+  DState d;
+  d.cur = c->cur; d.status = c->status; d.last_commit = c->last_commit; d.scur = c->scur;
+  d.iter = c->iter; d.gstep = c->gstep; d.diverged_at = c->diverged_at; d.adam_t = c->adam_t;
+  d.step = c->step;
+  return d;
+}
+__device__ __forceinline__ void dstate_store(Ctrl* c, const DState& d) {
+  c->cur = d.cur; c->status = d.status; c->last_commit = d.last_commit; c->scur = d.scur;
+  c->iter = d.iter; c->gstep = d.gstep; c->diverged_at = d.diverged_at; c->adam_t = d.adam_t;
+  c->step = d.step;
+}
+
+// Decide on d (no memory writes): returns true with the trace entry `tr` for
+// slot d.iter (before the update), false when the iteration pauses.
 template <int OPT>
-__device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
-  Ctrl* ctrl = A.ctrl;
+__device__ __forceinline__ bool decide_core(const StepArgs& A, double4 s, int need, DState& d, double2& tr) {
   const double misses = floor(s.w / kMissUnit);
   s.w -= misses * kMissUnit;
-  if (ctrl->need || misses > 0.0) {  // degenerate pairs without directions: pause, redo after the host draw
-    ctrl->status = 2;
-    ctrl->need = 0;
-    ctrl->next_tile = 0;
-    ctrl->arrive = 0;
-    return;
+  if (need || misses > 0.0) {  // degenerate pairs without directions: pause, redo after the host draw
+    d.status = 2;
+    return false;
   }
   const double E = 0.5 * s.x;
-  double step = ctrl->step;
+  double step = d.step;
   bool commit = true;
   if (OPT == OPT_FD && A.h.adapt) {
     const double dT = s.y - s.z;
@@ -408,23 +435,69 @@ __device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
       commit = false;
     }
   }
-  const long long it = ctrl->iter;
-  if (A.trace) A.trace[it] = make_double2(E, step);
+  const long long it = d.iter;
+  tr = make_double2(E, step);
   if (commit && s.w > 0.0) {
-    ctrl->status = 1;
-    ctrl->diverged_at = it;
+    d.status = 1;
+    d.diverged_at = it;
   } else {
-    if (A.fixed_io) ctrl->cur = A.out_index;  // the rollback copy (finalize_kernel) refills it
-    else if (commit) ctrl->cur ^= 1;
-    ctrl->last_commit = commit ? 1 : 0;
-    ctrl->step = step;
-    ctrl->iter = it + 1;
+    if (A.fixed_io) d.cur = A.out_index;  // the rollback copy (finalize_kernel) refills it
+    else if (commit) d.cur ^= 1;
+    d.last_commit = commit ? 1 : 0;
+    d.step = step;
+    d.iter = it + 1;
   }
-  ctrl->gstep += 1;
-  ctrl->scur ^= 1;  // the state written this iteration is current (FD keeps new deltas on rollback)
-  if (OPT == OPT_ADAM) ctrl->adam_t += 1;
+  d.gstep += 1;
+  d.scur ^= 1;  // the state written this iteration is current (FD keeps new deltas on rollback)
+  if (OPT == OPT_ADAM) d.adam_t += 1;
+  return true;
+}
+
+template <int OPT>
+__device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
+  Ctrl* ctrl = A.ctrl;
+  DState d = dstate_load(ctrl);
+  double2 tr;
+  if (decide_core<OPT>(A, s, ctrl->need, d, tr) && A.trace) A.trace[ctrl->iter] = tr;
+  dstate_store(ctrl, d);
+  ctrl->need = 0;
   ctrl->next_tile = 0;
   ctrl->arrive = 0;  // the next launch is ordered after this grid completes
+}
+
+// Deferred decisions: every block adds its partial to the launch's slot in
+// fixed point (2^-24) with integer atomics — order-independent, so the sum is
+// the same bit pattern whatever order the blocks finish in — and the next
+// launch reads the four sums back.  Values beyond the fixed-point range (or
+// non-finite) are flagged and read back as inf / NaN.
+constexpr double kFixScale = 16777216.0;  // 2^24
+__device__ __forceinline__ void fix_add(Ctrl* c, int slot, double4 t) {
+  const double v[4] = {t.x, t.y, t.z, t.w};
+  int nf = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double x = v[q] * kFixScale;
+    if (isnan(x)) {
+      nf |= 2 << (2 * q);
+    } else if (!(fabs(x) < 4.0e18)) {
+      nf |= 1 << (2 * q);
+    } else {
+      atomicAdd(&c->facc[slot][q], (unsigned long long)llrint(x));
+    }
+  }
+  if (nf) atomicOr(&c->fnf[slot], nf);
+}
+__device__ __forceinline__ double4 fix_read(const Ctrl* c, int slot) {
+  double r[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r[q] = (double)(long long)__ldcg(&c->facc[slot][q]) / kFixScale;
+  const int nf = __ldcg(&c->fnf[slot]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // as the fp64 sum of the partials would read (all are >= 0)
+    if ((nf >> (2 * q)) & 2) r[q] = NAN;
+    else if ((nf >> (2 * q)) & 1) r[q] = INFINITY;
+  }
+  return make_double4(r[0], r[1], r[2], r[3]);
 }
 
 // ---------------------------------------------------------------- finalize
@@ -712,7 +785,7 @@ constexpr int kUnitCache = IVHD_UNIT_CACHE;  // unit words cached per block
 // are issued first, then ~20 instructions per entry.  Slots past the lane's
 // last entry are self pairs (zero contribution).
 template <int D, bool GCOL>
-__device__ __forceinline__ void fast_row(const StepArgs& A, const uint32_t* __restrict__ cb, int G, int deg,
+__device__ __forceinline__ void fast_row(const StepArgs& A, int* need, const uint32_t* __restrict__ cb, int G, int deg,
                                          int ebase, const float* __restrict__ Yin, uint32_t v, float y0, float y1,
                                          float c, long long gstep, float (&f)[2], float& e) {
   uint32_t cw[D];
@@ -747,7 +820,7 @@ __device__ __forceinline__ void fast_row(const StepArgs& A, const uint32_t* __re
     // applies them (ivhd_capi.cu resume_degenerate).
 #pragma unroll
     for (int q = 0; q < D; ++q)
-      if ((dmask >> q) & 1u) record_degenerate(A.ctrl, A.miss_n, A.miss, A.miss_cap, v, ebase + q * G);
+      if ((dmask >> q) & 1u) record_degenerate(need, A.miss_n, A.miss, A.miss_cap, v, ebase + q * G);
   }
   f[0] = fx;
   f[1] = fy;
@@ -974,6 +1047,51 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   float te = 0.f, tn = 0.f, to = 0.f, tb = 0.f;
   __shared__ double4 sm_wacc[kConsumerWarps];
   if (tid < kConsumerWarps) sm_wacc[tid] = make_double4(0, 0, 0, 0);
+
+  // deferred decisions (A.defer): consumer warp 0 decides the pending launch's
+  // iteration right after the dependency wait; every warp then reads the
+  // decided state from shared memory.  sm_df: 0 write slot, 1 decided (trace
+  // entry valid), 2 pending slot consumed, 3 its index, 4 stopped before this launch
+  __shared__ DState sm_dec;
+  __shared__ int sm_df[5];
+  __shared__ double2 sm_tr;
+  __shared__ long long sm_trit;
+  auto defer_decide = [&]() {  // one thread
+    DState d = dstate_load(ctrl);
+    const int pend = ctrl->pend, pslot = ctrl->pslot, pre = d.status;
+    int decided = 0;
+    double2 tr = make_double2(0.0, 0.0);
+    const long long trit = d.iter;
+    if (pre == 0 && pend) decided = decide_core<OPT>(A, fix_read(ctrl, pslot), ctrl->needw[pslot], d, tr) ? 1 : 0;
+    if (lane == 0) {
+      sm_dec = d;
+      sm_df[0] = pend ? (pslot ^ 1) : 0;
+      sm_df[1] = decided;
+      sm_df[2] = pend;
+      sm_df[3] = pslot;
+      sm_df[4] = pre != 0;
+      sm_tr = tr;
+      sm_trit = trit;
+    }
+  };
+  // block 0, one thread, after every block of this launch has read the control
+  // block: the decided state, the trace entry, this launch's partials pending
+  auto defer_persist = [&]() {
+    while (*reinterpret_cast<volatile unsigned int*>(&ctrl->readers) < gridDim.x) __nanosleep(32);
+    dstate_store(ctrl, sm_dec);
+    if (sm_df[1] && A.trace) A.trace[sm_trit] = sm_tr;
+    if (sm_df[2]) {  // consumed: free for the launch after next
+      ctrl->needw[sm_df[3]] = 0;
+      ctrl->fnf[sm_df[3]] = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ctrl->facc[sm_df[3]][q] = 0ull;
+    }
+    ctrl->pend = sm_dec.status == 0 ? 1 : 0;
+    ctrl->pslot = sm_df[0];
+    ctrl->readers = 0;
+    ctrl->next_tile = 0;
+    ctrl->arrive = 0;
+  };
   auto flush_partials = [&]() {
     double a = te, b = tn, c2 = to, d = tb;
 #pragma unroll
@@ -1054,11 +1172,14 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       }
       __syncwarp();
       griddep_wait();  // the previous iteration (positions, state, ctrl) is complete
-      if (ctrl->status != 0) {  // diverged earlier: drain the prefetch and leave
+      if (A.defer) block_sync();  // consumer warp 0 has decided the pending iteration
+      const int p_status = A.defer ? sm_dec.status : ctrl->status;
+      if (p_status != 0) {  // diverged / paused: drain the prefetch and leave
         for (int k = 0; k < pre; ++k) mbar_wait(&bar_b[k], 0);
       } else {
-        const float* Yin = (A.fixed_io || !ctrl->cur) ? A.ybuf0 : A.ybuf1;
-        Sin = A.state + (ctrl->scur ? A.sstride : 0);
+        const int p_cur = A.defer ? sm_dec.cur : ctrl->cur, p_scur = A.defer ? sm_dec.scur : ctrl->scur;
+        const float* Yin = (A.fixed_io || !p_cur) ? A.ybuf0 : A.ybuf1;
+        Sin = A.state + (p_scur ? A.sstride : 0);
         if (lane == 0)
           for (int k = 0; k < pre; ++k) issue_ys(k, Yin);
         // Event loop: stages are claimed as consumers free them; a unit's
@@ -1081,12 +1202,24 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
           nc += (ok >> 1) & 1;
         }
       }
-    griddep_wait();
-    if (ctrl->status != 0) return;
+    if (p_status != 0) return;
   } else {
     // ----------------------------------------------------- consumer warps
     griddep_wait();
-    if (ctrl->status != 0) return;  // diverged earlier: later iterations are no-ops
+    if (A.defer) {
+      if (warp == 0 && lane == 0) defer_decide();
+      block_sync();
+      if (sm_dec.status != 0) {  // stopped: before this launch (nothing to do) or by this decision
+        if (!sm_df[4] && warp == 0 && lane == 0) {
+          atomicAdd(&ctrl->readers, 1u);
+          if (blockIdx.x == 0) defer_persist();
+        }
+        return;
+      }
+      if (warp == 0 && lane == 0) atomicAdd(&ctrl->readers, 1u);
+    } else if (ctrl->status != 0) {
+      return;  // diverged earlier: later iterations are no-ops
+    }
 #ifdef IVHD_TIMELINE
     if (A.fuse_finalize && (ctrl->iter == 10 || ctrl->iter == 11) && blockIdx.x < kTlBlocks) {
       tl_rec = g_tl[ctrl->iter - 10][blockIdx.x];
@@ -1094,16 +1227,18 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
     }
     IVHD_TL(1);
 #endif
-    const int ycur = A.fixed_io ? 0 : ctrl->cur;
+    const int ycur = A.fixed_io ? 0 : (A.defer ? sm_dec.cur : ctrl->cur);
     const float c = (float)ctrl->c;
-    const float step = (float)ctrl->step;
-    const long long gstep = ctrl->gstep;
+    const float step = (float)(A.defer ? sm_dec.step : ctrl->step);
+    const long long gstep = A.defer ? sm_dec.gstep : ctrl->gstep;
     const float* __restrict__ Yin = ycur ? A.ybuf1 : A.ybuf0;
     float* __restrict__ Yout = ycur ? A.ybuf0 : A.ybuf1;
-    float* __restrict__ Sout = A.state + (ctrl->scur ? 0 : A.sstride);
+    float* __restrict__ Sout = A.state + ((A.defer ? sm_dec.scur : ctrl->scur) ? 0 : A.sstride);
+    // degenerate pairs without a direction: flagged per partial slot when deferred
+    int* const needp = A.defer ? &ctrl->needw[sm_df[0]] : &ctrl->need;
     float bc1 = 1.f, bc2 = 1.f;  // Adam bias corrections (optim.py:203-204)
     if constexpr (OPT == OPT_ADAM) {
-      const double tt = (double)(ctrl->adam_t + 1);
+      const double tt = (double)((A.defer ? sm_dec.adam_t : ctrl->adam_t) + 1);
       bc1 = (float)(1.0 / (1.0 - pow((double)A.h.gv, tt)));
       bc2 = (float)(1.0 / (1.0 - pow((double)A.h.gs, tt)));
     }
@@ -1156,7 +1291,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
               if (slots <= 8) {
                 switch (slots) {
 #define IVHD_FAST_CASE(D) \
-  case D: fast_row<D, GC>(A, cb, G, nl, lg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
+  case D: fast_row<D, GC>(A, needp, cb, G, nl, lg, Yin, (uint32_t)v, yi[0], yi[1], c, gstep, ff, e); break;
                   IVHD_FAST_CASE(1) IVHD_FAST_CASE(2) IVHD_FAST_CASE(3) IVHD_FAST_CASE(4)
                   IVHD_FAST_CASE(5) IVHD_FAST_CASE(6) IVHD_FAST_CASE(7) IVHD_FAST_CASE(8)
 #undef IVHD_FAST_CASE
@@ -1164,7 +1299,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
                 }
               } else {
                 for (int c0 = 0; c0 < nl; c0 += 8)
-                  fast_row<8, GC>(A, cb + c0 * G, G, nl - c0, lg + c0 * G, Yin, (uint32_t)v, yi[0], yi[1], c,
+                  fast_row<8, GC>(A, needp, cb + c0 * G, G, nl - c0, lg + c0 * G, Yin, (uint32_t)v, yi[0], yi[1], c,
                                   gstep, ff, e);
               }
             };
@@ -1215,7 +1350,7 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
             for (int q = 0; q < kUnroll; ++q) {
               if ((dmask >> q) & 1u) {
                 float uvec[DIM];
-                degenerate_vec<DIM>(A, (uint32_t)v, (int)(k0 + (uint32_t)(q * G) - beg), gstep, uvec);
+                degenerate_vec<DIM>(A, needp, (uint32_t)v, (int)(k0 + (uint32_t)(q * G) - beg), gstep, uvec);
 #pragma unroll
                 for (int d = 0; d < DIM; ++d) f[d] += uvec[d];
               }
@@ -1295,6 +1430,18 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
   if (warp < kConsumerWarps) flush_partials();  // the last (partial) group of units
   block_sync();
   if (warp != 0) return;
+  if (A.defer) {  // the block partial into this launch's slot; the next launch decides
+    if (lane == 0) {
+      double4 t = make_double4(0, 0, 0, 0);
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        t.x += sm_wacc[w].x; t.y += sm_wacc[w].y; t.z += sm_wacc[w].z; t.w += sm_wacc[w].w;
+      }
+      fix_add(ctrl, sm_df[0], t);
+      if (blockIdx.x == 0) defer_persist();
+    }
+    return;
+  }
   // last-block-done: lane 0 publishes the block partial with a release
   // arrival; the block that arrives last (acquire) reduces and decides
   int last = 0;

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kBlock) step_kernel_f64(StepArgs A) {
         for (int d = 0; d < DIM; ++d) yo[d] = Yin[(size_t)o * FL::DP + d];
         if (entry_f64<DIM, NORM>(yi, yo, t_, w, f, e)) {  // forces.py:167-174 (host-drawn direction)
           float u[DIM];
-          degenerate_vec<DIM>(A, (uint32_t)v, (int)(k - beg), gstep, u);
+          degenerate_vec<DIM>(A, &ctrl->need, (uint32_t)v, (int)(k - beg), gstep, u);
 #pragma unroll
           for (int d = 0; d < DIM; ++d) f[d] += (double)u[d];
         }
