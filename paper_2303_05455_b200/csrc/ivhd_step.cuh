@@ -26,9 +26,12 @@
 // positions and optimizer state with cp.async.bulk into a 3-stage ring; the G
 // lanes of a row gather neighbour positions, reduce with a fixed xor
 // butterfly (all lanes get the bit-identical sum) and lane 0 of the group
-// applies the optimizer.  No atomics touch the data; the last block to finish
-// reduces the partials in fixed order and writes the decision (cur buffer, b,
-// trace, status) that the next launch reads.
+// applies the optimizer.  No atomics touch the data.  One GPU: every block
+// adds its partials to four fixed-point sums (integer atomics, order-
+// independent) and the NEXT launch decides this iteration at its start (cur
+// buffer, b, trace, status; Ctrl::pend), block 0 persisting the decided state.
+// Sharded / Adam: the last block to finish reduces the partials in fixed order
+// and writes the decision that the next launch reads.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -174,7 +177,7 @@ struct StepArgs {
   int tile0;              // global index of its first work unit
   int n_tiles_global;     // work-unit partials reduced by the finalizer
   int norm;               // 0 = L2, 1 = L1
-  int fuse_finalize;      // last block reduces + decides (single GPU)
+  int fuse_finalize;      // single GPU: running sums, one partial per block (decided by the last block or deferred)
   int defer;              // fuse_finalize with deferred decisions (Ctrl::pend): the next launch decides
   int fixed_io;           // sharded async mode: read ybuf0, write ybuf1 (host-chosen parity)
   int out_index;          // fixed_io: which context buffer ybuf1 is (becomes ctrl->cur)
