@@ -29,7 +29,8 @@
 // applies the optimizer.  No atomics touch the data.  One GPU: every block
 // adds its partials to four fixed-point sums (integer atomics, order-
 // independent) and the NEXT launch decides this iteration at its start (cur
-// buffer, b, trace, status; Ctrl::pend), block 0 persisting the decided state.
+// buffer, b, trace, status; Ctrl::pend), the last block to read the control
+// block persisting the decided state.
 // Sharded / Adam: the last block to finish reduces the partials in fixed order
 // and writes the decision that the next launch reads.
 #pragma once
@@ -102,7 +103,7 @@ struct Ctrl {
   int dg_n;             // directions in the degenerate-pair table ...
   long long dg_gstep;   // ... valid for this global iteration only
   // deferred decisions (single-GPU loop): launch t+1 decides iteration t from
-  // t's block partials before its own work; block 0 persists the decided state
+  // t's partial sums before its own work; the last block to read persists the decision
   int pend;             // the partial sums in slot `pslot` await their decision
   int pslot;
   int needw[2];         // per slot: a degenerate pair had no direction
@@ -1077,10 +1078,10 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       sm_trit = trit;
     }
   };
-  // block 0, one thread, after every block of this launch has read the control
-  // block: the decided state, the trace entry, this launch's partials pending
+  // the block that reads the control block last (its reader count says every
+  // other block has read it), one thread: the decided state, the trace entry,
+  // this launch's partials pending — no block waits for another
   auto defer_persist = [&]() {
-    while (*reinterpret_cast<volatile unsigned int*>(&ctrl->readers) < gridDim.x) __nanosleep(32);
     dstate_store(ctrl, sm_dec);
     if (sm_df[1] && A.trace) A.trace[sm_trit] = sm_tr;
     if (sm_df[2]) {  // consumed: free for the launch after next
@@ -1213,13 +1214,10 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
       if (warp == 0 && lane == 0) defer_decide();
       block_sync();
       if (sm_dec.status != 0) {  // stopped: before this launch (nothing to do) or by this decision
-        if (!sm_df[4] && warp == 0 && lane == 0) {
-          atomicAdd(&ctrl->readers, 1u);
-          if (blockIdx.x == 0) defer_persist();
-        }
+        if (!sm_df[4] && warp == 0 && lane == 0 && atomicAdd(&ctrl->readers, 1u) == gridDim.x - 1) defer_persist();
         return;
       }
-      if (warp == 0 && lane == 0) atomicAdd(&ctrl->readers, 1u);
+      if (warp == 0 && lane == 0 && atomicAdd(&ctrl->readers, 1u) == gridDim.x - 1) defer_persist();
     } else if (ctrl->status != 0) {
       return;  // diverged earlier: later iterations are no-ops
     }
@@ -1441,7 +1439,6 @@ __global__ void __launch_bounds__(kThreads, step_min_blocks<DIM, OPT, WEIGHTED, 
         t.x += sm_wacc[w].x; t.y += sm_wacc[w].y; t.z += sm_wacc[w].z; t.w += sm_wacc[w].w;
       }
       fix_add(ctrl, sm_df[0], t);
-      if (blockIdx.x == 0) defer_persist();
     }
     return;
   }
