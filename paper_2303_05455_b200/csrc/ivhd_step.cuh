@@ -109,7 +109,7 @@ struct Ctrl {
   int needw[2];         // per slot: a degenerate pair had no direction
   unsigned int readers; // blocks of this launch that have read the control block
   int fnf[2];           // per slot: bit 2q component q was +-inf / out of range, bit 2q+1 NaN
-  unsigned long long facc[2][4];  // per slot: the launch's partials in fixed point (2^-24), summed by atomics
+  unsigned long long facc[2][4];  // per slot: the launch's partials in fixed point (2^-20), summed by atomics
 };
 
 constexpr int kMaxPeers = 7;  // up to 8 ranks (one node)
@@ -470,11 +470,13 @@ __device__ __forceinline__ void decide(const StepArgs& A, double4 s) {
 }
 
 // Deferred decisions: every block adds its partial to the launch's slot in
-// fixed point (2^-24) with integer atomics — order-independent, so the sum is
+// fixed point (2^-20) with integer atomics — order-independent, so the sum is
 // the same bit pattern whatever order the blocks finish in — and the next
-// launch reads the four sums back.  Values beyond the fixed-point range (or
-// non-finite) are flagged and read back as inf / NaN.
-constexpr double kFixScale = 16777216.0;  // 2^24
+// launch reads the four sums back.  A block partial beyond 2^63 / 2^11 (so that
+// the sum of up to 2048 blocks cannot wrap) or non-finite is flagged and read
+// back as inf / NaN.
+constexpr double kFixScale = 1048576.0;  // 2^20: per-block rounding <= 5e-7
+constexpr double kFixMax = 4.5e15;       // ~2^63 / 2048
 __device__ __forceinline__ void fix_add(Ctrl* c, int slot, double4 t) {
   const double v[4] = {t.x, t.y, t.z, t.w};
   int nf = 0;
@@ -483,7 +485,7 @@ __device__ __forceinline__ void fix_add(Ctrl* c, int slot, double4 t) {
     const double x = v[q] * kFixScale;
     if (isnan(x)) {
       nf |= 2 << (2 * q);
-    } else if (!(fabs(x) < 4.0e18)) {
+    } else if (!(fabs(x) < kFixMax)) {
       nf |= 1 << (2 * q);
     } else {
       atomicAdd(&c->facc[slot][q], (unsigned long long)llrint(x));
