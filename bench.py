@@ -557,7 +557,9 @@ def gpu_arm(args, w):
                                  "per iteration incl. inter-launch gaps; peak = MEASURED_PEAKS.json hbm_gbs"},
             "gather_floor": gfloor,
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * iters * dev_launches, "clocks": clk.summary(), "nvlink": nvlink,
+            # per step: one step-kernel launch per iteration, plus (one GPU) the
+            # launch that decides the run's last iteration (deferred decisions)
+            "gpu_launches": args.steps * (iters * dev_launches + (0 if sharded else 1)), "clocks": clk.summary(), "nvlink": nvlink,
             "final_stress_e2e": final_stress,
             "knn": knn, "quality": quality,
         }
