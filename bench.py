@@ -559,7 +559,8 @@ def gpu_arm(args, w):
             "cpu_baseline": cpu, "e2e": e2e,
             # per step: one step-kernel launch per iteration, plus (one GPU) the
             # launch that decides the run's last iteration (deferred decisions)
-            "gpu_launches": args.steps * (iters * dev_launches + (0 if sharded else 1)), "clocks": clk.summary(), "nvlink": nvlink,
+            "gpu_launches": args.steps * (iters * dev_launches + (0 if sharded else 1)),
+            "clocks": clk.summary(), "nvlink": nvlink,
             "final_stress_e2e": final_stress,
             "knn": knn, "quality": quality,
         }
